@@ -1,0 +1,35 @@
+"""ORACLE — test infrastructure, not product code.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import anything under ``oracle/``.  It shares no
+code with ``paper_1507_06078_b200`` (the CUDA path) and never imports it; the
+only shared module is ``synth`` (seeded inputs, no method arithmetic).
+
+A plain, slow, fp64 CPU implementation of what the hot path computes, written
+from arXiv 1507.06078 (PAPER.md = P):
+
+* sparse part in plain C (``csr_oracle.c``: SpMM, Chebyshev filter, column
+  norms), loaded with ctypes;
+* dense part with numpy/scipy library primitives (pivoted Householder QR,
+  symmetric eig) used as single steps of the paper's algorithms.
+
+Every function cites the passage it follows.  The pins that tie it to the
+paper and to mathematics (not to itself) are in ``tests/test_oracle_*.py``.
+Functions without such a pin are marked "parity unpinned" — currently none.
+"""
+from .core import (  # noqa: F401
+    load_lib,
+    spmm,
+    cheb_filter,
+    col_norms,
+    mpm_sweep,
+    gershgorin_lower,
+    chebyshev_T,
+    orthonormalize,
+    rayleigh_ritz,
+    arr,
+    residuals,
+    sweeps_rule,
+    solve,
+    SolveResult,
+)

@@ -1,0 +1,269 @@
+"""ORACLE — test infrastructure only (see oracle/__init__.py).
+
+Plain fp64 CPU implementation of the ARRABIT-MPM hot path, arXiv 1507.06078
+(P = /root/reference/PAPER.md line numbers; readings in DESIGN.md §4).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "csr_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+def build_lib(force: bool = False) -> str:
+    """Compile csr_oracle.c -> liboracle.so (plain gcc, -O2, OpenMP, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def load_lib():
+    global _lib
+    if _lib is None:
+        build_lib()
+        lib = ctypes.CDLL(_LIB)
+        lib.orc_spmm.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i32p, _f64p,
+                                 _f64p, ctypes.c_int64, _f64p, ctypes.c_int64]
+        lib.orc_spmm.restype = None
+        lib.orc_cheb_filter.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i32p, _f64p,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                        _f64p, ctypes.c_int64, _f64p, ctypes.c_int64]
+        lib.orc_cheb_filter.restype = ctypes.c_int
+        lib.orc_col_norms.argtypes = [ctypes.c_int64, ctypes.c_int64, _f64p, ctypes.c_int64, _f64p]
+        lib.orc_col_norms.restype = None
+        _lib = lib
+    return _lib
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _csr_args(A):
+    rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(A.col_idx, dtype=np.int32)
+    va = np.ascontiguousarray(A.val, dtype=np.float64)
+    return rp, ci, va
+
+
+# --------------------------------------------------------------------------- sparse
+def spmm(A, X: np.ndarray) -> np.ndarray:
+    """Y = A X (plain CSR row loop in C).  P:1527-1528: A enters only through AX."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        return spmm(A, X[:, None])[:, 0]
+    n, w = X.shape
+    if n != A.n:
+        raise ValueError("dimension mismatch")
+    Y = np.empty_like(X)
+    rp, ci, va = _csr_args(A)
+    load_lib().orc_spmm(n, w, _p(rp, _i64p), _p(ci, _i32p), _p(va, _f64p),
+                        _p(X, _f64p), w, _p(Y, _f64p), w)
+    return Y
+
+
+def cheb_filter(A, a: float, b: float, d: int, X: np.ndarray) -> np.ndarray:
+    """Y = T_d((A - cI)/e) X, c=(a+b)/2, e=(b-a)/2 (Eq. cheby-poly P:377-383 on the
+    affine map of Eq. rhod; reading DESIGN.md §4 R1/R2)."""
+    if not a < b:
+        raise ValueError("need a < b")
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n, w = X.shape
+    Y = np.empty_like(X)
+    rp, ci, va = _csr_args(A)
+    rc = load_lib().orc_cheb_filter(n, w, _p(rp, _i64p), _p(ci, _i32p), _p(va, _f64p),
+                                    float(a), float(b), int(d), _p(X, _f64p), w, _p(Y, _f64p), w)
+    if rc != 0:
+        raise RuntimeError(f"orc_cheb_filter failed ({rc})")
+    return Y
+
+
+def col_norms(X: np.ndarray) -> np.ndarray:
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n, w = X.shape
+    out = np.empty(w)
+    load_lib().orc_col_norms(n, w, _p(X, _f64p), w, _p(out, _f64p))
+    return out
+
+
+def mpm_sweep(A, a: float, b: float, d: int, X: np.ndarray) -> np.ndarray:
+    """One multi-power sweep: x_i <- rho(A) x_i, x_i <- x_i/||x_i||_2 for every
+    column, no orthogonalisation (Alg. Arrabit2)."""
+    Y = cheb_filter(A, a, b, d, X)
+    nrm = col_norms(Y)
+    if np.any(nrm == 0) or not np.all(np.isfinite(nrm)):
+        raise FloatingPointError("zero or non-finite column after filtering")
+    return Y / nrm
+
+
+def gershgorin_lower(A) -> float:
+    """a = min_i (A_ii - sum_{j != i} |A_ij|): a lower bound of lambda_n, used
+    in place of the paper's eigs call (reading DESIGN.md §4 R3)."""
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    diag = np.zeros(A.n)
+    off = np.zeros(A.n)
+    isd = A.col_idx == rows
+    np.add.at(diag, rows[isd], A.val[isd])
+    np.add.at(off, rows[~isd], np.abs(A.val[~isd]))
+    return float(np.min(diag - off))
+
+
+def chebyshev_T(d: int, t):
+    """rho_d(t) by the three-term recursion rho_{d+1} = 2 t rho_d - rho_{d-1},
+    rho_0 = 1, rho_1 = t (Eq. cheby-poly)."""
+    t = np.asarray(t, dtype=np.float64)
+    r0 = np.ones_like(t)
+    if d == 0:
+        return r0
+    r1 = t.copy()
+    for _ in range(1, d):
+        r0, r1 = r1, 2.0 * t * r1 - r0
+    return r1
+
+
+# --------------------------------------------------------------------------- dense
+def orthonormalize(Z: np.ndarray):
+    """U in orth(Z) (Alg. RR step 1): equilibrate columns (span unchanged),
+    Householder QR with column pivoting (library step), keep
+    r = #{i : |R_ii| > n*eps*|R_11|} columns (reading DESIGN.md §4 R8)."""
+    Z = np.asarray(Z, dtype=np.float64)
+    n, m = Z.shape
+    nrm = np.linalg.norm(Z, axis=0)
+    keep = nrm > 0
+    Zs = Z[:, keep] / nrm[keep]
+    if Zs.shape[1] == 0:
+        return np.zeros((n, 0)), 0
+    Q, R, _ = scipy.linalg.qr(Zs, mode="economic", pivoting=True)
+    dR = np.abs(np.diag(R))
+    r = int(np.sum(dR > n * np.finfo(float).eps * dR[0]))
+    return Q[:, :r], r
+
+
+def rayleigh_ritz(A, Z: np.ndarray):
+    """(Y, Sigma) = RR(A, Z), Alg. RR: U = orth(Z); H = U^T A U;
+    H = V^T Sigma V; Y = U V.  Ritz values sorted descending."""
+    U, r = orthonormalize(Z)
+    AU = spmm(A, U) if r > 0 else np.zeros_like(U)
+    H = U.T @ AU
+    H = 0.5 * (H + H.T)
+    mu, V = np.linalg.eigh(H)
+    order = np.argsort(-mu, kind="stable")
+    mu = mu[order]
+    V = V[:, order]
+    return mu, U @ V, r
+
+
+def arr(A, X: np.ndarray, p: int, keep: int | None = None, rng_seed: int = 12345):
+    """(Y, Sigma) = ARR(A, X, p), Alg. ARR: Z = [X, AX, ..., A^p X]
+    (plain A, Eq. S:ARR P:515-523), RR(A, Z), keep the leading pairs.
+    Returns (mu_all_descending, Y_keep, rank).  If the rank r < keep the block
+    is topped up with seeded Gaussian columns orthonormalised against Y
+    (reading DESIGN.md §4 R7; never triggered in the pinned cases)."""
+    n, w = X.shape
+    keep = w if keep is None else keep
+    if (p + 1) * w >= n:
+        raise ValueError("(p+1)k must be < n (Alg. ARR input, P:536)")
+    blocks = [np.asarray(X, dtype=np.float64)]
+    for _ in range(p):
+        blocks.append(spmm(A, blocks[-1]))
+    Z = np.hstack(blocks)
+    mu, Y, r = rayleigh_ritz(A, Z)
+    if r >= keep:
+        return mu, Y[:, :keep], r
+    rng = np.random.default_rng(rng_seed)
+    extra = rng.standard_normal((n, keep - r))
+    extra -= Y @ (Y.T @ extra)
+    Q, _ = np.linalg.qr(extra)
+    return mu, np.hstack([Y, Q]), r
+
+
+def residuals(A, Y: np.ndarray, mu: np.ndarray) -> np.ndarray:
+    """res_i = ||A y_i - mu_i y_i||_2 / max(1, |mu_i|)  (Eq. resi)."""
+    AY = spmm(A, Y)
+    R = AY - Y * mu[None, :]
+    return col_norms(R) / np.maximum(1.0, np.abs(mu))
+
+
+def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int) -> int:
+    """Sweeps between ARR steps (DESIGN.md §4 R6, the dynamic-range rule that
+    replaces the paper's rcond inner stop P:1355-1388): amp = |T_d((mu_1-c)/e)|,
+    s = s_max if amp <= 1 else clamp(floor(8/log10(amp)), 1, s_max)."""
+    c = 0.5 * (a + b)
+    e = 0.5 * (b - a)
+    amp = abs(float(chebyshev_T(d, (mu1 - c) / e)))
+    if not amp > 1.0:
+        return s_max
+    if not math.isfinite(amp):
+        return 1
+    return int(min(max(math.floor(8.0 / math.log10(amp)), 1), s_max))
+
+
+@dataclass
+class SolveResult:
+    mu: np.ndarray
+    Y: np.ndarray
+    res: np.ndarray
+    converged: bool
+    outer: int
+    sweeps: int
+    log: list = field(default_factory=list)
+
+
+def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
+          s_max: int = 5, w: int | None = None, max_outer: int | None = None) -> SolveResult:
+    """Fixed-parameter ARRABIT-MPM (Alg. Arrabit2, with the
+    adaptive lines disabled; DESIGN.md §4 R3/R6/R10):
+
+        a := Gershgorin lower bound;  U0 := orth(X0); mu := eig(U0^T A U0); b := mu_w
+        loop: s := sweeps_rule(mu_1);  s x { X := T_d((A-cI)/e) X; normalise }
+              (mu, Y) := ARR(A, X, p)
+              res_i, i <= k  (Eq. resi)  ;  stop if max res <= tol              (Eq. out-stop)
+              b := mu_{w+1};  X := Y[:, :w]
+    """
+    n = A.n
+    w = k if w is None else w
+    X = np.array(X0[:, :w], dtype=np.float64, copy=True)
+    a = gershgorin_lower(A)
+    mu0, _, _ = rayleigh_ritz(A, X)
+    b = float(mu0[w - 1])
+    if not a < b:
+        a = b - 1e-8 * (abs(b) + 1.0)
+    mu1 = float(mu0[0])
+    log = []
+    sweeps = 0
+    limit = maxit if max_outer is None else min(maxit, max_outer)
+    mu = mu0
+    Y = X
+    res = np.full(k, np.inf)
+    for outer in range(1, limit + 1):
+        s = sweeps_rule(mu1, a, b, d, s_max)
+        for _ in range(s):
+            X = mpm_sweep(A, a, b, d, X)
+        sweeps += s
+        mu, Y, r = arr(A, X, p, keep=w)
+        res = residuals(A, Y[:, :k], mu[:k])
+        maxres = float(np.max(res))
+        log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres))
+        if maxres <= tol:
+            return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log)
+        b = float(mu[min(w, r - 1)])
+        if not a < b:
+            a = b - 1e-8 * (abs(b) + 1.0)
+        mu1 = float(mu[0])
+        X = Y[:, :w]
+    return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, False, limit, sweeps, log)

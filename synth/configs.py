@@ -1,0 +1,77 @@
+"""The five BASELINE.json configs (verbatim) and small analogues.
+
+A ConfigSpec only names sizes, seeds and solver parameters; ``build_config``
+returns the CSR matrix from ``generators``.  The starting block is
+``generators.gaussian_block(n, w, seed)`` (or row slices of it).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import generators as g
+
+
+@dataclass(frozen=True)
+class ConfigSpec:
+    name: str
+    kind: str            # lap1d | lap2d | lap3dV | zipf | st27
+    size: int            # n (1-D, zipf) or grid edge N
+    k: int
+    d: int
+    p: int
+    seed: int
+    tol: float = 1e-10
+    maxit: int = 300
+    s_max: int = 5
+    gpus: str = "1"
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        if self.kind in ("lap1d", "zipf"):
+            return self.size
+        if self.kind == "lap2d":
+            return self.size ** 2
+        return self.size ** 3
+
+    @property
+    def w(self) -> int:
+        # block width w = k (guard vectors are NEXT)
+        return self.k
+
+
+CONFIGS = {
+    1: ConfigSpec("cfg1_lap1d_n2000", "lap1d", 2000, k=20, d=10, p=1, seed=0),
+    2: ConfigSpec("cfg2_lap2d_300x300", "lap2d", 300, k=200, d=20, p=1, seed=1),
+    3: ConfigSpec("cfg3_lap3d_100^3_plusV", "lap3dV", 100, k=500, d=20, p=2, seed=2, gpus="1/2/4/8"),
+    4: ConfigSpec("cfg4_zipf_n4e6", "zipf", 4_000_000, k=1000, d=15, p=1, seed=3, gpus="1/2/4/8"),
+    5: ConfigSpec("cfg5_st27_256^3", "st27", 256, k=256, d=30, p=2, seed=4, gpus="1/2/4/8"),
+}
+
+# Small analogues of every config generator (oracle-solvable in seconds).
+SMALL_ANALOGS = {
+    "lap1d": ConfigSpec("small_lap1d_n300", "lap1d", 300, k=8, d=10, p=1, seed=0),
+    "lap2d": ConfigSpec("small_lap2d_24x24", "lap2d", 24, k=16, d=12, p=1, seed=1),
+    "lap3dV": ConfigSpec("small_lap3dV_9^3", "lap3dV", 9, k=12, d=10, p=2, seed=2),
+    "zipf": ConfigSpec("small_zipf_n1500", "zipf", 1500, k=16, d=15, p=1, seed=3),
+    "st27": ConfigSpec("small_st27_8^3", "st27", 8, k=12, d=12, p=2, seed=4),
+}
+
+
+def build_matrix(kind: str, size: int, seed: int) -> g.CSR:
+    if kind == "lap1d":
+        return g.laplacian_1d(size)
+    if kind == "lap2d":
+        return g.laplacian_2d(size)
+    if kind == "lap3dV":
+        return g.laplacian_3d_potential(size, seed)
+    if kind == "zipf":
+        return g.zipf_random(size, seed)
+    if kind == "st27":
+        return g.stencil27_3d(size)
+    raise ValueError(kind)
+
+
+def build_config(spec_or_id) -> tuple[g.CSR, ConfigSpec]:
+    spec = CONFIGS[spec_or_id] if isinstance(spec_or_id, int) else spec_or_id
+    return build_matrix(spec.kind, spec.size, spec.seed), spec

@@ -1,0 +1,70 @@
+"""Oracle pins for the full fixed-parameter ARRABIT-MPM iteration (SURVEY.md
+§8c-3): converged eigenvalues against closed-form spectra, Weyl bounds and a
+dense numpy eigensolve; every residual <= tol (Eq. out-stop)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import configs
+
+
+def _check(res, ref, k, tol=1e-10):
+    assert res.converged
+    assert np.all(res.res <= tol)
+    rel = np.abs(res.mu - ref[:k]) / np.maximum(1, np.abs(ref[:k]))
+    assert rel.max() < 1e-10, rel.max()
+    # partial-trace monitor
+    assert abs(res.mu.sum() - ref[:k].sum()) < 1e-9 * abs(ref[:k].sum())
+
+
+def test_solve_cfg1_closed_form():
+    A, spec = configs.build_config(1)
+    X0 = synth.gaussian_block(A.n, spec.w, spec.seed)
+    r = oracle.solve(A, spec.k, spec.d, spec.p, X0, tol=spec.tol)
+    n = A.n
+    lam = np.sort(2 - 2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1)))[::-1]
+    _check(r, lam, spec.k)
+    # survey's closed-form partial trace
+    assert r.mu.sum() == pytest.approx(79.99292600087112, rel=1e-13)
+
+
+def test_solve_small_lap2d_closed_form():
+    spec = configs.SMALL_ANALOGS["lap2d"]
+    A, _ = configs.build_config(spec)
+    N = spec.size
+    c = 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
+    lam = np.sort((4 - c[:, None] - c[None, :]).ravel())[::-1]
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    _check(r, lam, spec.k)
+
+
+def test_solve_small_st27_closed_form():
+    spec = configs.SMALL_ANALOGS["st27"]
+    A, _ = configs.build_config(spec)
+    N = spec.size
+    t = 1 + 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
+    lam = np.sort((27 - t[:, None, None] * t[None, :, None] * t[None, None, :]).ravel())[::-1]
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    _check(r, lam, spec.k)
+
+
+def test_solve_small_lap3d_potential_weyl_and_dense():
+    spec = configs.SMALL_ANALOGS["lap3dV"]
+    A, _ = configs.build_config(spec)
+    N = spec.size
+    c = 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
+    L = np.sort((6 - c[:, None, None] - c[None, :, None] - c[None, None, :]).ravel())[::-1]
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1]
+    _check(r, lam, spec.k)
+    # Weyl: lambda_i(L) <= lambda_i(L+V) <= lambda_i(L) + max V
+    assert np.all(r.mu >= L[:spec.k] - 1e-12) and np.all(r.mu <= L[:spec.k] + 1 + 1e-12)
+
+
+def test_solve_small_zipf_dense():
+    spec = configs.SMALL_ANALOGS["zipf"]
+    A, _ = configs.build_config(spec)
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1]
+    _check(r, lam, spec.k)
