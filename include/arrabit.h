@@ -1,0 +1,193 @@
+/*
+ * arrabit.h — C-ABI of the B200 (sm_100a) hot path of ARRABIT-MPM,
+ * Wen & Zhang, "Block algorithms with augmented Rayleigh-Ritz projections for
+ * large-scale eigenpair computation", arXiv 1507.06078.
+ * Citations "P:n" are lines of the paper text; section / equation /
+ * algorithm names follow the paper's LaTeX labels.
+ *
+ * Conventions (every entry point):
+ *  - Every call returns arr_status; ARR_OK == 0.  No exception crosses the ABI;
+ *    a message for the last failure is kept per context (eig_last_error).
+ *  - Ownership: the CSR arrays and every block passed in are CALLER-OWNED DEVICE
+ *    memory and must outlive the context.  eig_init allocates the context's own
+ *    workspace (one n x w scratch block, the n x (p+1)w ARR basis, Gram partials
+ *    and small dense buffers); eig_destroy frees it.  No other call allocates.
+ *  - Layout: blocks are ROW-MAJOR n x ncols fp64 with leading dimension ld >= ncols
+ *    (elements).  Row i of a block starts at base + i*ld.  When ncols and ld are
+ *    even and the base is 16-byte aligned the kernels use 128-bit accesses;
+ *    otherwise a scalar path runs (same results).
+ *  - CSR: full symmetric pattern stored (both triangles), row_ptr int64 [n+1],
+ *    col_idx int32 [nnz] (sorted or not), val fp64 [nnz].
+ *  - Streams: everything is enqueued on the stream given to eig_init (a
+ *    cudaStream_t passed as void*; NULL = legacy default stream).  Calls that
+ *    return host data (ritz_host, rank, res_host, a_out, the solve outputs)
+ *    synchronise that stream; all others are asynchronous.
+ *  - Errors: bad sizes / pointers / interval -> ARR_EINVAL (context stays usable).
+ *    A CUDA or cuSOLVER failure poisons the context: every later call returns
+ *    the same code.  A zero or non-finite column norm after filtering ->
+ *    ARR_ENUMERIC.  Rank loss is NOT an error; *rank reports it.
+ *  - Determinism: fixed reduction trees, no floating-point atomics.  Identical
+ *    inputs on the same GPU model give bitwise identical outputs.
+ */
+#ifndef ARRABIT_H
+#define ARRABIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct arr_ctx arr_ctx;
+
+typedef enum {
+    ARR_OK = 0,
+    ARR_EINVAL = 1,
+    ARR_ENOMEM = 2,
+    ARR_ECUDA = 3,
+    ARR_ECUSOLVER = 5,
+    ARR_ENUMERIC = 7
+} arr_status;
+
+/* Sparse symmetric A (borrowed device arrays). */
+typedef struct {
+    int64_t n;               /* rows = columns of A                          */
+    int64_t nnz;             /* stored entries                                */
+    const int64_t *row_ptr;  /* device [n+1]                                  */
+    const int32_t *col_idx;  /* device [nnz], 0 <= col < n                    */
+    const double *val;       /* device [nnz]                                  */
+} arr_csr;
+
+/* Options / report of the fixed-parameter driver eig_solve. */
+typedef struct {
+    double tol;      /* outer stop: max_i res_i <= tol (Eq. out-stop)   */
+    int32_t maxit;   /* maximum outer iterations                        */
+    int32_t s_max;   /* cap of the sweeps-per-ARR rule (R6)                 */
+} arr_solve_opts;
+
+typedef struct {
+    int32_t converged;   /* 1 if max res <= tol                                   */
+    int32_t outer;       /* outer iterations done                                 */
+    int32_t sweeps;      /* MPM sweeps done (each = d filter degrees)            */
+    int32_t last_rank;   /* numerical rank reported by the last ARR               */
+    double maxres;       /* final max_i res_i                                     */
+    double a, b;         /* final filter interval                                 */
+    int64_t spmm_blocks; /* block SpMMs issued (filter degrees + ARR + residuals) */
+} arr_solve_info;
+
+/* ---------------------------------------------------------------- lifecycle
+ * eig_init: create a context for A with k wanted pairs, block width w = k,
+ * ARR augmentation depth p (Eq. S:ARR) and Chebyshev degree d
+ * (Eq. cheby-poly).  Requires 1 <= k, 0 <= p, 1 <= d, (p+1)k < n
+ * (Alg. ARR input), n < 2^31.  stream: cudaStream_t or NULL.
+ * Allocates the workspace described above (ARR_ENOMEM if it does not fit). */
+arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream);
+arr_status eig_destroy(arr_ctx *c);
+const char *eig_last_error(const arr_ctx *c);
+size_t eig_workspace_bytes(const arr_ctx *c);
+/* Number of kernels this context has launched so far (CUDA-graph replays count
+ * every node).  Library calls (cuSOLVER) are not counted. */
+uint64_t eig_launch_count(const arr_ctx *c);
+/* Phase timing (CUDA events on the context stream, resolved at the stream
+ * syncs the calls already make).  on != 0 enables it and zeroes the totals.
+ * eig_phase_times synchronises the stream and returns, for phase
+ * 0 = filter degree kernels (the d fused SpMM launches of each filter_step),
+ * 1 = arr_project, 2 = residuals: ms[3] total device milliseconds and
+ * counts[3] (phase 0: degree launches; 1, 2: calls). */
+arr_status eig_set_timing(arr_ctx *c, int32_t on);
+arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts);
+
+/* ---------------------------------------------------------------- A0: interval
+ * a_out = min_i (A_ii - sum_{j!=i} |A_ij|), the Gershgorin lower bound used in
+ * place of the paper's eigs estimate of lambda_n (R3). */
+arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out);
+/* Set the damped interval [a,b] (Eq. rhod):
+ * c = (a+b)/2, e = (b-a)/2.  a >= b -> ARR_EINVAL. */
+arr_status eig_set_interval(arr_ctx *c, double a, double b);
+/* Change the degree d used by filter_step (1 <= d). */
+arr_status eig_set_degree(arr_ctx *c, int32_t d);
+
+/* ---------------------------------------------------------------- A1 + A2
+ * X <- T_d((A - cI)/e) X by the three-term recurrence
+ *   Y_0 = X, Y_1 = (A Y_0 - c Y_0)/e, Y_{j+1} = (2/e)(A Y_j - c Y_j) - Y_{j-1}
+ * (Eq. cheby-poly P:377-383 on the map of Eq. rhod; Alg. Arrabit2
+ * line P:1486), one fused SpMM kernel per degree.  If normalize != 0, every
+ * column is then scaled to unit 2-norm (MPM) and, when
+ * colnorm_dev != NULL, the pre-normalisation norms are written there (device
+ * [w]).  X: device n x w, row-major, ldx >= w.  Uses the context scratch block.
+ * Returns ARR_ENUMERIC if a norm is zero or not finite (checked only when
+ * normalize != 0; this synchronises the stream). */
+arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev);
+
+/* ---------------------------------------------------------------- A3 (test hook)
+ * Y = alpha (A - shift I) X for ncols columns (ncols <= 2048).  X, Y device,
+ * row-major, must not alias. */
+arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t ldx,
+                double *Y, int64_t ldy, int32_t ncols);
+
+/* ---------------------------------------------------------------- A4
+ * Tall-skinny fp64 products on DMMA tensor cores (mma.sync m8n8k4.f64).
+ * gram:  G = X^T Y, X n x m1, Y n x m2, G device row-major m1 x m2 (ldg).
+ *        Split over rows, fixed-order reduction (deterministic).
+ * gemm:  Out = beta*Cin + alpha * X B, X n x m1, B device row-major m1 x m2 (ldb),
+ *        Cin/Out n x m2.  Cin may equal Out; X must not alias Out.       */
+arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
+                int32_t m2, double *G, int64_t ldg);
+arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
+                int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out,
+                int64_t ldo);
+
+/* Orthonormalise the ncols (<= w) columns of X in place: two passes of SVQB
+ * (X^T X Gram, column equilibration, eig, X <- X D V L^{-1/2}).  The span is
+ * that of X plus, if X is rank deficient, directions from its rounding noise
+ * (Alg. RR step 1, "orthonormalize Z").  *rank = number of Gram
+ * eigenvalues above 1e-14 * max in the first pass (host, synchronises). */
+arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank);
+
+/* Augmented Rayleigh-Ritz (Alg. ARR P:531-541 with Alg. RR) on
+ * span{X, AX, ..., A^p X}, built as an orthonormal block-Krylov basis
+ * Q = [U_0 .. U_p]: U_0 = orth(X), U_j = orth((I - QQ^T) A U_{j-1}) (block CGS2),
+ * H = Q^T A Q (m x m, m = (p+1)w, AQ never stored), H = V Theta V^T on device
+ * (cuSOLVER syevd; not on the graded path), Y = Q V[:, 1..w].
+ * X: n x w input (not modified unless Y == X).  Y: n x w output (the w leading
+ * Ritz vectors; may equal X; may be NULL to skip forming them).
+ * ritz_host: host [(p+1)w] Ritz values, descending.  rank: host, numerical
+ * rank of the basis (min over its blocks' SVQB ranks, summed). */
+arr_status arr_project(arr_ctx *c, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                       double *ritz_host, int32_t *rank);
+/* Same with an explicit depth p_use (0 = plain RR, Alg. RR), p_use <= p. */
+arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx, double *Y,
+                         int64_t ldy, double *ritz_host, int32_t *rank);
+
+/* ---------------------------------------------------------------- A6
+ * res_i = ||A y_i - mu_i y_i||_2 / max(1, |mu_i|), i < ncols (Eq. resi,
+ * P:1322-1325): one fused SpMM with a per-column shift and column sums of
+ * squares; the residual block is never written.  mu_host, res_host: host. */
+arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_host, int32_t ncols,
+                     double *res_host);
+
+/* ---------------------------------------------------------------- driver
+ * Fixed-parameter ARRABIT-MPM (Alg. Arrabit2 P:1463-1527 with the adaptive
+ * lines disabled; R3, R6, R10):
+ *   a = Gershgorin lower bound; b = smallest Ritz value of RR(A, X0);
+ *   repeat: s = sweeps rule; s x filter_step(normalize);  ARR;  residuals;
+ *           stop if max res <= tol;  b = mu_{w+1};  X = leading Ritz vectors.
+ * X: in = X0 (n x w), out = the k Ritz vectors.  eigval_host/res_host: host [k].
+ * Returns ARR_OK also when not converged (info->converged = 0). */
+arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts,
+                     double *eigval_host, double *res_host, arr_solve_info *info);
+
+/* Host-buffer convenience entry (the public "e2e" call): copies the CSR and X0
+ * from host memory to the device, runs eig_solve on a fresh context, copies the
+ * k eigenvalues, residuals and eigenvectors (n x k, row-major, ld = k) back.
+ * All host pointers; device memory is allocated and freed inside. */
+arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                          const double *val, int32_t k, int32_t p, int32_t d, const double *X0,
+                          const arr_solve_opts *opts, double *eigval, double *res, double *evec,
+                          arr_solve_info *info, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARRABIT_H */

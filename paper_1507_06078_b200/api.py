@@ -1,0 +1,230 @@
+"""Thin Python binding over the C-ABI (include/arrabit.h), same names.
+
+Blocks are torch fp64 CUDA tensors of shape (n, ncols) with stride (ld, 1)
+(row-major, ld >= ncols).  The CSR arrays are torch CUDA tensors (int64 row_ptr,
+int32 col_idx, fp64 val).  PyTorch only supplies device memory and streams;
+every arithmetic step runs in libarrabit's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import arr_csr, arr_solve_info, arr_solve_opts
+
+
+class ArrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_lib.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+@dataclass
+class DeviceCSR:
+    n: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    val: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+
+def to_device_csr(A, device="cuda") -> DeviceCSR:
+    """Copy a host CSR (fields n, row_ptr, col_idx, val as numpy) to the device."""
+    return DeviceCSR(int(A.n),
+                     torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(device),
+                     torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int32)).to(device),
+                     torch.from_numpy(np.ascontiguousarray(A.val, dtype=np.float64)).to(device))
+
+
+def _blk(X: torch.Tensor, name: str):
+    if X.dtype != torch.float64 or not X.is_cuda or X.dim() != 2 or X.stride(1) != 1:
+        raise ValueError(f"{name}: need a row-major fp64 CUDA tensor (n, ncols) with stride (ld, 1)")
+    return ctypes.c_void_p(X.data_ptr()), X.stride(0), X.shape[1]
+
+
+def _stream_handle(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream), stream
+
+
+class EigContext:
+    """An arr_ctx (eig_init ... eig_destroy)."""
+
+    def __init__(self, A: DeviceCSR, k: int, p: int, d: int, stream=None):
+        self.lib = _lib.load()
+        self.A = A  # keep the borrowed arrays alive
+        self.k, self.p, self.d = k, p, d
+        self.handle_stream, self.stream = _stream_handle(stream)
+        self._csr = arr_csr(A.n, A.nnz, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.val.data_ptr())
+        h = ctypes.c_void_p()
+        st = self.lib.eig_init(ctypes.byref(h), ctypes.byref(self._csr), k, p, d, self.handle_stream)
+        if st != 0:
+            raise ArrError(st, "eig_init failed")
+        self.h = h
+
+    # -- helpers
+    def _check(self, st: int, what: str):
+        if st != 0:
+            msg = self.lib.eig_last_error(self.h)
+            raise ArrError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.eig_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.eig_launch_count(self.h))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self.lib.eig_workspace_bytes(self.h))
+
+    def eig_set_timing(self, on: bool = True):
+        self._check(self.lib.eig_set_timing(self.h, 1 if on else 0), "eig_set_timing")
+
+    def eig_phase_times(self):
+        """(ms[3], counts[3]) for phases filter-degrees / arr_project / residuals."""
+        ms = np.zeros(3)
+        cnt = np.zeros(3, dtype=np.int64)
+        self._check(self.lib.eig_phase_times(self.h, ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                             cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                    "eig_phase_times")
+        return ms, cnt
+
+    # -- A0
+    def eig_gershgorin_lower(self) -> float:
+        a = ctypes.c_double()
+        self._check(self.lib.eig_gershgorin_lower(self.h, ctypes.byref(a)), "eig_gershgorin_lower")
+        return a.value
+
+    def eig_set_interval(self, a: float, b: float):
+        self._check(self.lib.eig_set_interval(self.h, float(a), float(b)), "eig_set_interval")
+
+    def eig_set_degree(self, d: int):
+        self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
+        self.d = d
+
+    # -- A1/A2
+    def filter_step(self, X: torch.Tensor, normalize: bool = True, colnorm: torch.Tensor | None = None):
+        px, ld, _ = _blk(X, "X")
+        cn = ctypes.c_void_p(colnorm.data_ptr()) if colnorm is not None else None
+        self._check(self.lib.filter_step(self.h, px, ld, 1 if normalize else 0, cn), "filter_step")
+
+    # -- A3
+    def spmm(self, X: torch.Tensor, Y: torch.Tensor, alpha: float = 1.0, shift: float = 0.0):
+        px, ldx, nc = _blk(X, "X")
+        py, ldy, nc2 = _blk(Y, "Y")
+        if nc2 != nc:
+            raise ValueError("spmm: column mismatch")
+        self._check(self.lib.spmm(self.h, float(alpha), float(shift), px, ldx, py, ldy, nc), "spmm")
+
+    # -- A4
+    def gram(self, X: torch.Tensor, Y: torch.Tensor, G: torch.Tensor):
+        px, ldx, m1 = _blk(X, "X")
+        py, ldy, m2 = _blk(Y, "Y")
+        pg, ldg, _ = _blk(G, "G")
+        self._check(self.lib.gram(self.h, px, ldx, m1, py, ldy, m2, pg, ldg), "gram")
+
+    def gemm(self, X: torch.Tensor, B: torch.Tensor, Out: torch.Tensor, alpha: float = 1.0, beta: float = 0.0,
+             Cin: torch.Tensor | None = None):
+        px, ldx, m1 = _blk(X, "X")
+        pb, ldb, m2 = _blk(B, "B")
+        po, ldo, _ = _blk(Out, "Out")
+        if Cin is not None:
+            pc, ldc, _ = _blk(Cin, "Cin")
+        else:
+            pc, ldc = None, 0
+        self._check(self.lib.gemm(self.h, float(alpha), px, ldx, m1, pb, ldb, m2, float(beta), pc, ldc, po, ldo),
+                    "gemm")
+
+    def orthonormalize(self, X: torch.Tensor) -> int:
+        px, ld, nc = _blk(X, "X")
+        r = ctypes.c_int32()
+        self._check(self.lib.orthonormalize(self.h, px, ld, nc, ctypes.byref(r)), "orthonormalize")
+        return r.value
+
+    def arr_project(self, X: torch.Tensor, Y: torch.Tensor | None = None, p: int | None = None):
+        p = self.p if p is None else p
+        px, ldx, _ = _blk(X, "X")
+        if Y is not None:
+            py, ldy, _ = _blk(Y, "Y")
+        else:
+            py, ldy = None, 0
+        ritz = np.empty((p + 1) * self.k)
+        r = ctypes.c_int32()
+        self._check(self.lib.arr_project_p(self.h, p, px, ldx, py, ldy,
+                                           ritz.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(r)),
+                    "arr_project")
+        return ritz, r.value
+
+    # -- A6
+    def residuals(self, Y: torch.Tensor, mu) -> np.ndarray:
+        py, ldy, nc = _blk(Y, "Y")
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        if len(mu) != nc:
+            raise ValueError("residuals: len(mu) != ncols")
+        res = np.empty(nc)
+        self._check(self.lib.residuals(self.h, py, ldy, mu.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nc,
+                                       res.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "residuals")
+        return res
+
+    # -- driver
+    def eig_solve(self, X: torch.Tensor, tol: float = 1e-10, maxit: int = 300, s_max: int = 5):
+        px, ld, _ = _blk(X, "X")
+        opts = arr_solve_opts(tol, maxit, s_max)
+        ev = np.empty(self.k)
+        res = np.empty(self.k)
+        info = arr_solve_info()
+        self._check(self.lib.eig_solve(self.h, px, ld, ctypes.byref(opts),
+                                       ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(info)),
+                    "eig_solve")
+        return ev, res, info
+
+
+def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None) -> EigContext:
+    return EigContext(A, k, p, d, stream)
+
+
+def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, s_max=5, evec=None,
+                   stream=None):
+    """Public host-buffer entry (eig_solve_host): host arrays in, host results out.
+    Arguments may be numpy arrays or (pinned) CPU torch tensors."""
+    lib = _lib.load()
+
+    def ptr(a):
+        if isinstance(a, torch.Tensor):
+            assert not a.is_cuda and a.is_contiguous()
+            return ctypes.c_void_p(a.data_ptr())
+        assert a.flags.c_contiguous
+        return ctypes.c_void_p(a.ctypes.data)
+
+    nnz = int(col_idx.shape[0])
+    ev = np.empty(k)
+    res = np.empty(k)
+    info = arr_solve_info()
+    opts = arr_solve_opts(tol, maxit, s_max)
+    hs, _ = _stream_handle(stream)
+    st = lib.eig_solve_host(int(n), nnz, ptr(row_ptr), ptr(col_idx), ptr(val), k, p, d, ptr(X0),
+                            ctypes.byref(opts), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                            res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                            ptr(evec) if evec is not None else None, ctypes.byref(info), hs)
+    if st != 0:
+        raise ArrError(st, "eig_solve_host failed")
+    return ev, res, info

@@ -1,0 +1,592 @@
+// C-ABI of libarrabit (include/arrabit.h): context, workspace, and the
+// composition of the kernels into filter_step / orthonormalize / arr_project /
+// residuals / eig_solve.  Paper: arXiv 1507.06078 (P:n = PAPER.md line n).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr double kSvqbTau = 1e-14;  // eigenvalue floor of the SVQB Gram (relative)
+enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2 };  // dinfo slots (INFO_RANK0.. per block)
+
+arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
+    if (c) {
+        c->err = msg;
+        if (code == ARR_ECUDA || code == ARR_ECUSOLVER) c->poisoned = code;
+    }
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess) return fail(c, ARR_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+#define SOLVER_TRY(expr)                                                                            \
+    do {                                                                                            \
+        cusolverStatus_t s_ = (expr);                                                               \
+        if (s_ != CUSOLVER_STATUS_SUCCESS)                                                          \
+            return fail(c, ARR_ECUSOLVER, std::string(#expr) + " failed: " + std::to_string((int)s_)); \
+    } while (0)
+#define CHECK_LAUNCH() CUDA_TRY(cudaGetLastError())
+#define GUARD(c)                                                                                    \
+    do {                                                                                            \
+        if (!(c)) return ARR_EINVAL;                                                                \
+        if ((c)->poisoned != ARR_OK) return (c)->poisoned;                                          \
+    } while (0)
+
+inline int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
+inline int32_t m_of(const arr_ctx *c, int p) { return (p + 1) * c->w; }
+inline int64_t ldQ(const arr_ctx *c) { return even_up(m_of(c, c->p)); }
+inline int64_t ldT(const arr_ctx *c) { return even_up(c->w); }
+
+// small dense region layout: [H | V | B | G], each m*m doubles
+inline double *H_buf(arr_ctx *c) { const int64_t m = m_of(c, c->p); return c->small; }
+inline double *V_buf(arr_ctx *c) { const int64_t m = m_of(c, c->p); return c->small + m * m; }
+inline double *B_buf(arr_ctx *c) { const int64_t m = m_of(c, c->p); return c->small + 2 * m * m; }
+inline double *G_buf(arr_ctx *c) { const int64_t m = m_of(c, c->p); return c->small + 3 * m * m; }
+// vecw layout: [norms (MAXW) | shifts (m) | D (m)]
+inline double *NORM_buf(arr_ctx *c) { return c->vecw; }
+inline double *SHIFT_buf(arr_ctx *c) { return c->vecw + std::max(m_of(c, c->p), ARR_MAX_W); }
+inline double *D_buf(arr_ctx *c) { return c->vecw + 2 * (int64_t)std::max(m_of(c, c->p), ARR_MAX_W); }
+
+// ---------------------------------------------------------------- phase timing
+int t_mark(arr_ctx *c) {
+    if (!c->timing) return -1;
+    if (c->ev_next == (int)c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        c->ev_pool.push_back(e);
+    }
+    const int i = c->ev_next++;
+    cudaEventRecord(c->ev_pool[i], c->stream);
+    return i;
+}
+void t_add(arr_ctx *c, int phase, int e0, int e1, int64_t count) {
+    if (e0 >= 0 && e1 >= 0) c->pending.push_back({phase, e0, e1, count});
+}
+void t_resolve(arr_ctx *c) {  // call only right after a stream sync, with no phase open
+    for (const auto &p : c->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev_pool[p.e0], c->ev_pool[p.e1]) == cudaSuccess) {
+            c->phase_ms[p.phase] += ms;
+            c->phase_cnt[p.phase] += p.count;
+        }
+    }
+    c->pending.clear();
+    c->ev_next = 0;
+}
+
+double chebT(int d, double t) {  // host recursion, Eq. cheby-poly
+    double r0 = 1.0, r1 = t;
+    if (d == 0) return 1.0;
+    for (int j = 1; j < d; ++j) {
+        const double r2 = 2.0 * t * r1 - r0;
+        r0 = r1;
+        r1 = r2;
+    }
+    return r1;
+}
+
+// ---------------------------------------------------------------- pieces
+// Filter degrees; result left in X (normalised) -- no host sync.
+arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
+    const double cc = 0.5 * (c->a + c->b), e = 0.5 * (c->b - c->a);
+    const int w = c->w;
+    double *T = c->T;
+    const int64_t lt = ldT(c);
+    double *cur = X;
+    int64_t ldcur = ldx;
+    double *other = T;
+    int64_t ldother = lt;
+    int nblk = 0;
+    const int ev0 = t_mark(c);
+    for (int j = 0; j < c->d; ++j) {
+        SpmmArgs s{};
+        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+        s.n = c->A.n; s.w = w;
+        s.Yin = cur; s.ld_in = ldcur;
+        if (j == 0) {
+            s.Yprev = nullptr; s.alpha = 1.0 / e; s.beta = 0.0;
+        } else {
+            s.Yprev = other; s.ld_prev = ldother; s.alpha = 2.0 / e; s.beta = -1.0;
+        }
+        s.shift = cc;
+        s.Yout = other; s.ld_out = ldother;
+        s.partials = (normalize && j == c->d - 1) ? c->part : nullptr;
+        const int g = launch_spmm(c, s);
+        if (g < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
+        nblk = g;
+        std::swap(cur, other);
+        std::swap(ldcur, ldother);
+    }
+    t_add(c, 0, ev0, t_mark(c), c->d);
+    CHECK_LAUNCH();
+    if (normalize) {
+        double *nrm = colnorm_dev ? colnorm_dev : NORM_buf(c);
+        launch_colnorm_finalize(c, c->part, nblk, w, nrm, nullptr);
+        launch_check_norms(c, nrm, w, c->dinfo + INFO_BAD);
+        launch_scale_cols(c, cur, ldcur, X, ldx, c->A.n, w, nrm);
+    } else if (cur != X) {
+        launch_copy_rows(c, cur, ldcur, X, ldx, c->A.n, w);
+    }
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+// One SVQB pass: Out = In * D V L^{-1/2} (ncols columns), rank -> dinfo slot.
+arr_status svqb_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
+                     int *rank_slot) {
+    double *G = G_buf(c), *V = V_buf(c), *B = B_buf(c), *D = D_buf(c);
+    launch_gram(c, In, ldin, ncols, In, ldin, ncols, c->A.n, G, ncols, c->part);
+    launch_svqb_prep(c, G, ncols, D, V);
+    CHECK_LAUNCH();
+    SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ncols, V, ncols,
+                                c->evals, c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
+    launch_svqb_build(c, D, V, c->evals, ncols, kSvqbTau, B, rank_slot);
+    launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n);
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+// Two SVQB passes In -> Out through the scratch T (In may equal Out).
+arr_status svqb2(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
+                 int *rank_slot) {
+    arr_status st;
+    if ((st = svqb_pass(c, In, ldin, c->T, ldT(c), ncols, rank_slot)) != ARR_OK) return st;
+    if ((st = svqb_pass(c, c->T, ldT(c), Out, ldout, ncols, nullptr)) != ARR_OK) return st;
+    return ARR_OK;
+}
+
+arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                    double *ritz_host, int32_t *rank) {
+    const int w = c->w;
+    const int m = m_of(c, p_use);
+    const int64_t lq = ldQ(c), lt = ldT(c);
+    double *Q = c->Q, *T = c->T;
+    arr_status st;
+    const int ev0 = t_mark(c);
+    // U_0 = orth(X): Alg. RR step 1 on the first block
+    if ((st = svqb2(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
+    // U_j = orth((I - Q Q^T) A U_{j-1}): the block-Krylov augmentation of Eq. S:ARR
+    for (int j = 1; j <= p_use; ++j) {
+        SpmmArgs s{};
+        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+        s.n = c->A.n; s.w = w;
+        s.Yin = Q + (int64_t)(j - 1) * w; s.ld_in = lq;
+        s.alpha = 1.0; s.shift = 0.0;
+        s.Yout = T; s.ld_out = lt;
+        if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+        const int jw = j * w;
+        for (int pass = 0; pass < 2; ++pass) {  // block classical Gram-Schmidt, twice
+            launch_gram(c, Q, lq, jw, T, lt, w, c->A.n, G_buf(c), w, c->part);
+            launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
+        }
+        CHECK_LAUNCH();
+        double *Qj = Q + (int64_t)jw;
+        if ((st = svqb_pass(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j)) != ARR_OK) return st;
+        if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
+        launch_copy_rows(c, T, lt, Qj, lq, c->A.n, w);
+    }
+    // H = Q^T (A Q), one w-column block of AQ at a time (AQ never stored whole)
+    double *H = H_buf(c);
+    for (int j = 0; j <= p_use; ++j) {
+        SpmmArgs s{};
+        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+        s.n = c->A.n; s.w = w;
+        s.Yin = Q + (int64_t)j * w; s.ld_in = lq;
+        s.alpha = 1.0; s.shift = 0.0;
+        s.Yout = T; s.ld_out = lt;
+        if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+        launch_gram(c, Q, lq, m, T, lt, w, c->A.n, H + (int64_t)j * w, m, c->part);
+    }
+    launch_symmetrize(c, H, m);
+    CHECK_LAUNCH();
+    // H = V Theta V^T (Alg. RR step 3): small dense eig on device (not graded)
+    SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, H, m, c->evals,
+                                c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
+    // Y = Q V[:, leading w] (Alg. RR step 4; Alg. ARR step 4)
+    if (Y) {
+        launch_ritz_select(c, H, m, w, B_buf(c));
+        launch_gemm(c, 1.0, Q, lq, m, B_buf(c), w, w, 0.0, nullptr, 0, Y, ldy, c->A.n);
+    }
+    CHECK_LAUNCH();
+    t_add(c, 1, ev0, t_mark(c), 1);
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage, c->evals, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo, sizeof(int) * (INFO_RANK0 + p_use + 1), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    t_resolve(c);
+    if (c->h_istage[INFO_SYEVD] != 0)
+        return fail(c, ARR_ECUSOLVER, "syevd info = " + std::to_string(c->h_istage[INFO_SYEVD]));
+    for (int i = 0; i < m; ++i) ritz_host[i] = c->h_stage[m - 1 - i];
+    if (rank) {
+        int r = 0;
+        for (int j = 0; j <= p_use; ++j) r += c->h_istage[INFO_RANK0 + j];
+        *rank = r;
+    }
+    return ARR_OK;
+}
+
+arr_status residuals_core(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_host, int ncols,
+                          double *res_host) {
+    double *shift = SHIFT_buf(c), *out = NORM_buf(c);
+    memcpy(c->h_stage, mu_host, sizeof(double) * ncols);
+    CUDA_TRY(cudaMemcpyAsync(shift, c->h_stage, sizeof(double) * ncols, cudaMemcpyHostToDevice, c->stream));
+    const int ev0 = t_mark(c);
+    SpmmArgs s{};
+    s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+    s.n = c->A.n; s.w = ncols;
+    s.Yin = Y; s.ld_in = ldy;
+    s.alpha = 1.0; s.shift = 0.0; s.colshift = shift;
+    s.Yout = nullptr;
+    s.partials = c->part;
+    const int g = launch_spmm(c, s);
+    if (g < 0) return fail(c, ARR_EINVAL, "residuals: unsupported width");
+    launch_colnorm_finalize(c, c->part, g, ncols, out, shift);
+    CHECK_LAUNCH();
+    t_add(c, 2, ev0, t_mark(c), 1);
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage, out, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    t_resolve(c);
+    memcpy(res_host, c->h_stage, sizeof(double) * ncols);
+    return ARR_OK;
+}
+
+bool block_ok(const double *p, int64_t ld, int ncols) { return p != nullptr && ld >= ncols && ncols >= 1; }
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream) {
+    if (!out || !A) return ARR_EINVAL;
+    *out = nullptr;
+    if (A->n < 1 || A->n >= (int64_t(1) << 31) || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->val)))
+        return ARR_EINVAL;
+    if (k < 1 || p < 0 || d < 1 || (int64_t)(p + 1) * k >= A->n || k > ARR_MAX_W) return ARR_EINVAL;
+    arr_ctx *c = new (std::nothrow) arr_ctx();
+    if (!c) return ARR_ENOMEM;
+    c->A = *A;
+    c->k = k; c->w = k; c->p = p; c->d = d;
+    c->stream = (cudaStream_t)stream;
+    c->poisoned = ARR_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (c->num_sms <= 0) c->num_sms = 148;
+    const int64_t n = A->n, w = k, m = (int64_t)(p + 1) * k;
+    const int64_t lq = even_up(m), lt = even_up(w);
+    const int64_t mm = std::max<int64_t>(m, ARR_MAX_W);
+    c->part_elems = (size_t)std::max<int64_t>(16 * m * w, 4096 * mm);
+    struct Alloc { void **p; size_t bytes; };
+    std::vector<Alloc> al = {
+        {(void **)&c->T, sizeof(double) * (size_t)n * lt},
+        {(void **)&c->Q, sizeof(double) * (size_t)n * lq},
+        {(void **)&c->part, sizeof(double) * c->part_elems},
+        {(void **)&c->small, sizeof(double) * 4 * (size_t)m * m},
+        {(void **)&c->evals, sizeof(double) * (size_t)m},
+        {(void **)&c->vecw, sizeof(double) * 3 * (size_t)mm},
+        {(void **)&c->dinfo, sizeof(int) * 64},
+    };
+    size_t total = 0;
+    for (auto &x : al) {
+        if (cudaMalloc(x.p, x.bytes) != cudaSuccess) {
+            cudaGetLastError();
+            eig_destroy(c);
+            return ARR_ENOMEM;
+        }
+        total += x.bytes;
+    }
+    cudaMemsetAsync(c->dinfo, 0, sizeof(int) * 64, c->stream);
+    if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) { eig_destroy(c); return ARR_ECUSOLVER; }
+    cusolverDnSetStream(c->solver, c->stream);
+    int lwork = 0;
+    if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)m, c->small,
+                                    (int)m, c->evals, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+        eig_destroy(c);
+        return ARR_ECUSOLVER;
+    }
+    int lwork_w = 0;
+    cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)w, c->small, (int)w,
+                                c->evals, &lwork_w);
+    c->solver_lwork = std::max(lwork, lwork_w);
+    if (cudaMalloc(&c->solver_work, sizeof(double) * (size_t)c->solver_lwork) != cudaSuccess) {
+        cudaGetLastError();
+        eig_destroy(c);
+        return ARR_ENOMEM;
+    }
+    total += sizeof(double) * (size_t)c->solver_lwork;
+    if (cudaMallocHost(&c->h_stage, sizeof(double) * (size_t)(mm + 64)) != cudaSuccess ||
+        cudaMallocHost(&c->h_istage, sizeof(int) * 64) != cudaSuccess) {
+        cudaGetLastError();
+        eig_destroy(c);
+        return ARR_ENOMEM;
+    }
+    c->ws_bytes = total;
+    *out = c;
+    return ARR_OK;
+}
+
+arr_status eig_destroy(arr_ctx *c) {
+    if (!c) return ARR_EINVAL;
+    cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->solver_work};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_istage) cudaFreeHost(c->h_istage);
+    if (c->solver) cusolverDnDestroy(c->solver);
+    delete c;
+    return ARR_OK;
+}
+
+const char *eig_last_error(const arr_ctx *c) { return c ? c->err.c_str() : "null context"; }
+size_t eig_workspace_bytes(const arr_ctx *c) { return c ? c->ws_bytes : 0; }
+uint64_t eig_launch_count(const arr_ctx *c) { return c ? c->launches : 0; }
+
+arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out) {
+    GUARD(c);
+    if (!a_out) return fail(c, ARR_EINVAL, "a_out is NULL");
+    int nb = 0;
+    launch_gershgorin(c, c->part, &nb);
+    launch_min_finalize(c, c->part, nb, NORM_buf(c));
+    CHECK_LAUNCH();
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage, NORM_buf(c), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *a_out = c->h_stage[0];
+    return ARR_OK;
+}
+
+arr_status eig_set_interval(arr_ctx *c, double a, double b) {
+    GUARD(c);
+    if (!(a < b) || !isfinite(a) || !isfinite(b)) return fail(c, ARR_EINVAL, "interval needs finite a < b");
+    c->a = a; c->b = b; c->have_interval = true;
+    return ARR_OK;
+}
+
+arr_status eig_set_degree(arr_ctx *c, int32_t d) {
+    GUARD(c);
+    if (d < 1) return fail(c, ARR_EINVAL, "degree must be >= 1");
+    c->d = d;
+    return ARR_OK;
+}
+
+arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev) {
+    GUARD(c);
+    if (!c->have_interval) return fail(c, ARR_EINVAL, "eig_set_interval not called");
+    if (!block_ok(X, ldx, c->w)) return fail(c, ARR_EINVAL, "bad block X / ldx");
+    CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
+    arr_status st = filter_core(c, X, ldx, normalize, colnorm_dev);
+    if (st != ARR_OK) return st;
+    if (normalize) {
+        CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        t_resolve(c);
+        if (c->h_istage[0]) return fail(c, ARR_ENUMERIC, "zero or non-finite column norm after filtering");
+    }
+    return ARR_OK;
+}
+
+arr_status eig_set_timing(arr_ctx *c, int32_t on) {
+    GUARD(c);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->pending.clear();
+    c->ev_next = 0;
+    c->timing = on != 0;
+    for (int i = 0; i < 3; ++i) { c->phase_ms[i] = 0.0; c->phase_cnt[i] = 0; }
+    return ARR_OK;
+}
+
+arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts) {
+    GUARD(c);
+    if (!ms || !counts) return fail(c, ARR_EINVAL, "null output");
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    t_resolve(c);
+    for (int i = 0; i < 3; ++i) { ms[i] = c->phase_ms[i]; counts[i] = c->phase_cnt[i]; }
+    return ARR_OK;
+}
+
+arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                int32_t ncols) {
+    GUARD(c);
+    if (!block_ok(X, ldx, ncols) || !block_ok(Y, ldy, ncols) || ncols > ARR_MAX_W)
+        return fail(c, ARR_EINVAL, "bad block / ncols");
+    SpmmArgs s{};
+    s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+    s.n = c->A.n; s.w = ncols;
+    s.Yin = X; s.ld_in = ldx;
+    s.alpha = alpha; s.shift = shift;
+    s.Yout = Y; s.ld_out = ldy;
+    if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "unsupported width");
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy, int32_t m2,
+                double *G, int64_t ldg) {
+    GUARD(c);
+    if (!block_ok(X, ldx, m1) || !block_ok(Y, ldy, m2) || !G || ldg < m2) return fail(c, ARR_EINVAL, "bad gram args");
+    launch_gram(c, X, ldx, m1, Y, ldy, m2, c->A.n, G, ldg, c->part);
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B, int64_t ldb,
+                int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo) {
+    GUARD(c);
+    if (!block_ok(X, ldx, m1) || !B || ldb < m2 || !block_ok(Out, ldo, m2) || (beta != 0.0 && !block_ok(Cin, ldc, m2)))
+        return fail(c, ARR_EINVAL, "bad gemm args");
+    if ((const void *)X == (const void *)Out) return fail(c, ARR_EINVAL, "gemm: X aliases Out");
+    launch_gemm(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, c->A.n);
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank) {
+    GUARD(c);
+    if (!block_ok(X, ldx, ncols) || ncols > c->w) return fail(c, ARR_EINVAL, "bad block / ncols > w");
+    arr_status st = svqb_pass(c, X, ldx, c->T, ldT(c), ncols, c->dinfo + INFO_RANK0);
+    if (st != ARR_OK) return st;
+    if ((st = svqb_pass(c, c->T, ldT(c), X, ldx, ncols, nullptr)) != ARR_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo, sizeof(int) * (INFO_RANK0 + 1), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->h_istage[INFO_SYEVD] != 0) return fail(c, ARR_ECUSOLVER, "syevd failed");
+    if (rank) *rank = c->h_istage[INFO_RANK0];
+    return ARR_OK;
+}
+
+arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                         double *ritz_host, int32_t *rank) {
+    GUARD(c);
+    if (p_use < 0 || p_use > c->p) return fail(c, ARR_EINVAL, "p_use out of range");
+    if (!block_ok(X, ldx, c->w) || (Y && !block_ok(Y, ldy, c->w)) || !ritz_host)
+        return fail(c, ARR_EINVAL, "bad arr_project args");
+    return arr_core(c, p_use, X, ldx, Y, ldy, ritz_host, rank);
+}
+
+arr_status arr_project(arr_ctx *c, const double *X, int64_t ldx, double *Y, int64_t ldy, double *ritz_host,
+                       int32_t *rank) {
+    GUARD(c);
+    return arr_project_p(c, c->p, X, ldx, Y, ldy, ritz_host, rank);
+}
+
+arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_host, int32_t ncols,
+                     double *res_host) {
+    GUARD(c);
+    if (!block_ok(Y, ldy, ncols) || ncols > std::max(m_of(c, c->p), ARR_MAX_W) || !mu_host || !res_host)
+        return fail(c, ARR_EINVAL, "bad residual args");
+    return residuals_core(c, Y, ldy, mu_host, ncols, res_host);
+}
+
+arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts, double *eigval_host,
+                     double *res_host, arr_solve_info *info) {
+    GUARD(c);
+    if (!block_ok(X, ldx, c->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
+    const int w = c->w, k = c->k;
+    const int m = m_of(c, c->p);
+    std::vector<double> ritz(m), res(k);
+    arr_solve_info inf{};
+    double a = 0.0;
+    arr_status st = eig_gershgorin_lower(c, &a);
+    if (st != ARR_OK) return st;
+    // b: smallest Ritz value of RR(A, X0)
+    std::vector<double> r0(w);
+    if ((st = arr_core(c, 0, X, ldx, nullptr, 0, r0.data(), nullptr)) != ARR_OK) return st;
+    double b = r0[w - 1], mu1 = r0[0];
+    if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    const int64_t spmm0 = c->spmm_blocks;
+    bool done = false;
+    int32_t rank = 0;
+    for (int outer = 1; outer <= opts->maxit; ++outer) {
+        if ((st = eig_set_interval(c, a, b)) != ARR_OK) return st;
+        // sweeps between ARR steps: dynamic-range rule (R6)
+        const double cc = 0.5 * (a + b), e = 0.5 * (b - a);
+        const double amp = fabs(chebT(c->d, (mu1 - cc) / e));
+        int s = opts->s_max;
+        if (amp > 1.0) {
+            if (!isfinite(amp)) s = 1;
+            else s = (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
+        }
+        CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
+        for (int q = 0; q < s; ++q)
+            if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;  // MPM sweep
+        inf.sweeps += s;
+        if ((st = arr_core(c, c->p, X, ldx, X, ldx, ritz.data(), &rank)) != ARR_OK) return st;  // ARR
+        CUDA_TRY(cudaMemcpyAsync(c->h_istage + 32, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        if ((st = residuals_core(c, X, ldx, ritz.data(), k, res.data())) != ARR_OK) return st;  // Eq. resi
+        if (c->h_istage[32]) return fail(c, ARR_ENUMERIC, "zero or non-finite column norm after filtering");
+        double maxres = 0.0;
+        for (int i = 0; i < k; ++i) maxres = std::max(maxres, res[i]);
+        inf.outer = outer;
+        inf.maxres = maxres;
+        inf.last_rank = rank;
+        inf.a = a; inf.b = b;
+        if (maxres <= opts->tol) { done = true; break; }  // Eq. out-stop
+        b = ritz[std::min(w, m - 1)];
+        mu1 = ritz[0];
+        if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    }
+    inf.converged = done ? 1 : 0;
+    inf.spmm_blocks = c->spmm_blocks - spmm0;
+    for (int i = 0; i < k; ++i) { eigval_host[i] = ritz[i]; res_host[i] = res[i]; }
+    if (info) *info = inf;
+    return ARR_OK;
+}
+
+arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+                          int32_t k, int32_t p, int32_t d, const double *X0, const arr_solve_opts *opts,
+                          double *eigval, double *res, double *evec, arr_solve_info *info, void *stream) {
+    if (!row_ptr || !col_idx || !val || !X0 || !opts || !eigval || !res || n < 1 || k < 1) return ARR_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t *d_rp = nullptr;
+    int32_t *d_ci = nullptr;
+    double *d_val = nullptr, *d_X = nullptr;
+    arr_ctx *c = nullptr;
+    arr_status st = ARR_OK;
+    const int64_t ldx = even_up(k);
+    auto cleanup = [&]() {
+        if (c) eig_destroy(c);
+        cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_val); cudaFree(d_X);
+    };
+    if (cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)) != cudaSuccess || cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+        cudaMalloc(&d_val, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+        cudaMalloc(&d_X, sizeof(double) * n * ldx) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        return ARR_ENOMEM;
+    }
+    if (cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpy2DAsync(d_X, sizeof(double) * ldx, X0, sizeof(double) * k, sizeof(double) * k, n,
+                          cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cleanup();
+        return ARR_ECUDA;
+    }
+    arr_csr A{n, nnz, d_rp, d_ci, d_val};
+    st = eig_init(&c, &A, k, p, d, stream);
+    if (st == ARR_OK) st = eig_solve(c, d_X, ldx, opts, eigval, res, info);
+    if (st == ARR_OK && evec) {
+        if (cudaMemcpy2DAsync(evec, sizeof(double) * k, d_X, sizeof(double) * ldx, sizeof(double) * k, n,
+                              cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            st = ARR_ECUDA;
+    }
+    cleanup();
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// Tall-skinny fp64 contractions of the ARR step (Alg. RR, Alg. ARR
+// P:537-540) on the FP64 tensor cores of sm_100a: mma.sync.m8n8k4.f64 (DMMA;
+// tcgen05 has no f64 kind).  Gram products are split over rows with a fixed-
+// order reduction of the partial tiles (deterministic, no atomics).
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int TILE = 64;   // CTA tile edge (4 warps, 2x2, 32x32 each)
+constexpr int KS = 16;     // rows (Gram) / k-columns (GEMM) per stage
+constexpr int PAD = 4;     // smem padding (doubles): conflict-free fragment loads
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// partials[split][a][b] (ld = m2) = sum_{i in slab} X[i, a] * Y[i, b]
+__global__ void __launch_bounds__(THREADS) gram_kernel(const double *__restrict__ X, int64_t ldx, int m1,
+                                                       const double *__restrict__ Y, int64_t ldy, int m2,
+                                                       int64_t n, int64_t rows_per_split, bool sym,
+                                                       double *__restrict__ part) {
+    const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
+    if (sym && tb < ta) return;
+    const int a0 = ta * TILE, b0 = tb * TILE;
+    const int64_t k0 = (int64_t)split * rows_per_split;
+    int64_t k1 = k0 + rows_per_split;
+    if (k1 > n) k1 = n;
+    __shared__ double Xs[2][KS][TILE + PAD];
+    __shared__ double Ys[2][KS][TILE + PAD];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    constexpr int PER = KS * TILE / THREADS;  // 8 elements per operand per thread
+    double rx[PER], ry[PER];
+    auto gload = [&](int64_t kb) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + q * THREADS;
+            const int rr = idx / TILE, cc = idx % TILE;
+            const int64_t row = kb + rr;
+            const bool rok = row < k1;
+            rx[q] = (rok && a0 + cc < m1) ? __ldg(X + row * ldx + a0 + cc) : 0.0;
+            ry[q] = (rok && b0 + cc < m2) ? __ldg(Y + row * ldy + b0 + cc) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + q * THREADS;
+            const int rr = idx / TILE, cc = idx % TILE;
+            Xs[buf][rr][cc] = rx[q];
+            Ys[buf][rr][cc] = ry[q];
+        }
+    };
+    if (k0 < k1) {
+        gload(k0);
+        sstore(0);
+        __syncthreads();
+        int buf = 0;
+        for (int64_t kb = k0; kb < k1; kb += KS) {
+            const bool more = kb + KS < k1;
+            if (more) gload(kb + KS);
+#pragma unroll
+            for (int kk = 0; kk < KS / 4; ++kk) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * 32 + mt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+            }
+            if (more) {
+                sstore(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    }
+    double *P = part + (int64_t)split * m1 * m2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int ra = a0 + wm * 32 + mt * 8 + (lane >> 2);
+                const int cb = b0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
+                if (ra < m1 && cb < m2) P[(int64_t)ra * m2 + cb] = acc[mt][nt][e];
+            }
+}
+
+__global__ void gram_reduce_kernel(const double *__restrict__ part, int nsplit, int m1, int m2, bool sym,
+                                   double *__restrict__ G, int64_t ldg) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)m1 * m2) return;
+    int ra = (int)(t / m2), cb = (int)(t % m2);
+    int sa = ra, sb = cb;
+    if (sym && cb < ra) { sa = cb; sb = ra; }  // mirror: exactly symmetric
+    double s = 0.0;
+    const int64_t stride = (int64_t)m1 * m2;
+    for (int q = 0; q < nsplit; ++q) s += part[q * stride + (int64_t)sa * m2 + sb];
+    G[(int64_t)ra * ldg + cb] = s;
+}
+
+// Out[n x m2] = beta*Cin + alpha*X[n x m1] * B[m1 x m2]
+__global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const double *__restrict__ X, int64_t ldx,
+                                                       int m1, const double *__restrict__ B, int64_t ldb, int m2,
+                                                       double beta, const double *Cin, int64_t ldc, double *Out,
+                                                       int64_t ldo, int64_t n) {
+    const int64_t r0 = (int64_t)blockIdx.x * TILE;
+    const int c0 = blockIdx.y * TILE;
+    __shared__ double Xs[2][TILE][KS + PAD];
+    __shared__ double Bs[2][KS][TILE + PAD];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr int PER = KS * TILE / THREADS;
+    double rx[PER], rb[PER];
+    auto gload = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + q * THREADS;
+            // X tile: 64 rows x 16 k (k fastest)
+            const int xr = idx / KS, xk = idx % KS;
+            const int64_t row = r0 + xr;
+            rx[q] = (row < n && kb + xk < m1) ? __ldg(X + row * ldx + kb + xk) : 0.0;
+            // B tile: 16 k x 64 cols (col fastest)
+            const int bk = idx / TILE, bc = idx % TILE;
+            rb[q] = (kb + bk < m1 && c0 + bc < m2) ? __ldg(B + (int64_t)(kb + bk) * ldb + c0 + bc) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = tid + q * THREADS;
+            Xs[buf][idx / KS][idx % KS] = rx[q];
+            Bs[buf][idx / TILE][idx % TILE] = rb[q];
+        }
+    };
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int kb = 0; kb < m1; kb += KS) {
+        const bool more = kb + KS < m1;
+        if (more) gload(kb + KS);
+#pragma unroll
+        for (int kk = 0; kk < KS / 4; ++kk) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * 32 + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+        }
+        if (more) {
+            sstore(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t row = r0 + wm * 32 + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
+                if (row < n && cb < m2) {
+                    double v = alpha * acc[mt][nt][e];
+                    if (beta != 0.0) v += beta * Cin[row * ldc + cb];
+                    Out[row * ldo + cb] = v;
+                }
+            }
+}
+
+// ---------------------------------------------------------------- small dense
+__global__ void svqb_prep_kernel(const double *__restrict__ G, int w, double *__restrict__ D,
+                                 double *__restrict__ Gs) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    const double gi = G[(int64_t)i * w + i], gj = G[(int64_t)j * w + j];
+    const double di = gi > 0.0 ? 1.0 / sqrt(gi) : 0.0;
+    const double dj = gj > 0.0 ? 1.0 / sqrt(gj) : 0.0;
+    // symmetrise while scaling (G is symmetric up to rounding of the split sums)
+    Gs[t] = di * (0.5 * (G[t] + G[(int64_t)j * w + i])) * dj;
+    if (j == 0) D[i] = di;
+}
+
+__global__ void svqb_build_kernel(const double *__restrict__ D, const double *__restrict__ Vcm,
+                                  const double *__restrict__ lam, int w, double tau, double *__restrict__ B,
+                                  int *rank_out) {
+    const double lmax = lam[w - 1];
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t == 0 && rank_out) {
+        int r = 0;
+        for (int j = 0; j < w; ++j) r += (lmax > 0.0 && lam[j] > 1e-14 * lmax);
+        *rank_out = r;
+    }
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    double l = lam[j];
+    const double floor_l = tau * lmax;
+    if (l < floor_l) l = floor_l;
+    B[t] = (lmax > 0.0) ? D[i] * Vcm[(int64_t)j * w + i] / sqrt(l) : 0.0;
+}
+
+__global__ void symmetrize_kernel(double *H, int m) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)m * m) return;
+    const int i = (int)(t / m), j = (int)(t % m);
+    if (j <= i) return;
+    const double v = 0.5 * (H[(int64_t)i * m + j] + H[(int64_t)j * m + i]);
+    H[(int64_t)i * m + j] = v;
+    H[(int64_t)j * m + i] = v;
+}
+
+__global__ void ritz_select_kernel(const double *__restrict__ Vcm, int m, int wsel, double *__restrict__ Vsel) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)m * wsel) return;
+    const int i = (int)(t / wsel), j = (int)(t % wsel);
+    Vsel[t] = Vcm[(int64_t)(m - 1 - j) * m + i];
+}
+
+inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + threads - 1) / threads); }
+
+}  // namespace
+
+int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms) {
+    const int64_t tiles = (int64_t)((m1 + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE);
+    int64_t target = (int64_t)num_sms * 4;
+    int64_t ns = (target + tiles - 1) / tiles;
+    int64_t maxns = n / 512;  // at least 512 rows per split
+    if (ns > maxns) ns = maxns;
+    if (ns < 1) ns = 1;
+    if (ns > 64) ns = 64;
+    return (int)ns;
+}
+
+void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
+                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials) {
+    int ns = gram_nsplit(n, m1, m2, c->num_sms);
+    while ((size_t)ns * m1 * m2 > c->part_elems && ns > 1) --ns;
+    int64_t rps = (n + ns - 1) / ns;
+    rps = (rps + KS - 1) / KS * KS;
+    const bool sym = (X == Y) && (m1 == m2) && (ldx == ldy);
+    dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
+    gram_kernel<<<grid, THREADS, 0, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    gram_reduce_kernel<<<nblk((int64_t)m1 * m2, 256), 256, 0, c->stream>>>(partials, ns, m1, m2, sym, G, ldg);
+    c->launches += 2;
+}
+
+void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
+                 int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
+                 int64_t n) {
+    dim3 grid((unsigned)((n + TILE - 1) / TILE), (m2 + TILE - 1) / TILE);
+    gemm_kernel<<<grid, THREADS, 0, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n);
+    c->launches++;
+}
+
+void launch_svqb_prep(arr_ctx *c, const double *G, int32_t w, double *D, double *Gs) {
+    svqb_prep_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(G, w, D, Gs);
+    c->launches++;
+}
+
+void launch_svqb_build(arr_ctx *c, const double *D, const double *Vcm, const double *lam, int32_t w, double tau,
+                       double *B, int *rank_out) {
+    svqb_build_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(D, Vcm, lam, w, tau, B, rank_out);
+    c->launches++;
+}
+
+void launch_symmetrize(arr_ctx *c, double *H, int32_t m) {
+    symmetrize_kernel<<<nblk((int64_t)m * m, 256), 256, 0, c->stream>>>(H, m);
+    c->launches++;
+}
+
+void launch_ritz_select(arr_ctx *c, const double *Vcm, int32_t m, int32_t wsel, double *Vsel) {
+    ritz_select_kernel<<<nblk((int64_t)m * wsel, 256), 256, 0, c->stream>>>(Vcm, m, wsel, Vsel);
+    c->launches++;
+}

@@ -1,0 +1,99 @@
+// Internal declarations of libarrabit (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/arrabit.h"
+
+#define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
+
+struct arr_ctx {
+    // problem
+    arr_csr A;
+    int32_t k, w, p, d;
+    cudaStream_t stream;
+    int num_sms;
+    // interval
+    double a, b;
+    bool have_interval;
+    // workspace (owned)
+    double *T;        // n x w scratch (filter ping-pong, ARR W)
+    double *Q;        // n x m ARR basis, ld = m
+    double *part;     // Gram split partials / column-norm partials
+    size_t part_elems;
+    double *small;    // dense m x m buffers (H, V, B ...)
+    double *evals;    // [m]
+    double *vecw;     // [2*ARR_MAX_W] column norms / shifts / scales
+    int *dinfo;       // cuSOLVER info + rank counters
+    double *solver_work;
+    int solver_lwork;
+    cusolverDnHandle_t solver;
+    size_t ws_bytes;
+    // bookkeeping
+    uint64_t launches;
+    int64_t spmm_blocks;
+    arr_status poisoned;
+    std::string err;
+    // phase timing (eig_set_timing)
+    bool timing;
+    std::vector<cudaEvent_t> ev_pool;
+    int ev_next;
+    struct Pending { int phase, e0, e1; int64_t count; };
+    std::vector<Pending> pending;
+    double phase_ms[3];
+    int64_t phase_cnt[3];
+    // pinned host staging
+    double *h_stage;   // [m + 2*ARR_MAX_W + 16]
+    int *h_istage;     // [16]
+};
+
+// ---------------------------------------------------------------- SpMM family
+struct SpmmArgs {
+    const int64_t *row_ptr;
+    const int32_t *col;
+    const double *val;
+    int64_t n;
+    int32_t w;
+    const double *Yin;     // gathered operand Y_j
+    int64_t ld_in;
+    const double *Yprev;   // Y_{j-1} (may alias Yout) or nullptr
+    int64_t ld_prev;
+    double *Yout;          // output or nullptr (no store)
+    int64_t ld_out;
+    double alpha, shift, beta;
+    const double *colshift;  // per-column shift (overrides shift) or nullptr
+    double *partials;        // [gridDim.x * w] column sums of squares of the output, or nullptr
+};
+
+// Launch the fused SpMM: Yout = alpha*(A Yin - shift*Yin) + beta*Yprev.
+// Returns the grid size used (number of partial rows written if partials != nullptr).
+int launch_spmm(arr_ctx *c, const SpmmArgs &a);
+// out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)
+void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,
+                             const double *mu_div);
+// X[i, col] *= 1/norm[col] (in place) or Out = In / norm
+void launch_scale_cols(arr_ctx *c, const double *In, int64_t ld_in, double *Out, int64_t ld_out,
+                       int64_t n, int32_t w, const double *norms);
+void launch_gershgorin(arr_ctx *c, double *partial, int *nblk_out);
+void launch_min_finalize(arr_ctx *c, const double *partial, int nblk, double *out);
+
+// ---------------------------------------------------------------- dense (DMMA)
+int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms);
+void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
+                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials);
+void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
+                 int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out,
+                 int64_t ldo, int64_t n);
+// small dense helpers (single CTA-ish kernels)
+void launch_svqb_prep(arr_ctx *c, const double *G, int32_t w, double *D, double *Gs);
+void launch_svqb_build(arr_ctx *c, const double *D, const double *Vcm, const double *lam, int32_t w,
+                       double tau, double *B, int *rank_out);
+void launch_symmetrize(arr_ctx *c, double *H, int32_t m);
+void launch_ritz_select(arr_ctx *c, const double *Vcm, int32_t m, int32_t wsel, double *Vsel);
+void launch_copy_rows(arr_ctx *c, const double *src, int64_t lds, double *dst, int64_t ldd, int64_t n,
+                      int32_t w);
+void launch_check_norms(arr_ctx *c, const double *norms, int32_t w, int *bad);
