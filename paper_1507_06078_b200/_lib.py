@@ -7,7 +7,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libarrabit.so")
+LIB_PATH = os.environ.get("ARRABIT_LIB", os.path.join(HERE, "libarrabit.so"))  # override: tuning variants
 
 ARR_OK, ARR_EINVAL, ARR_ENOMEM, ARR_ECUDA, ARR_ECUSOLVER, ARR_ENUMERIC = 0, 1, 2, 3, 5, 7
 STATUS_NAMES = {0: "ARR_OK", 1: "ARR_EINVAL", 2: "ARR_ENOMEM", 3: "ARR_ECUDA", 5: "ARR_ECUSOLVER",

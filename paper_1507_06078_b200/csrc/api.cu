@@ -335,6 +335,14 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
         return ARR_ENOMEM;
     }
     c->ws_bytes = total;
+    launch_rowlen_max(c, c->dinfo + 63);
+    if (cudaMemcpyAsync(c->h_istage, c->dinfo + 63, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        eig_destroy(c);
+        return ARR_ECUDA;
+    }
+    c->max_row_nnz = c->h_istage[0];
     *out = c;
     return ARR_OK;
 }

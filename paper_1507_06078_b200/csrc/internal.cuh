@@ -17,6 +17,7 @@ struct arr_ctx {
     int32_t k, w, p, d;
     cudaStream_t stream;
     int num_sms;
+    int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
     // interval
     double a, b;
     bool have_interval;
@@ -79,6 +80,7 @@ void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32
 void launch_scale_cols(arr_ctx *c, const double *In, int64_t ld_in, double *Out, int64_t ld_out,
                        int64_t n, int32_t w, const double *norms);
 void launch_gershgorin(arr_ctx *c, double *partial, int *nblk_out);
+void launch_rowlen_max(arr_ctx *c, int *dev_out);
 void launch_min_finalize(arr_ctx *c, const double *partial, int nblk, double *out);
 
 // ---------------------------------------------------------------- dense (DMMA)

@@ -10,7 +10,10 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef ARR_SPMM_U
+#define ARR_SPMM_U 8  // gathers in flight per row (single column-vector case)
+#endif
+constexpr int kMaxThreads = 512;  // fused SpMM CTA size (R x TX rounded to warps)
 
 template <int VEC>
 struct Vec;
@@ -47,17 +50,105 @@ __device__ __forceinline__ void fma_vec<2>(double2 &acc, double a, const double2
     acc.y = fma(a, x.y, acc.y);
 }
 
-// Thread (r, v0) of a CTA owns row r of each row group and the vector columns
-// v0, v0+TX, ... (NV of them).  Row groups of R rows are visited grid-stride so
-// the rows active on the chip at any time form one contiguous window (L2 reuse
-// of gathered neighbour rows).  Per-row sums run in CSR order (fixed, partition
-// independent).
-template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
-__global__ void __launch_bounds__(kThreads) spmm_fused_kernel(SpmmArgs a, int TX, int R, int wv,
-                                                               int64_t ngroups) {
+// One staged non-zero: element offset of the referenced Y row and the value.
+struct __align__(16) Ent {
+    int64_t off;  // col * ld_in
+    double val;
+};
+
+// Rows of one tile owned by row slot r.  Each row is processed in chunks of K
+// non-zeros: the K {offset, value} entries come from shared memory with one
+// 128-bit LDS each, the K gathers of Y_j are issued back to back (all in
+// flight together), then K FMAs in CSR order.  Slots past the row end are
+// predicated by value 0 and re-read the row's first entry (no branches).
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+__device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nrows, int R, int RR, int r, int TX,
+                                          int v0, int wv, const int *s_rp, const Ent *s_ent,
+                                          double (&ss)[NV][VEC]) {
     using V = Vec<VEC>;
     using T = typename V::T;
+    const double *yin_v[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int vv = v0 + v * TX;
+        yin_v[v] = a.Yin + (vv < wv ? vv : 0) * VEC;
+    }
+    for (int rr = 0; rr < RR; ++rr) {
+        const int lr = rr * R + r;
+        if (lr >= nrows) break;
+        const int64_t i = r0 + lr;
+        T yp[NV];
+        if (HAS_PREV) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int vv = v0 + v * TX;
+                yp[v] = (vv < wv) ? V::ldcs(a.Yprev + i * a.ld_prev + vv * VEC) : V::zero();
+            }
+        }
+        const int p0 = s_rp[lr];
+        const int p1 = s_rp[lr + 1];
+        T acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+        for (int p = p0; p < p1; p += K) {
+            T x[K][NV];
+            double av[K];
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                const bool ok = p + u < p1;
+                const Ent e = s_ent[ok ? p + u : p0];
+                av[u] = ok ? e.val : 0.0;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) x[u][v] = V::ldg(yin_v[v] + e.off);
+            }
+#pragma unroll
+            for (int u = 0; u < K; ++u)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) fma_vec<VEC>(acc[v], av[u], x[u][v]);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int vv = v0 + v * TX;
+            if (vv >= wv) continue;
+            const T yi = V::ldg(a.Yin + i * a.ld_in + vv * VEC);
+            T out;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
+                double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
+                if (HAS_PREV) o += a.beta * V::get(yp[v], e);
+                V::set(out, e, o);
+                if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
+            }
+            if (STORE) V::stcs(a.Yout + i * a.ld_out + vv * VEC, out);
+        }
+    }
+}
+
+// Tiled fused SpMM.  A CTA of R x TX threads (rounded up to whole warps)
+// processes tiles of RT = R*RR consecutive rows.  Each tile's CSR slice is
+// staged in shared memory with coalesced loads as 16-byte {col*ld, val}
+// entries, so the only global latency left per row is the batch of Y_j
+// gathers (the row_ptr -> col -> Y chain of a plain CSR loop is paid once per
+// tile).  Thread (r, v0) owns row slot r (rows r0 + rr*R + r) and the 16-byte
+// column vectors v0, v0+TX, ... (NV of them); Y_{j-1} is prefetched with an
+// evict-first load before the gathers and Y_{j+1} is stored evict-first.
+// Tiles are visited grid-stride so the rows in flight chip-wide form one
+// contiguous window (L2 reuse of gathered neighbour rows).  Per-row sums run
+// in CSR order, so results do not depend on the partition or the tiling.
+// A tile whose slice exceeds the staging capacity is staged in several passes
+// of whole rows.
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+__global__ void __launch_bounds__(kMaxThreads, 2) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RR, int wv,
+                                                                    int64_t ntiles, int nnz_cap) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int RT = R * RR;
+    Ent *s_ent = reinterpret_cast<Ent *>(smem_raw);                      // [nnz_cap]
+    int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [RT+1] (relative)
+    __shared__ int64_t s_base;
+
     const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
     const int r = tid / TX;
     const int v0 = tid - r * TX;
     const bool active = r < R;
@@ -66,75 +157,84 @@ __global__ void __launch_bounds__(kThreads) spmm_fused_kernel(SpmmArgs a, int TX
     for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int e = 0; e < VEC; ++e) ss[v][e] = 0.0;
+    const int64_t *__restrict__ rp = a.row_ptr;
+    const int32_t *__restrict__ col = a.col;
+    const double *__restrict__ val = a.val;
+    const int64_t ld = a.ld_in;
 
-    if (active) {
-        const int64_t *__restrict__ rp = a.row_ptr;
-        const int32_t *__restrict__ col = a.col;
-        const double *__restrict__ val = a.val;
-        const double *__restrict__ Yin = a.Yin;
-        for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-            const int64_t i = g * R + r;
-            if (i >= a.n) break;
-            const int64_t p0 = rp[i];
-            const int64_t p1 = rp[i + 1];
-            T acc[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-            int64_t p = p0;
-            constexpr int U = (NV == 1) ? 4 : 2;
-            for (; p + U <= p1; p += U) {
-                int jj[U];
-                double aa[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    jj[u] = __ldg(col + p + u);
-                    aa[u] = __ldg(val + p + u);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = t * RT;
+        const int nrows = (int)min((int64_t)RT, a.n - r0);
+        int done = 0;  // rows of this tile already processed
+        while (done < nrows) {
+            __syncthreads();  // previous pass finished with the staged slice
+            if (tid == 0) s_base = __ldg(rp + r0 + done);
+            __syncthreads();
+            const int64_t base = s_base;
+            // rows [done, done+cnt) whose slice fits the capacity (at least one row)
+            for (int q = tid; q <= nrows - done; q += nthr) {
+                const int64_t o = __ldg(rp + r0 + done + q) - base;
+                s_rp[q] = o <= nnz_cap ? (int)o : nnz_cap + 1;
+            }
+            __syncthreads();
+            int cnt = 0;
+            {
+                // largest cnt with s_rp[cnt] <= nnz_cap (s_rp is nondecreasing)
+                int lo = 1, hi = nrows - done;
+                if (s_rp[1] > nnz_cap) hi = 0;
+                while (lo <= hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_rp[mid] <= nnz_cap) { cnt = mid; lo = mid + 1; } else hi = mid - 1;
                 }
-                T x[U][NV];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
+            }
+            if (cnt == 0) {
+                // a single row longer than the capacity: process it in K-chunks from global memory
+                if (active && r == 0) {
+                    const int64_t i = r0 + done;
+                    using V = Vec<VEC>;
+                    using T = typename V::T;
+                    const int64_t p0 = __ldg(rp + i), p1 = __ldg(rp + i + 1);
                     for (int v = 0; v < NV; ++v) {
                         const int vv = v0 + v * TX;
-                        x[u][v] = (vv < wv) ? V::ldg(Yin + (int64_t)jj[u] * a.ld_in + vv * VEC) : V::zero();
+                        if (vv >= wv) continue;
+                        T acc = V::zero();
+                        for (int64_t p = p0; p < p1; ++p)
+                            fma_vec<VEC>(acc, __ldg(val + p), V::ldg(a.Yin + (int64_t)__ldg(col + p) * ld + vv * VEC));
+                        const T yi = V::ldg(a.Yin + i * ld + vv * VEC);
+                        T yp = V::zero();
+                        if (HAS_PREV) yp = V::ldcs(a.Yprev + i * a.ld_prev + vv * VEC);
+                        T out;
+                        for (int e = 0; e < VEC; ++e) {
+                            const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
+                            double o = a.alpha * (V::get(acc, e) - sh * V::get(yi, e));
+                            if (HAS_PREV) o += a.beta * V::get(yp, e);
+                            V::set(out, e, o);
+                            if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
+                        }
+                        if (STORE) V::stcs(a.Yout + i * a.ld_out + vv * VEC, out);
                     }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) fma_vec<VEC>(acc[v], aa[u], x[u][v]);
-            }
-            for (; p < p1; ++p) {
-                const int j = __ldg(col + p);
-                const double av = __ldg(val + p);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int vv = v0 + v * TX;
-                    if (vv < wv) fma_vec<VEC>(acc[v], av, V::ldg(Yin + (int64_t)j * a.ld_in + vv * VEC));
                 }
+                // other row-slot threads of the block stay idle for this row
+                done += 1;
+                continue;
             }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int vv = v0 + v * TX;
-                if (vv >= wv) continue;
-                const T yi = V::ldg(Yin + i * a.ld_in + vv * VEC);
-                T yp = V::zero();
-                if (HAS_PREV) yp = V::ldcs(a.Yprev + i * a.ld_prev + vv * VEC);
-                T out;
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
-                    double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
-                    if (HAS_PREV) o += a.beta * V::get(yp, e);
-                    V::set(out, e, o);
-                    if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
-                }
-                if (STORE) V::stcs(a.Yout + i * a.ld_out + vv * VEC, out);
+            const int nnz_t = s_rp[cnt];
+            for (int q = tid; q < nnz_t; q += nthr) {
+                Ent e;
+                e.off = (int64_t)__ldg(col + base + q) * ld;
+                e.val = __ldg(val + base + q);
+                s_ent[q] = e;
             }
+            __syncthreads();
+            if (active)
+                tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
+                                                                        s_rp, s_ent, ss);
+            done += cnt;
         }
     }
     if (SUMSQ) {
-        // fixed-order block reduction over the R row-threads of each column
-        __shared__ double red[kThreads * VEC];
+        // fixed-order block reduction over the R row slots of each column
+        double *red = reinterpret_cast<double *>(smem_raw);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             __syncthreads();
@@ -147,56 +247,86 @@ __global__ void __launch_bounds__(kThreads) spmm_fused_kernel(SpmmArgs a, int TX
             if (active && r == 0 && vv < wv) {
 #pragma unroll
                 for (int e = 0; e < VEC; ++e) {
-                    double s = 0.0;
-                    for (int rr = 0; rr < R; ++rr) s += red[(rr * TX + v0) * VEC + e];
+                    double sum = 0.0;
+                    for (int q = 0; q < R; ++q) sum += red[(q * TX + v0) * VEC + e];
                     const int colid = vv * VEC + e;
-                    if (colid < a.w) a.partials[(int64_t)blockIdx.x * a.w + colid] = s;
+                    if (colid < a.w) a.partials[(int64_t)blockIdx.x * a.w + colid] = sum;
                 }
             }
         }
     }
 }
 
-template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+constexpr int kNnzCap = 2048;
+
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
-    auto kern = spmm_fused_kernel<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
-    static int occ = -1;  // per instantiation
-    if (occ < 0) {
+    auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
+    const int nthr = ((R * TX + 31) / 32) * 32;
+    const int RR = R >= 64 ? 1 : (64 + R - 1) / R;
+    const int RT = R * RR;
+    // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
+    size_t smem = sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(RT + 2);
+    const size_t red = 8 * (size_t)nthr * VEC;
+    if (smem < red) smem = red;
+    static int occ = -1;  // per instantiation (one device per process)
+    static size_t occ_smem = 0;
+    if (occ < 0 || occ_smem != smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, nthr, smem);
         occ = o > 0 ? o : 1;
+        occ_smem = smem;
     }
-    const int64_t ngroups = (a.n + R - 1) / R;
+    const int64_t ntiles = (a.n + RT - 1) / RT;
     int64_t G = (int64_t)c->num_sms * occ;
-    if (G > ngroups) G = ngroups;
+    if (G > ntiles) G = ntiles;
     if (G < 1) G = 1;
-    kern<<<(unsigned)G, kThreads, 0, c->stream>>>(a, TX, R, wv, ngroups);
+    kern<<<(unsigned)G, nthr, smem, c->stream>>>(a, TX, R, RR, wv, ntiles, kNnzCap);
     c->launches++;
     return (int)G;
 }
 
-template <int VEC, int NV>
+template <int VEC, int NV, int K>
 int dispatch_flags(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     const bool prev = a.Yprev != nullptr, store = a.Yout != nullptr, ss = a.partials != nullptr,
                cs = a.colshift != nullptr;
-    if (prev && store && !ss && !cs) return launch_t<VEC, NV, true, true, false, false>(c, a, TX, R, wv);
-    if (prev && store && ss && !cs) return launch_t<VEC, NV, true, true, true, false>(c, a, TX, R, wv);
-    if (!prev && store && !ss && !cs) return launch_t<VEC, NV, false, true, false, false>(c, a, TX, R, wv);
-    if (!prev && store && ss && !cs) return launch_t<VEC, NV, false, true, true, false>(c, a, TX, R, wv);
-    if (!prev && !store && ss && cs) return launch_t<VEC, NV, false, false, true, true>(c, a, TX, R, wv);
+    if (prev && store && !ss && !cs) return launch_t<VEC, NV, K, true, true, false, false>(c, a, TX, R, wv);
+    if (prev && store && ss && !cs) return launch_t<VEC, NV, K, true, true, true, false>(c, a, TX, R, wv);
+    if (!prev && store && !ss && !cs) return launch_t<VEC, NV, K, false, true, false, false>(c, a, TX, R, wv);
+    if (!prev && store && ss && !cs) return launch_t<VEC, NV, K, false, true, true, false>(c, a, TX, R, wv);
+    if (!prev && !store && ss && cs) return launch_t<VEC, NV, K, false, false, true, true>(c, a, TX, R, wv);
     return -1;
 }
 
+// Chunk size K from the longest row: whole rows in one chunk for the 3-, 5-
+// and 7-point stencils, 3 chunks of 9 for the 27-point stencil, chunks of 8
+// otherwise (irregular rows).
 template <int VEC>
 int dispatch_nv(arr_ctx *c, const SpmmArgs &a) {
     const int wv = (a.w + VEC - 1) / VEC;
-    const int TX = wv < kThreads ? wv : kThreads;
-    const int R = kThreads / TX;
+    const int TX = wv < kMaxThreads ? wv : kMaxThreads;
+    const int R = kMaxThreads / TX;
     const int nv = (wv + TX - 1) / TX;
-    if (nv == 1) return dispatch_flags<VEC, 1>(c, a, TX, R, wv);
-    if (nv == 2) return dispatch_flags<VEC, 2>(c, a, TX, R, wv);
-    if (nv <= 4) return dispatch_flags<VEC, 4>(c, a, TX, R, wv);
+    const int L = c->max_row_nnz;
+    if (nv == 1) {
+        if (L <= 3) return dispatch_flags<VEC, 1, 3>(c, a, TX, R, wv);
+        if (L <= 5) return dispatch_flags<VEC, 1, 5>(c, a, TX, R, wv);
+        if (L <= 7) return dispatch_flags<VEC, 1, 7>(c, a, TX, R, wv);
+        if (L % 9 == 0) return dispatch_flags<VEC, 1, 9>(c, a, TX, R, wv);
+        return dispatch_flags<VEC, 1, 8>(c, a, TX, R, wv);
+    }
+    if (nv == 2) return dispatch_flags<VEC, 2, 4>(c, a, TX, R, wv);
+    if (nv <= 4) return dispatch_flags<VEC, 4, 2>(c, a, TX, R, wv);
     return -1;
+}
+
+__global__ void rowlen_max_kernel(const int64_t *__restrict__ rp, int64_t n, int *out) {
+    int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        { const int64_t L = rp[i + 1] - rp[i]; m = max(m, L > (1 << 30) ? (1 << 30) : (int)L); }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);  // integer max: order independent
 }
 
 __global__ void colnorm_finalize_kernel(const double *__restrict__ part, int nblk, int w,
@@ -280,6 +410,15 @@ __global__ void copy_rows_kernel(const double *__restrict__ src, int64_t lds, do
 bool vec2_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
 
 }  // namespace
+
+void launch_rowlen_max(arr_ctx *c, int *dev_out) {
+    cudaMemsetAsync(dev_out, 0, sizeof(int), c->stream);
+    int64_t blocks = (c->A.n + 255) / 256;
+    if (blocks > (int64_t)c->num_sms * 4) blocks = (int64_t)c->num_sms * 4;
+    if (blocks < 1) blocks = 1;
+    rowlen_max_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.n, dev_out);
+    c->launches++;
+}
 
 int launch_spmm(arr_ctx *c, const SpmmArgs &a) {
     bool v2 = (a.w % 2 == 0) && vec2_ok(a.Yin, a.ld_in);

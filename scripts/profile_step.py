@@ -1,0 +1,58 @@
+"""Short driver for ncu: warm up, then run ONE filter_step (d degree launches),
+ONE arr_project and ONE residuals pass of a config's hot path.
+
+    python scripts/profile_step.py [--config 2] [--reps 1]
+"""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from synth import configs  # noqa: E402
+import paper_1507_06078_b200 as arr  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--k", type=int, default=None, help="override block width (filter only)")
+    ap.add_argument("--filter-only", action="store_true")
+    args = ap.parse_args()
+    A, spec = configs.build_config(args.config)
+    k = args.k or spec.k
+    X0 = synth.gaussian_block_rows(A.n, k, spec.seed, 0, A.n) if A.n * k < 2e9 else None
+    ctx = arr.eig_init(arr.to_device_csr(A), k, spec.p if not args.filter_only else 0, spec.d)
+    X = torch.from_numpy(X0).cuda()
+    a = ctx.eig_gershgorin_lower()
+    ctx.eig_set_interval(a, a + 0.9 * (float(A.val.max()) * 2 - a))
+    Y = torch.empty_like(X)
+    for _ in range(args.warmup):
+        ctx.filter_step(X, normalize=True)
+        if not args.filter_only:
+            ritz, _ = ctx.arr_project(X, Y)
+            ctx.residuals(Y, ritz[:k])
+    torch.cuda.synchronize()
+    ctx.eig_set_timing(True)
+    t = time.perf_counter()
+    for _ in range(args.reps):
+        ctx.filter_step(X, normalize=True)
+        if not args.filter_only:
+            ritz, _ = ctx.arr_project(X, Y)
+            ctx.residuals(Y, ritz[:k])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t
+    ms, cnt = ctx.eig_phase_times()
+    print(f"config {spec.name} k={k}: wall {wall*1e3:.2f} ms; filter {ms[0]:.3f} ms / {cnt[0]} degree launches "
+          f"({ms[0]/max(cnt[0],1)*1e3:.1f} us each); arr {ms[1]:.3f} ms / {cnt[1]}; residuals {ms[2]:.3f} ms / {cnt[2]}")
+
+
+if __name__ == "__main__":
+    main()
