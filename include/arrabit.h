@@ -105,6 +105,16 @@ arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out);
 /* Set the damped interval [a,b] (Eq. rhod):
  * c = (a+b)/2, e = (b-a)/2.  a >= b -> ARR_EINVAL. */
 arr_status eig_set_interval(arr_ctx *c, double a, double b);
+/* Optional processing order of the rows of A for every SpMM of this context
+ * (results are unchanged: only the order in which rows are computed moves,
+ * to shorten the L2 reuse distance of gathered rows).  Tile t is
+ * the contiguous row range [tile_row0[t], tile_row0[t] + tile_len[t]),
+ * 1 <= tile_len[t] <= 64; tiles are processed in increasing t.  The tiles must
+ * cover every row exactly once (checked here with a device pass over the
+ * scratch block; ARR_EINVAL otherwise; synchronises the stream).  Device
+ * arrays, borrowed (must outlive the context or the next call).
+ * tile_row0 == NULL restores natural order. */
+arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles);
 /* Change the degree d used by filter_step (1 <= d). */
 arr_status eig_set_degree(arr_ctx *c, int32_t d);
 

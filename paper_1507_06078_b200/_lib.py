@@ -18,7 +18,7 @@ EXPORTED = [
     "eig_init", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
-    "eig_set_timing", "eig_phase_times",
+    "eig_set_timing", "eig_phase_times", "eig_set_schedule",
 ]
 
 
@@ -62,6 +62,7 @@ def load(path: str = LIB_PATH):
         "eig_set_interval": ([vp, f64, f64], ctypes.c_int),
         "eig_set_degree": ([vp, i32], ctypes.c_int),
         "eig_set_timing": ([vp, i32], ctypes.c_int),
+        "eig_set_schedule": ([vp, vp, vp, i64], ctypes.c_int),
         "eig_phase_times": ([vp, pf64, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "filter_step": ([vp, vp, i64, i32, vp], ctypes.c_int),
         "spmm": ([vp, f64, f64, vp, i64, vp, i64, i32], ctypes.c_int),

@@ -116,6 +116,18 @@ class EigContext:
     def eig_set_interval(self, a: float, b: float):
         self._check(self.lib.eig_set_interval(self.h, float(a), float(b)), "eig_set_interval")
 
+    def eig_set_schedule(self, tile_row0: np.ndarray | None, tile_len: np.ndarray | None = None):
+        """Processing order of row tiles (see include/arrabit.h); None = natural order."""
+        if tile_row0 is None:
+            self._sched = None
+            self._check(self.lib.eig_set_schedule(self.h, None, None, 0), "eig_set_schedule")
+            return
+        r0 = torch.from_numpy(np.ascontiguousarray(tile_row0, dtype=np.int64)).to(self.A.row_ptr.device)
+        ln = torch.from_numpy(np.ascontiguousarray(tile_len, dtype=np.int32)).to(self.A.row_ptr.device)
+        self._sched = (r0, ln)  # keep the borrowed arrays alive
+        self._check(self.lib.eig_set_schedule(self.h, ctypes.c_void_p(r0.data_ptr()), ctypes.c_void_p(ln.data_ptr()),
+                                              int(r0.numel())), "eig_set_schedule")
+
     def eig_set_degree(self, d: int):
         self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
         self.d = d

@@ -299,6 +299,7 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
         {(void **)&c->evals, sizeof(double) * (size_t)m},
         {(void **)&c->vecw, sizeof(double) * 3 * (size_t)mm},
         {(void **)&c->dinfo, sizeof(int) * 64},
+        {(void **)&c->sched, sizeof(unsigned long long) * 2},
     };
     size_t total = 0;
     for (auto &x : al) {
@@ -310,6 +311,7 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
         total += x.bytes;
     }
     cudaMemsetAsync(c->dinfo, 0, sizeof(int) * 64, c->stream);
+    cudaMemsetAsync(c->sched, 0, sizeof(unsigned long long) * 2, c->stream);
     if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) { eig_destroy(c); return ARR_ECUSOLVER; }
     cusolverDnSetStream(c->solver, c->stream);
     int lwork = 0;
@@ -351,7 +353,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->solver_work};
+    void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -382,6 +384,23 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b) {
     GUARD(c);
     if (!(a < b) || !isfinite(a) || !isfinite(b)) return fail(c, ARR_EINVAL, "interval needs finite a < b");
     c->a = a; c->b = b; c->have_interval = true;
+    return ARR_OK;
+}
+
+arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles) {
+    GUARD(c);
+    if (!tile_row0) {
+        c->tile_row0 = nullptr; c->tile_len = nullptr; c->ntiles = 0;
+        return ARR_OK;
+    }
+    if (!tile_len || ntiles < 1) return fail(c, ARR_EINVAL, "schedule: null lengths or no tiles");
+    int *marks = reinterpret_cast<int *>(c->T);  // scratch block holds >= n ints
+    launch_schedule_check(c, tile_row0, tile_len, ntiles, marks, c->dinfo + INFO_BAD);
+    CHECK_LAUNCH();
+    CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->h_istage[0]) return fail(c, ARR_EINVAL, "schedule does not cover every row exactly once with tiles of 1..64 rows");
+    c->tile_row0 = tile_row0; c->tile_len = tile_len; c->ntiles = ntiles;
     return ARR_OK;
 }
 

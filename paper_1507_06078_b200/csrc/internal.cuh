@@ -30,6 +30,10 @@ struct arr_ctx {
     double *evals;    // [m]
     double *vecw;     // [2*ARR_MAX_W] column norms / shifts / scales
     int *dinfo;       // cuSOLVER info + rank counters
+    unsigned long long *sched;  // [2] SpMM tile ticket (zeroed at init, self-resetting)
+    const int64_t *tile_row0;   // eig_set_schedule (borrowed device arrays) or nullptr
+    const int32_t *tile_len;
+    int64_t ntiles;
     double *solver_work;
     int solver_lwork;
     cusolverDnHandle_t solver;
@@ -68,6 +72,10 @@ struct SpmmArgs {
     double alpha, shift, beta;
     const double *colshift;  // per-column shift (overrides shift) or nullptr
     double *partials;        // [gridDim.x * w] column sums of squares of the output, or nullptr
+    unsigned long long *sched;  // [2] dynamic tile ticket + finished-CTA count (self-resetting)
+    const int64_t *tile_row0;   // optional processing order: tile t = rows [tile_row0[t], +tile_len[t])
+    const int32_t *tile_len;
+    int64_t ntiles;
 };
 
 // Launch the fused SpMM: Yout = alpha*(A Yin - shift*Yin) + beta*Yprev.
@@ -81,6 +89,9 @@ void launch_scale_cols(arr_ctx *c, const double *In, int64_t ld_in, double *Out,
                        int64_t n, int32_t w, const double *norms);
 void launch_gershgorin(arr_ctx *c, double *partial, int *nblk_out);
 void launch_rowlen_max(arr_ctx *c, int *dev_out);
+// exact-cover check of a schedule: bad = 1 unless every row is covered once
+void launch_schedule_check(arr_ctx *c, const int64_t *row0, const int32_t *len, int64_t ntiles, int *marks,
+                           int *bad);
 void launch_min_finalize(arr_ctx *c, const double *partial, int nblk, double *out);
 
 // ---------------------------------------------------------------- dense (DMMA)

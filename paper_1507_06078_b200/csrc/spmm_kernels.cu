@@ -13,7 +13,42 @@ namespace {
 #ifndef ARR_SPMM_U
 #define ARR_SPMM_U 8  // gathers in flight per row (single column-vector case)
 #endif
-constexpr int kMaxThreads = 512;  // fused SpMM CTA size (R x TX rounded to warps)
+#ifndef ARR_SPMM_MAXT
+#define ARR_SPMM_MAXT 512
+#endif
+#ifndef ARR_SPMM_MINB
+#define ARR_SPMM_MINB 2
+#endif
+#ifndef ARR_SPMM_PAIR
+#define ARR_SPMM_PAIR 0
+#endif
+constexpr int kMaxThreads = ARR_SPMM_MAXT;  // fused SpMM CTA size (R x TX rounded to warps)
+
+#ifndef ARR_L2HINT
+#define ARR_L2HINT 1  // L2 eviction-priority hints: gathers evict_last, streams evict_first
+#endif
+
+// Cache-policy handles (createpolicy) and hinted 64/128-bit accesses.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+#if ARR_L2HINT
+#define GATHER(p) V::ldg_h((p), pol_keep)
+#define STREAM_LD(p) V::ldcs_h((p), pol_stream)
+#define STREAM_ST(p, v) V::stcs_h((p), (v), pol_stream)
+#else
+#define GATHER(p) V::ldg(p)
+#define STREAM_LD(p) V::ldcs(p)
+#define STREAM_ST(p, v) V::stcs((p), (v))
+#endif
 
 template <int VEC>
 struct Vec;
@@ -24,6 +59,19 @@ struct Vec<1> {
     static __device__ __forceinline__ T ldg(const double *p) { return __ldg(p); }
     static __device__ __forceinline__ T ldcs(const double *p) { return __ldcs(p); }
     static __device__ __forceinline__ void stcs(double *p, T v) { __stcs(p, v); }
+    static __device__ __forceinline__ T ldg_h(const double *p, uint64_t pol) {
+        double r;
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ T ldcs_h(const double *p, uint64_t pol) {
+        double r;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ void stcs_h(double *p, T v, uint64_t pol) {
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+    }
     static __device__ __forceinline__ double get(const T &v, int) { return v; }
     static __device__ __forceinline__ void set(T &v, int, double x) { v = x; }
 };
@@ -34,6 +82,23 @@ struct Vec<2> {
     static __device__ __forceinline__ T ldg(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
     static __device__ __forceinline__ T ldcs(const double *p) { return __ldcs(reinterpret_cast<const double2 *>(p)); }
     static __device__ __forceinline__ void stcs(double *p, T v) { __stcs(reinterpret_cast<double2 *>(p), v); }
+    static __device__ __forceinline__ T ldg_h(const double *p, uint64_t pol) {
+        double2 r;
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ T ldcs_h(const double *p, uint64_t pol) {
+        double2 r;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                     : "=d"(r.x), "=d"(r.y)
+                     : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ void stcs_h(double *p, T v, uint64_t pol) {
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
+                     "d"(v.y), "l"(pol)
+                     : "memory");
+    }
     static __device__ __forceinline__ double get(const T &v, int e) { return e ? v.y : v.x; }
     static __device__ __forceinline__ void set(T &v, int e, double x) {
         if (e) v.y = x; else v.x = x;
@@ -50,77 +115,133 @@ __device__ __forceinline__ void fma_vec<2>(double2 &acc, double a, const double2
     acc.y = fma(a, x.y, acc.y);
 }
 
+constexpr int kTile = 64;  // rows per tile (the unit of the processing order)
+
 // One staged non-zero: element offset of the referenced Y row and the value.
 struct __align__(16) Ent {
     int64_t off;  // col * ld_in
     double val;
 };
 
+// Epilogue of one row: out = alpha*(acc - shift*y_i) + beta*y_prev, column
+// sums of squares, evict-first store.
+template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+__device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int TX, int v0, int wv,
+                                             const typename Vec<VEC>::T (&acc)[NV],
+                                             const typename Vec<VEC>::T (&yp)[NV], double (&ss)[NV][VEC],
+                                             uint64_t pol_stream) {
+    using V = Vec<VEC>;
+    using T = typename V::T;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int vv = v0 + v * TX;
+        if (vv >= wv) continue;
+        const T yi = V::ldg(a.Yin + i * a.ld_in + vv * VEC);
+        T out;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
+            double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
+            if (HAS_PREV) o += a.beta * V::get(yp[v], e);
+            V::set(out, e, o);
+            if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
+        }
+        if (STORE) STREAM_ST(a.Yout + i * a.ld_out + vv * VEC, out);
+    }
+}
+
 // Rows of one tile owned by row slot r.  Each row is processed in chunks of K
-// non-zeros: the K {offset, value} entries come from shared memory with one
-// 128-bit LDS each, the K gathers of Y_j are issued back to back (all in
-// flight together), then K FMAs in CSR order.  Slots past the row end are
-// predicated by value 0 and re-read the row's first entry (no branches).
+// non-zeros: the K row offsets come from shared memory, the K gathers of Y_j
+// are issued back to back (all in flight together), then the values are read
+// from shared memory and K FMAs run in CSR order.  Slots past the row end
+// re-gather the row's first entry with value 0 (no branches).  When every row
+// fits one chunk (K >= longest row) two rows are kept in flight per thread.
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nrows, int R, int RR, int r, int TX,
                                           int v0, int wv, const int *s_rp, const Ent *s_ent,
-                                          double (&ss)[NV][VEC]) {
+                                          double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream) {
     using V = Vec<VEC>;
     using T = typename V::T;
+    constexpr int P = (ARR_SPMM_PAIR && NV == 1 && K <= 7) ? 2 : 1;  // rows in flight per thread
     const double *yin_v[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const int vv = v0 + v * TX;
         yin_v[v] = a.Yin + (vv < wv ? vv : 0) * VEC;
     }
-    for (int rr = 0; rr < RR; ++rr) {
-        const int lr = rr * R + r;
-        if (lr >= nrows) break;
-        const int64_t i = r0 + lr;
-        T yp[NV];
-        if (HAS_PREV) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int vv = v0 + v * TX;
-                yp[v] = (vv < wv) ? V::ldcs(a.Yprev + i * a.ld_prev + vv * VEC) : V::zero();
+    if constexpr (P == 2) {
+        for (int rr = 0; rr < RR; rr += 2) {
+            const int lr0 = rr * R + r, lr1 = lr0 + R;
+            if (lr0 >= nrows) break;
+            const bool has1 = (rr + 1 < RR) && (lr1 < nrows);
+            const int64_t i0 = r0 + lr0, i1 = r0 + (has1 ? lr1 : lr0);
+            T yp0[NV], yp1[NV];
+            if (HAS_PREV) {
+                yp0[0] = STREAM_LD(a.Yprev + i0 * a.ld_prev + v0 * VEC);
+                yp1[0] = has1 ? STREAM_LD(a.Yprev + i1 * a.ld_prev + v0 * VEC) : V::zero();
             }
-        }
-        const int p0 = s_rp[lr];
-        const int p1 = s_rp[lr + 1];
-        T acc[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = V::zero();
-        for (int p = p0; p < p1; p += K) {
-            T x[K][NV];
-            double av[K];
+            const int p00 = s_rp[lr0], p01 = s_rp[lr0 + 1];
+            const int p10 = has1 ? s_rp[lr1] : p01, p11 = has1 ? s_rp[lr1 + 1] : p01;
+            const int64_t safe0 = p00 < p01 ? s_ent[p00].off : i0 * a.ld_in;
+            const int64_t safe1 = p10 < p11 ? s_ent[p10].off : i1 * a.ld_in;
+            T x0[K], x1[K];
 #pragma unroll
             for (int u = 0; u < K; ++u) {
-                const bool ok = p + u < p1;
-                const Ent e = s_ent[ok ? p + u : p0];
-                av[u] = ok ? e.val : 0.0;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) x[u][v] = V::ldg(yin_v[v] + e.off);
+                const int64_t o0 = (p00 + u < p01) ? s_ent[p00 + u].off : safe0;
+                const int64_t o1 = (p10 + u < p11) ? s_ent[p10 + u].off : safe1;
+                x0[u] = GATHER(yin_v[0] + o0);
+                x1[u] = GATHER(yin_v[0] + o1);
             }
+            T acc0[NV], acc1[NV];
+            acc0[0] = V::zero();
+            acc1[0] = V::zero();
 #pragma unroll
-            for (int u = 0; u < K; ++u)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) fma_vec<VEC>(acc[v], av[u], x[u][v]);
+            for (int u = 0; u < K; ++u) {
+                const double a0 = (p00 + u < p01) ? s_ent[p00 + u].val : 0.0;
+                const double a1 = (p10 + u < p11) ? s_ent[p10 + u].val : 0.0;
+                fma_vec<VEC>(acc0[0], a0, x0[u]);
+                fma_vec<VEC>(acc1[0], a1, x1[u]);
+            }
+            if (v0 < wv) {
+                row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i0, TX, v0, wv, acc0, yp0, ss, pol_stream);
+                if (has1) row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i1, TX, v0, wv, acc1, yp1, ss, pol_stream);
+            }
         }
+    } else {
+        for (int rr = 0; rr < RR; ++rr) {
+            const int lr = rr * R + r;
+            if (lr >= nrows) break;
+            const int64_t i = r0 + lr;
+            T yp[NV];
+            if (HAS_PREV) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int vv = v0 + v * TX;
-            if (vv >= wv) continue;
-            const T yi = V::ldg(a.Yin + i * a.ld_in + vv * VEC);
-            T out;
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
-                double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
-                if (HAS_PREV) o += a.beta * V::get(yp[v], e);
-                V::set(out, e, o);
-                if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
+                for (int v = 0; v < NV; ++v) {
+                    const int vv = v0 + v * TX;
+                    yp[v] = (vv < wv) ? STREAM_LD(a.Yprev + i * a.ld_prev + vv * VEC) : V::zero();
+                }
             }
-            if (STORE) V::stcs(a.Yout + i * a.ld_out + vv * VEC, out);
+            const int p0 = s_rp[lr];
+            const int p1 = s_rp[lr + 1];
+            T acc[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = V::zero();
+            for (int p = p0; p < p1; p += K) {
+                T x[K][NV];
+                const int64_t safe = s_ent[p].off;
+#pragma unroll
+                for (int u = 0; u < K; ++u) {
+                    const int64_t o = (p + u < p1) ? s_ent[p + u].off : safe;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) x[u][v] = GATHER(yin_v[v] + o);
+                }
+#pragma unroll
+                for (int u = 0; u < K; ++u) {
+                    const double av = (p + u < p1) ? s_ent[p + u].val : 0.0;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fma_vec<VEC>(acc[v], av, x[u][v]);
+                }
+            }
+            row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i, TX, v0, wv, acc, yp, ss, pol_stream);
         }
     }
 }
@@ -139,10 +260,10 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
 // A tile whose slice exceeds the staging capacity is staged in several passes
 // of whole rows.
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
-__global__ void __launch_bounds__(kMaxThreads, 2) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RR, int wv,
+__global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RR, int wv,
                                                                     int64_t ntiles, int nnz_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int RT = R * RR;
+    const int RT = kTile;
     Ent *s_ent = reinterpret_cast<Ent *>(smem_raw);                      // [nnz_cap]
     int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [RT+1] (relative)
     __shared__ int64_t s_base;
@@ -161,10 +282,25 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmm_tile_kernel(SpmmArgs a, i
     const int32_t *__restrict__ col = a.col;
     const double *__restrict__ val = a.val;
     const int64_t ld = a.ld_in;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
 
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = t * RT;
-        const int nrows = (int)min((int64_t)RT, a.n - r0);
+    // Tile order: launches without a column reduction hand tiles out in order
+    // from an atomic ticket (CTAs cannot drift apart, so the rows in flight stay
+    // one contiguous window); SUMSQ launches keep the static grid-stride
+    // assignment so their per-CTA partial sums are deterministic.
+    constexpr bool DYN = !SUMSQ;
+    __shared__ int64_t s_next;
+    for (int64_t t = blockIdx.x; t < ntiles;) {
+        int64_t r0;
+        int nrows;
+        if (a.tile_row0) {  // caller-given processing order of contiguous row ranges
+            r0 = a.tile_row0[t];
+            nrows = a.tile_len[t];
+        } else {
+            r0 = t * RT;
+            nrows = (int)min((int64_t)RT, a.n - r0);
+        }
         int done = 0;  // rows of this tile already processed
         while (done < nrows) {
             __syncthreads();  // previous pass finished with the staged slice
@@ -228,8 +364,25 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmm_tile_kernel(SpmmArgs a, i
             __syncthreads();
             if (active)
                 tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
-                                                                        s_rp, s_ent, ss);
+                                                                        s_rp, s_ent, ss, pol_keep, pol_stream);
             done += cnt;
+        }
+        if (DYN) {
+            __syncthreads();
+            if (tid == 0) s_next = (int64_t)gridDim.x + (int64_t)atomicAdd(a.sched, 1ull);
+            __syncthreads();
+            t = s_next;
+        } else {
+            t += gridDim.x;
+        }
+    }
+    if (DYN && tid == 0) {
+        // the last CTA to finish resets the ticket for the next launch
+        __threadfence();
+        if (atomicAdd(a.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+            a.sched[0] = 0;
+            a.sched[1] = 0;
+            __threadfence();
         }
     }
     if (SUMSQ) {
@@ -263,8 +416,8 @@ template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool CO
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
     const int nthr = ((R * TX + 31) / 32) * 32;
-    const int RR = R >= 64 ? 1 : (64 + R - 1) / R;
-    const int RT = R * RR;
+    const int RR = R >= kTile ? 1 : (kTile + R - 1) / R;
+    const int RT = kTile;
     // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
     size_t smem = sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(RT + 2);
     const size_t red = 8 * (size_t)nthr * VEC;
@@ -278,7 +431,7 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
         occ = o > 0 ? o : 1;
         occ_smem = smem;
     }
-    const int64_t ntiles = (a.n + RT - 1) / RT;
+    const int64_t ntiles = a.tile_row0 ? a.ntiles : (a.n + RT - 1) / RT;
     int64_t G = (int64_t)c->num_sms * occ;
     if (G > ntiles) G = ntiles;
     if (G < 1) G = 1;
@@ -420,7 +573,14 @@ void launch_rowlen_max(arr_ctx *c, int *dev_out) {
     c->launches++;
 }
 
-int launch_spmm(arr_ctx *c, const SpmmArgs &a) {
+int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
+    SpmmArgs a = a_in;
+    a.sched = c->sched;
+    if (c->tile_row0 && a.n == c->A.n) {
+        a.tile_row0 = c->tile_row0;
+        a.tile_len = c->tile_len;
+        a.ntiles = c->ntiles;
+    }
     bool v2 = (a.w % 2 == 0) && vec2_ok(a.Yin, a.ld_in);
     if (a.Yprev) v2 = v2 && vec2_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
@@ -478,4 +638,35 @@ void launch_copy_rows(arr_ctx *c, const double *src, int64_t lds, double *dst, i
     if (blocks < 1) blocks = 1;
     copy_rows_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(src, lds, dst, ldd, n, w);
     c->launches++;
+}
+
+// ---------------------------------------------------------------- schedule check
+namespace {
+__global__ void sched_mark_kernel(const int64_t *row0, const int32_t *len, int64_t ntiles, int64_t n, int *marks,
+                                  int *bad) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row0[t];
+        const int l = len[t];
+        if (l < 1 || l > kTile || r < 0 || r + l > n) {
+            atomicOr(bad, 1);
+            continue;
+        }
+        for (int q = 0; q < l; ++q) atomicAdd(marks + r + q, 1);
+    }
+}
+__global__ void sched_verify_kernel(const int *marks, int64_t n, int *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (marks[i] != 1) atomicOr(bad, 1);
+}
+}  // namespace
+
+void launch_schedule_check(arr_ctx *c, const int64_t *row0, const int32_t *len, int64_t ntiles, int *marks,
+                           int *bad) {
+    cudaMemsetAsync(marks, 0, sizeof(int) * (size_t)c->A.n, c->stream);
+    cudaMemsetAsync(bad, 0, sizeof(int), c->stream);
+    const unsigned g = (unsigned)c->num_sms * 4;
+    sched_mark_kernel<<<g, 256, 0, c->stream>>>(row0, len, ntiles, c->A.n, marks, bad);
+    sched_verify_kernel<<<g, 256, 0, c->stream>>>(marks, c->A.n, bad);
+    c->launches += 2;
 }

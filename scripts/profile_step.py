@@ -25,12 +25,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--k", type=int, default=None, help="override block width (filter only)")
     ap.add_argument("--filter-only", action="store_true")
+    ap.add_argument("--size", type=int, default=None, help="override the generator size (grid edge or n)")
+    ap.add_argument("--band", type=int, default=0, help="3-D y-band schedule height (0 natural, -1 auto)")
     args = ap.parse_args()
-    A, spec = configs.build_config(args.config)
+    spec = configs.CONFIGS[args.config]
+    if args.size:
+        import dataclasses
+        spec = dataclasses.replace(spec, size=args.size, name=f"{spec.name}@{args.size}")
+    A, spec = configs.build_config(spec)
     k = args.k or spec.k
     X0 = synth.gaussian_block_rows(A.n, k, spec.seed, 0, A.n) if A.n * k < 2e9 else None
     ctx = arr.eig_init(arr.to_device_csr(A), k, spec.p if not args.filter_only else 0, spec.d)
     X = torch.from_numpy(X0).cuda()
+    if args.band and spec.kind in ("lap3dV", "st27"):
+        from paper_1507_06078_b200 import schedule
+        N = spec.size
+        by = schedule.auto_band(N, N, k) if args.band < 0 else args.band
+        ctx.eig_set_schedule(*schedule.yband_3d(N, N, N, by))
+        print(f"y-band schedule by={by}")
     a = ctx.eig_gershgorin_lower()
     ctx.eig_set_interval(a, a + 0.9 * (float(A.val.max()) * 2 - a))
     Y = torch.empty_like(X)
