@@ -83,6 +83,11 @@ typedef struct {
  * (Alg. ARR input), n < 2^31.  stream: cudaStream_t or NULL.
  * Allocates the workspace described above (ARR_ENOMEM if it does not fit). */
 arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream);
+/* Same with an explicit block width w >= k: w - k guard vectors (P:1291-1299,
+ * "the number of columns in iterate matrix X to k+q"); (p+1)w < n.  Blocks
+ * passed to filter_step / arr_project / eig_solve are then n x w; residuals and
+ * the stop rule use the k leading pairs; b = mu_{w+1}. */
+arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w, int32_t p, int32_t d, void *stream);
 arr_status eig_destroy(arr_ctx *c);
 const char *eig_last_error(const arr_ctx *c);
 size_t eig_workspace_bytes(const arr_ctx *c);
@@ -93,8 +98,10 @@ uint64_t eig_launch_count(const arr_ctx *c);
  * syncs the calls already make).  on != 0 enables it and zeroes the totals.
  * eig_phase_times synchronises the stream and returns, for phase
  * 0 = filter degree kernels (the d fused SpMM launches of each filter_step),
- * 1 = arr_project, 2 = residuals: ms[3] total device milliseconds and
- * counts[3] (phase 0: degree launches; 1, 2: calls). */
+ * 1 = arr_project, 2 = residuals, and the parts of arr_project 3 = building
+ * the orthonormal block-Krylov basis, 4 = H = Q^T A Q, 5 = small dense eig:
+ * ms[6] total device milliseconds and counts[6] (phase 0: degree launches;
+ * others: calls). */
 arr_status eig_set_timing(arr_ctx *c, int32_t on);
 arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts);
 
@@ -189,11 +196,12 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                      double *eigval_host, double *res_host, arr_solve_info *info);
 
 /* Host-buffer convenience entry (the public "e2e" call): copies the CSR and X0
- * from host memory to the device, runs eig_solve on a fresh context, copies the
- * k eigenvalues, residuals and eigenvectors (n x k, row-major, ld = k) back.
+ * (n x w, row-major, ld = w; w >= k, w - k guard columns) from host memory to
+ * the device, runs eig_solve on a fresh context, copies the k eigenvalues,
+ * residuals and eigenvectors (n x k, row-major, ld = k; evec may be NULL) back.
  * All host pointers; device memory is allocated and freed inside. */
 arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
-                          const double *val, int32_t k, int32_t p, int32_t d, const double *X0,
+                          const double *val, int32_t k, int32_t w, int32_t p, int32_t d, const double *X0,
                           const arr_solve_opts *opts, double *eigval, double *res, double *evec,
                           arr_solve_info *info, void *stream);
 

@@ -236,7 +236,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
               b := mu_{w+1};  X := Y[:, :w]
     """
     n = A.n
-    w = k if w is None else w
+    w = X0.shape[1] if w is None else w  # w - k guard vectors (P:1291-1299)
     X = np.array(X0[:, :w], dtype=np.float64, copy=True)
     a = gershgorin_lower(A)
     mu0, _, _ = rayleigh_ritz(A, X)

@@ -15,7 +15,7 @@ STATUS_NAMES = {0: "ARR_OK", 1: "ARR_EINVAL", 2: "ARR_ENOMEM", 3: "ARR_ECUDA", 5
 
 # Every symbol include/arrabit.h declares (checked by tests/test_abi.py).
 EXPORTED = [
-    "eig_init", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
+    "eig_init", "eig_init_w", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
     "eig_set_timing", "eig_phase_times", "eig_set_schedule",
@@ -54,6 +54,7 @@ def load(path: str = LIB_PATH):
     pi32 = ctypes.POINTER(ctypes.c_int32)
     sig = {
         "eig_init": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, vp], ctypes.c_int),
+        "eig_init_w": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, vp], ctypes.c_int),
         "eig_destroy": ([vp], ctypes.c_int),
         "eig_last_error": ([vp], ctypes.c_char_p),
         "eig_workspace_bytes": ([vp], ctypes.c_size_t),
@@ -74,7 +75,7 @@ def load(path: str = LIB_PATH):
         "residuals": ([vp, vp, i64, pf64, i32, pf64], ctypes.c_int),
         "eig_solve": ([vp, vp, i64, ctypes.POINTER(arr_solve_opts), pf64, pf64,
                        ctypes.POINTER(arr_solve_info)], ctypes.c_int),
-        "eig_solve_host": ([i64, i64, vp, vp, vp, i32, i32, i32, vp, ctypes.POINTER(arr_solve_opts), pf64, pf64,
+        "eig_solve_host": ([i64, i64, vp, vp, vp, i32, i32, i32, i32, vp, ctypes.POINTER(arr_solve_opts), pf64, pf64,
                             vp, ctypes.POINTER(arr_solve_info), vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():

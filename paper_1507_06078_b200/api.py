@@ -58,14 +58,15 @@ def _stream_handle(stream):
 class EigContext:
     """An arr_ctx (eig_init ... eig_destroy)."""
 
-    def __init__(self, A: DeviceCSR, k: int, p: int, d: int, stream=None):
+    def __init__(self, A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None):
         self.lib = _lib.load()
         self.A = A  # keep the borrowed arrays alive
         self.k, self.p, self.d = k, p, d
+        self.w = k if w is None else w
         self.handle_stream, self.stream = _stream_handle(stream)
         self._csr = arr_csr(A.n, A.nnz, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.val.data_ptr())
         h = ctypes.c_void_p()
-        st = self.lib.eig_init(ctypes.byref(h), ctypes.byref(self._csr), k, p, d, self.handle_stream)
+        st = self.lib.eig_init_w(ctypes.byref(h), ctypes.byref(self._csr), k, self.w, p, d, self.handle_stream)
         if st != 0:
             raise ArrError(st, "eig_init failed")
         self.h = h
@@ -99,9 +100,10 @@ class EigContext:
         self._check(self.lib.eig_set_timing(self.h, 1 if on else 0), "eig_set_timing")
 
     def eig_phase_times(self):
-        """(ms[3], counts[3]) for phases filter-degrees / arr_project / residuals."""
-        ms = np.zeros(3)
-        cnt = np.zeros(3, dtype=np.int64)
+        """(ms[6], counts[6]) for phases filter-degrees / arr_project / residuals /
+        arr.basis / arr.H / arr.eig (see include/arrabit.h)."""
+        ms = np.zeros(6)
+        cnt = np.zeros(6, dtype=np.int64)
         self._check(self.lib.eig_phase_times(self.h, ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                              cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
                     "eig_phase_times")
@@ -178,7 +180,7 @@ class EigContext:
             py, ldy, _ = _blk(Y, "Y")
         else:
             py, ldy = None, 0
-        ritz = np.empty((p + 1) * self.k)
+        ritz = np.empty((p + 1) * self.w)
         r = ctypes.c_int32()
         self._check(self.lib.arr_project_p(self.h, p, px, ldx, py, ldy,
                                            ritz.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(r)),
@@ -210,15 +212,18 @@ class EigContext:
         return ev, res, info
 
 
-def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None) -> EigContext:
-    return EigContext(A, k, p, d, stream)
+def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None) -> EigContext:
+    """eig_init (w = k) / eig_init_w (w >= k guard columns)."""
+    return EigContext(A, k, p, d, stream, w)
 
 
 def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, s_max=5, evec=None,
                    stream=None):
     """Public host-buffer entry (eig_solve_host): host arrays in, host results out.
-    Arguments may be numpy arrays or (pinned) CPU torch tensors."""
+    X0 is n x w (w >= k; w - k guard columns).  Arguments may be numpy arrays or
+    (pinned) CPU torch tensors."""
     lib = _lib.load()
+    w = int(X0.shape[1])
 
     def ptr(a):
         if isinstance(a, torch.Tensor):
@@ -233,7 +238,7 @@ def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, 
     info = arr_solve_info()
     opts = arr_solve_opts(tol, maxit, s_max)
     hs, _ = _stream_handle(stream)
-    st = lib.eig_solve_host(int(n), nnz, ptr(row_ptr), ptr(col_idx), ptr(val), k, p, d, ptr(X0),
+    st = lib.eig_solve_host(int(n), nnz, ptr(row_ptr), ptr(col_idx), ptr(val), k, w, p, d, ptr(X0),
                             ctypes.byref(opts), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                             res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                             ptr(evec) if evec is not None else None, ctypes.byref(info), hs)

@@ -5,6 +5,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -17,7 +18,8 @@
 namespace {
 
 constexpr double kSvqbTau = 1e-14;  // eigenvalue floor of the SVQB Gram (relative)
-enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2 };  // dinfo slots (INFO_RANK0.. per block)
+enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2, INFO_CHOL = 40 };  // dinfo slots (INFO_RANK0.. per block;
+                                                                        // INFO_CHOL..+5: potrf/trtri of 3 passes)
 
 arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
     if (c) {
@@ -159,6 +161,63 @@ arr_status svqb_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, in
     return ARR_OK;
 }
 
+// One CholeskyQR pass (optionally shifted, Fukaya et al. 2020): G = In^T In,
+// D = diag(G)^{-1/2}, R^T R = D G D + s I (potrf), Out = In D R^{-1} (trtri +
+// DMMA GEMM).  s = 11 (n c + c(c+1)) u c bounds the rounding of the Gram so the
+// shifted factorisation exists for any input; two unshifted passes follow.
+arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
+                       bool shifted, int *info2, int *rank_slot) {
+    double *G = G_buf(c), *Gs = V_buf(c), *B = B_buf(c), *D = D_buf(c);
+    const double u = 1.1102230246251565e-16;
+    const double shift = shifted ? 11.0 * ((double)c->A.n * ncols + (double)ncols * (ncols + 1)) * u * ncols : 0.0;
+    launch_gram(c, In, ldin, ncols, In, ldin, ncols, c->A.n, G, ncols, c->part);
+    launch_chol_prep(c, G, ncols, shift, D, Gs);
+    CHECK_LAUNCH();
+    SOLVER_TRY(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_UPPER, ncols, Gs, ncols, c->solver_work, c->solver_lwork,
+                                info2));
+    if (rank_slot) launch_diag_copy(c, Gs, ncols, c->evals);
+    SOLVER_TRY(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, ncols, CUDA_R_64F, Gs, ncols,
+                                c->trtri_dwork, c->trtri_dbytes, c->trtri_hwork.data(), c->trtri_hwork.size(),
+                                info2 + 1));
+    launch_chol_build(c, D, Gs, ncols, B, c->evals, 100.0 * shift, rank_slot);
+    launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n);
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
+// Shifted CholeskyQR3 In -> Out (In != Out) through the scratch T; *ok = 0 if
+// a factorisation failed (numerically rank-deficient input after the shift):
+// the caller then falls back to SVQB.  Synchronises the stream.
+arr_status cholqr3(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols, int *rank_slot,
+                   bool *ok) {
+    arr_status st;
+    int *inf = c->dinfo + INFO_CHOL;
+    CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(int) * 6, c->stream));
+    if ((st = cholqr_pass(c, In, ldin, Out, ldout, ncols, true, inf, rank_slot)) != ARR_OK) return st;
+    if ((st = cholqr_pass(c, Out, ldout, c->T, ldT(c), ncols, false, inf + 2, nullptr)) != ARR_OK) return st;
+    // The second pass's factor R2 measures how far pass 1 was from orthonormal:
+    // pass 2's output is orthonormal to O(u cond(R2)^2).  If R2^{-1} (left in V
+    // by trtri) is within 1e-6 of I entrywise, the third pass is skipped.
+    launch_dev_from_identity(c, V_buf(c), ncols, c->evals);
+    CUDA_TRY(cudaMemcpyAsync(c->h_istage + 40, inf, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage, c->evals, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *ok = true;
+    for (int q = 0; q < 4; ++q) *ok = *ok && c->h_istage[40 + q] == 0;
+    const double dev = c->h_stage[0];
+    if (!*ok) return ARR_OK;
+    if (!(dev <= 1e-6)) {
+        if ((st = cholqr_pass(c, c->T, ldT(c), Out, ldout, ncols, false, inf + 4, nullptr)) != ARR_OK) return st;
+        CUDA_TRY(cudaMemcpyAsync(c->h_istage + 44, inf + 4, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        *ok = c->h_istage[44] == 0 && c->h_istage[45] == 0;
+    } else {
+        launch_copy_rows(c, c->T, ldT(c), Out, ldout, c->A.n, ncols);
+        CHECK_LAUNCH();
+    }
+    return ARR_OK;
+}
+
 // Two SVQB passes In -> Out through the scratch T (In may equal Out).
 arr_status svqb2(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
                  int *rank_slot) {
@@ -176,28 +235,42 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
     double *Q = c->Q, *T = c->T;
     arr_status st;
     const int ev0 = t_mark(c);
+    int evs = ev0;
     // U_0 = orth(X): Alg. RR step 1 on the first block
-    if ((st = svqb2(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
+    bool ok = false;
+    if (c->orth_mode == 0 && (st = cholqr3(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0, &ok)) != ARR_OK) return st;
+    if (!ok && (st = svqb2(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
     // U_j = orth((I - Q Q^T) A U_{j-1}): the block-Krylov augmentation of Eq. S:ARR
     for (int j = 1; j <= p_use; ++j) {
-        SpmmArgs s{};
-        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
-        s.n = c->A.n; s.w = w;
-        s.Yin = Q + (int64_t)(j - 1) * w; s.ld_in = lq;
-        s.alpha = 1.0; s.shift = 0.0;
-        s.Yout = T; s.ld_out = lt;
-        if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
         const int jw = j * w;
-        for (int pass = 0; pass < 2; ++pass) {  // block classical Gram-Schmidt, twice
-            launch_gram(c, Q, lq, jw, T, lt, w, c->A.n, G_buf(c), w, c->part);
-            launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
-        }
-        CHECK_LAUNCH();
         double *Qj = Q + (int64_t)jw;
-        if ((st = svqb_pass(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j)) != ARR_OK) return st;
-        if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
-        launch_copy_rows(c, T, lt, Qj, lq, c->A.n, w);
+        auto make_W = [&]() -> arr_status {  // T = (I - Q Q^T) A U_{j-1}, block CGS twice
+            SpmmArgs s{};
+            s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+            s.n = c->A.n; s.w = w;
+            s.Yin = Q + (int64_t)(j - 1) * w; s.ld_in = lq;
+            s.alpha = 1.0; s.shift = 0.0;
+            s.Yout = T; s.ld_out = lt;
+            if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+            for (int pass = 0; pass < 2; ++pass) {
+                launch_gram(c, Q, lq, jw, T, lt, w, c->A.n, G_buf(c), w, c->part);
+                launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
+            }
+            CHECK_LAUNCH();
+            return ARR_OK;
+        };
+        if ((st = make_W()) != ARR_OK) return st;
+        ok = false;
+        if (c->orth_mode == 0 && (st = cholqr3(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j, &ok)) != ARR_OK)
+            return st;
+        if (!ok) {
+            if (c->orth_mode == 0 && (st = make_W()) != ARR_OK) return st;  // T was reused by CholeskyQR3
+            if ((st = svqb_pass(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j)) != ARR_OK) return st;
+            if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
+            launch_copy_rows(c, T, lt, Qj, lq, c->A.n, w);
+        }
     }
+    { const int e = t_mark(c); t_add(c, 3, evs, e, 1); evs = e; }
     // H = Q^T (A Q), one w-column block of AQ at a time (AQ never stored whole)
     double *H = H_buf(c);
     for (int j = 0; j <= p_use; ++j) {
@@ -208,13 +281,16 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         s.alpha = 1.0; s.shift = 0.0;
         s.Yout = T; s.ld_out = lt;
         if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
-        launch_gram(c, Q, lq, m, T, lt, w, c->A.n, H + (int64_t)j * w, m, c->part);
+        // upper block triangle only: rows [0, (j+1)w) of column block j (H is symmetric)
+        launch_gram(c, Q, lq, (j + 1) * w, T, lt, w, c->A.n, H + (int64_t)j * w, m, c->part);
     }
-    launch_symmetrize(c, H, m);
+    launch_symmetrize(c, H, m, w);
     CHECK_LAUNCH();
+    { const int e = t_mark(c); t_add(c, 4, evs, e, 1); evs = e; }
     // H = V Theta V^T (Alg. RR step 3): small dense eig on device (not graded)
     SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, H, m, c->evals,
                                 c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
+    { const int e = t_mark(c); t_add(c, 5, evs, e, 1); evs = e; }
     // Y = Q V[:, leading w] (Alg. RR step 4; Alg. ARR step 4)
     if (Y) {
         launch_ritz_select(c, H, m, w, B_buf(c));
@@ -271,22 +347,26 @@ bool block_ok(const double *p, int64_t ld, int ncols) { return p != nullptr && l
 extern "C" {
 
 arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream) {
+    return eig_init_w(out, A, k, k, p, d, stream);
+}
+
+arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, int32_t p, int32_t d, void *stream) {
     if (!out || !A) return ARR_EINVAL;
     *out = nullptr;
     if (A->n < 1 || A->n >= (int64_t(1) << 31) || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->val)))
         return ARR_EINVAL;
-    if (k < 1 || p < 0 || d < 1 || (int64_t)(p + 1) * k >= A->n || k > ARR_MAX_W) return ARR_EINVAL;
+    if (k < 1 || w_in < k || p < 0 || d < 1 || (int64_t)(p + 1) * w_in >= A->n || w_in > ARR_MAX_W) return ARR_EINVAL;
     arr_ctx *c = new (std::nothrow) arr_ctx();
     if (!c) return ARR_ENOMEM;
     c->A = *A;
-    c->k = k; c->w = k; c->p = p; c->d = d;
+    c->k = k; c->w = w_in; c->p = p; c->d = d;
     c->stream = (cudaStream_t)stream;
     c->poisoned = ARR_OK;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (c->num_sms <= 0) c->num_sms = 148;
-    const int64_t n = A->n, w = k, m = (int64_t)(p + 1) * k;
+    const int64_t n = A->n, w = w_in, m = (int64_t)(p + 1) * w_in;
     const int64_t lq = even_up(m), lt = even_up(w);
     const int64_t mm = std::max<int64_t>(m, ARR_MAX_W);
     c->part_elems = (size_t)std::max<int64_t>(16 * m * w, 4096 * mm);
@@ -323,7 +403,23 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
     int lwork_w = 0;
     cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)w, c->small, (int)w,
                                 c->evals, &lwork_w);
-    c->solver_lwork = std::max(lwork, lwork_w);
+    int lwork_p = 0;
+    cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_UPPER, (int)w, c->small, (int)w, &lwork_p);
+    c->solver_lwork = std::max(std::max(lwork, lwork_w), lwork_p);
+    size_t tdb = 0, thb = 0;
+    if (cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, w, CUDA_R_64F, c->small, w,
+                                    &tdb, &thb) != CUSOLVER_STATUS_SUCCESS) {
+        eig_destroy(c);
+        return ARR_ECUSOLVER;
+    }
+    c->trtri_dbytes = std::max<size_t>(tdb, 16);
+    c->trtri_hwork.resize(std::max<size_t>(thb, 16));
+    if (cudaMalloc(&c->trtri_dwork, c->trtri_dbytes) != cudaSuccess) {
+        cudaGetLastError();
+        eig_destroy(c);
+        return ARR_ENOMEM;
+    }
+    c->orth_mode = getenv("ARRABIT_ORTH_SVQB") ? 1 : 0;
     if (cudaMalloc(&c->solver_work, sizeof(double) * (size_t)c->solver_lwork) != cudaSuccess) {
         cudaGetLastError();
         eig_destroy(c);
@@ -353,7 +449,8 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work};
+    void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
+                    c->trtri_dwork};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -433,7 +530,7 @@ arr_status eig_set_timing(arr_ctx *c, int32_t on) {
     c->pending.clear();
     c->ev_next = 0;
     c->timing = on != 0;
-    for (int i = 0; i < 3; ++i) { c->phase_ms[i] = 0.0; c->phase_cnt[i] = 0; }
+    for (int i = 0; i < kPhases; ++i) { c->phase_ms[i] = 0.0; c->phase_cnt[i] = 0; }
     return ARR_OK;
 }
 
@@ -442,7 +539,7 @@ arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts) {
     if (!ms || !counts) return fail(c, ARR_EINVAL, "null output");
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     t_resolve(c);
-    for (int i = 0; i < 3; ++i) { ms[i] = c->phase_ms[i]; counts[i] = c->phase_cnt[i]; }
+    for (int i = 0; i < kPhases; ++i) { ms[i] = c->phase_ms[i]; counts[i] = c->phase_cnt[i]; }
     return ARR_OK;
 }
 
@@ -485,9 +582,13 @@ arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t 
 arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank) {
     GUARD(c);
     if (!block_ok(X, ldx, ncols) || ncols > c->w) return fail(c, ARR_EINVAL, "bad block / ncols > w");
-    arr_status st = svqb_pass(c, X, ldx, c->T, ldT(c), ncols, c->dinfo + INFO_RANK0);
-    if (st != ARR_OK) return st;
-    if ((st = svqb_pass(c, c->T, ldT(c), X, ldx, ncols, nullptr)) != ARR_OK) return st;
+    // keep the input in the basis buffer: CholeskyQR3 X_copy -> X, SVQB fallback from the copy
+    launch_copy_rows(c, X, ldx, c->Q, ldQ(c), c->A.n, ncols);
+    bool ok = false;
+    arr_status st;
+    if (c->orth_mode == 0 && (st = cholqr3(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0, &ok)) != ARR_OK)
+        return st;
+    if (!ok && (st = svqb2(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo, sizeof(int) * (INFO_RANK0 + 1), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->h_istage[INFO_SYEVD] != 0) return fail(c, ARR_ECUSOLVER, "syevd failed");
@@ -574,21 +675,22 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
 }
 
 arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
-                          int32_t k, int32_t p, int32_t d, const double *X0, const arr_solve_opts *opts,
+                          int32_t k, int32_t w, int32_t p, int32_t d, const double *X0, const arr_solve_opts *opts,
                           double *eigval, double *res, double *evec, arr_solve_info *info, void *stream) {
-    if (!row_ptr || !col_idx || !val || !X0 || !opts || !eigval || !res || n < 1 || k < 1) return ARR_EINVAL;
+    if (!row_ptr || !col_idx || !val || !X0 || !opts || !eigval || !res || n < 1 || k < 1 || w < k) return ARR_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     int64_t *d_rp = nullptr;
     int32_t *d_ci = nullptr;
     double *d_val = nullptr, *d_X = nullptr;
     arr_ctx *c = nullptr;
     arr_status st = ARR_OK;
-    const int64_t ldx = even_up(k);
+    const int64_t ldx = even_up(w);
     auto cleanup = [&]() {
         if (c) eig_destroy(c);
         cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_val); cudaFree(d_X);
     };
-    if (cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)) != cudaSuccess || cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+    if (cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
+        cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
         cudaMalloc(&d_val, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
         cudaMalloc(&d_X, sizeof(double) * n * ldx) != cudaSuccess) {
         cudaGetLastError();
@@ -598,13 +700,13 @@ arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const 
     if (cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(d_ci, col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(d_val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpy2DAsync(d_X, sizeof(double) * ldx, X0, sizeof(double) * k, sizeof(double) * k, n,
+        cudaMemcpy2DAsync(d_X, sizeof(double) * ldx, X0, sizeof(double) * w, sizeof(double) * w, n,
                           cudaMemcpyHostToDevice, s) != cudaSuccess) {
         cleanup();
         return ARR_ECUDA;
     }
     arr_csr A{n, nnz, d_rp, d_ci, d_val};
-    st = eig_init(&c, &A, k, p, d, stream);
+    st = eig_init_w(&c, &A, k, w, p, d, stream);
     if (st == ARR_OK) st = eig_solve(c, d_X, ldx, opts, eigval, res, info);
     if (st == ARR_OK && evec) {
         if (cudaMemcpy2DAsync(evec, sizeof(double) * k, d_X, sizeof(double) * ldx, sizeof(double) * k, n,

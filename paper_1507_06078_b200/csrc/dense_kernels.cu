@@ -227,12 +227,17 @@ __global__ void svqb_build_kernel(const double *__restrict__ D, const double *__
     B[t] = (lmax > 0.0) ? D[i] * Vcm[(int64_t)j * w + i] / sqrt(l) : 0.0;
 }
 
-__global__ void symmetrize_kernel(double *H, int m) {
+// H (m x m) was computed by column blocks of width bw, column block J only for
+// rows < (J+1)*bw (the upper block triangle).  For i < j: if (j, i) was also
+// computed (same diagonal block) average the pair, else mirror (i, j) into (j, i).
+__global__ void symmetrize_kernel(double *H, int m, int bw) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= (int64_t)m * m) return;
     const int i = (int)(t / m), j = (int)(t % m);
     if (j <= i) return;
-    const double v = 0.5 * (H[(int64_t)i * m + j] + H[(int64_t)j * m + i]);
+    const bool both = j < (i / bw + 1) * bw;
+    const double up = H[(int64_t)i * m + j];
+    const double v = both ? 0.5 * (up + H[(int64_t)j * m + i]) : up;
     H[(int64_t)i * m + j] = v;
     H[(int64_t)j * m + i] = v;
 }
@@ -291,12 +296,92 @@ void launch_svqb_build(arr_ctx *c, const double *D, const double *Vcm, const dou
     c->launches++;
 }
 
-void launch_symmetrize(arr_ctx *c, double *H, int32_t m) {
-    symmetrize_kernel<<<nblk((int64_t)m * m, 256), 256, 0, c->stream>>>(H, m);
+void launch_symmetrize(arr_ctx *c, double *H, int32_t m, int32_t bw) {
+    symmetrize_kernel<<<nblk((int64_t)m * m, 256), 256, 0, c->stream>>>(H, m, bw);
     c->launches++;
 }
 
 void launch_ritz_select(arr_ctx *c, const double *Vcm, int32_t m, int32_t wsel, double *Vsel) {
     ritz_select_kernel<<<nblk((int64_t)m * wsel, 256), 256, 0, c->stream>>>(Vcm, m, wsel, Vsel);
+    c->launches++;
+}
+
+// ---------------------------------------------------------------- CholeskyQR helpers
+namespace {
+// Gs = D G D + shift*I with D = diag(G)^{-1/2} (column equilibration; 0 for zero columns)
+__global__ void chol_prep_kernel(const double *__restrict__ G, int w, double shift, double *__restrict__ D,
+                                 double *__restrict__ Gs) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    const double gi = G[(int64_t)i * w + i], gj = G[(int64_t)j * w + j];
+    const double di = gi > 0.0 ? 1.0 / sqrt(gi) : 0.0;
+    const double dj = gj > 0.0 ? 1.0 / sqrt(gj) : 0.0;
+    double v = di * (0.5 * (G[t] + G[(int64_t)j * w + i])) * dj;
+    if (i == j) v += shift;
+    Gs[t] = v;
+    if (j == 0) D[i] = di;
+}
+// B = D * Rinv (row-major), Rinv upper triangular stored column-major (cuSOLVER);
+// rank_out (optional) = #{i : R_ii^2 > rank_thr}, read from the factor R kept in Rdiag.
+__global__ void chol_build_kernel(const double *__restrict__ D, const double *__restrict__ Rinv_cm, int w,
+                                  double *__restrict__ B, const double *__restrict__ Rdiag, double rank_thr,
+                                  int *rank_out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t == 0 && rank_out) {
+        int r = 0;
+        for (int q = 0; q < w; ++q) r += (Rdiag[q] * Rdiag[q] > rank_thr);
+        *rank_out = r;
+    }
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    B[t] = (i <= j) ? D[i] * Rinv_cm[(int64_t)j * w + i] : 0.0;
+}
+__global__ void diag_copy_kernel(const double *__restrict__ A_cm, int w, double *__restrict__ d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < w) d[i] = A_cm[(int64_t)i * w + i];
+}
+}  // namespace
+
+namespace {
+// out = max over the upper triangle of |M_ij - delta_ij| (M column-major w x w), one CTA
+__global__ void dev_from_identity_kernel(const double *__restrict__ M_cm, int w, double *out) {
+    double m = 0.0;
+    for (int64_t t = threadIdx.x; t < (int64_t)w * w; t += blockDim.x) {
+        const int j = (int)(t / w), i = (int)(t % w);  // column-major: t = j*w + i
+        if (i > j) continue;
+        const double v = fabs(M_cm[t] - (i == j ? 1.0 : 0.0));
+        m = (v > m || v != v) ? v : m;  // NaN propagates
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            const double o = red[threadIdx.x + s];
+            if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+}  // namespace
+
+void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out) {
+    dev_from_identity_kernel<<<1, 256, 0, c->stream>>>(M_cm, w, out);
+    c->launches++;
+}
+
+void launch_chol_prep(arr_ctx *c, const double *G, int32_t w, double shift, double *D, double *Gs) {
+    chol_prep_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(G, w, shift, D, Gs);
+    c->launches++;
+}
+void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32_t w, double *B, const double *Rdiag,
+                       double rank_thr, int *rank_out) {
+    chol_build_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(D, Rinv_cm, w, B, Rdiag, rank_thr, rank_out);
+    c->launches++;
+}
+void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d) {
+    diag_copy_kernel<<<nblk(w, 256), 256, 0, c->stream>>>(A_cm, w, d);
     c->launches++;
 }

@@ -10,6 +10,7 @@
 #include "../../include/arrabit.h"
 
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
+constexpr int kPhases = 6;  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
 
 struct arr_ctx {
     // problem
@@ -36,6 +37,10 @@ struct arr_ctx {
     int64_t ntiles;
     double *solver_work;
     int solver_lwork;
+    void *trtri_dwork;      // cusolverDnXtrtri device workspace
+    size_t trtri_dbytes;
+    std::vector<char> trtri_hwork;
+    int orth_mode;          // 0 = shifted CholeskyQR3 (fallback SVQB), 1 = SVQB only
     cusolverDnHandle_t solver;
     size_t ws_bytes;
     // bookkeeping
@@ -49,8 +54,8 @@ struct arr_ctx {
     int ev_next;
     struct Pending { int phase, e0, e1; int64_t count; };
     std::vector<Pending> pending;
-    double phase_ms[3];
-    int64_t phase_cnt[3];
+    double phase_ms[6];
+    int64_t phase_cnt[6];
     // pinned host staging
     double *h_stage;   // [m + 2*ARR_MAX_W + 16]
     int *h_istage;     // [16]
@@ -105,8 +110,13 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
 void launch_svqb_prep(arr_ctx *c, const double *G, int32_t w, double *D, double *Gs);
 void launch_svqb_build(arr_ctx *c, const double *D, const double *Vcm, const double *lam, int32_t w,
                        double tau, double *B, int *rank_out);
-void launch_symmetrize(arr_ctx *c, double *H, int32_t m);
+void launch_symmetrize(arr_ctx *c, double *H, int32_t m, int32_t bw);
 void launch_ritz_select(arr_ctx *c, const double *Vcm, int32_t m, int32_t wsel, double *Vsel);
 void launch_copy_rows(arr_ctx *c, const double *src, int64_t lds, double *dst, int64_t ldd, int64_t n,
                       int32_t w);
 void launch_check_norms(arr_ctx *c, const double *norms, int32_t w, int *bad);
+void launch_chol_prep(arr_ctx *c, const double *G, int32_t w, double shift, double *D, double *Gs);
+void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32_t w, double *B, const double *Rdiag,
+                       double rank_thr, int *rank_out);
+void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d);
+void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out);

@@ -21,7 +21,7 @@ from synth import configs  # noqa: E402
 
 def main(cid: int):
     A, spec = configs.build_config(cid)
-    X0 = synth.gaussian_block(A.n, spec.w, spec.seed)
+    X0 = synth.starting_block(spec)
     t = time.time()
     r = oracle.solve(A, spec.k, spec.d, spec.p, X0, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max)
     out = dict(config=spec.name, converged=bool(r.converged), outer=r.outer, sweeps=r.sweeps,

@@ -63,7 +63,8 @@ def main():
     wall = time.perf_counter() - t
     ms, cnt = ctx.eig_phase_times()
     print(f"config {spec.name} k={k}: wall {wall*1e3:.2f} ms; filter {ms[0]:.3f} ms / {cnt[0]} degree launches "
-          f"({ms[0]/max(cnt[0],1)*1e3:.1f} us each); arr {ms[1]:.3f} ms / {cnt[1]}; residuals {ms[2]:.3f} ms / {cnt[2]}")
+          f"({ms[0]/max(cnt[0],1)*1e3:.1f} us each); arr {ms[1]:.3f} ms / {cnt[1]} [basis {ms[3]:.3f} H {ms[4]:.3f} "
+          f"eig {ms[5]:.3f}]; residuals {ms[2]:.3f} ms / {cnt[2]}")
 
 
 if __name__ == "__main__":

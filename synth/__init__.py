@@ -18,4 +18,4 @@ from .generators import (  # noqa: F401
     gaussian_block,
     gaussian_block_rows,
 )
-from .configs import CONFIGS, SMALL_ANALOGS, build_config, ConfigSpec  # noqa: F401
+from .configs import CONFIGS, SMALL_ANALOGS, build_config, starting_block, ConfigSpec  # noqa: F401

@@ -35,9 +35,14 @@ class ConfigSpec:
         return self.size ** 3
 
     @property
+    def q(self) -> int:
+        """Guard vectors: the paper's default q = round(0.1 k)."""
+        return int(round(0.1 * self.k))
+
+    @property
     def w(self) -> int:
-        # block width w = k (guard vectors are NEXT)
-        return self.k
+        """Block width w = k + q (reading R4)."""
+        return self.k + self.q
 
 
 CONFIGS = {
@@ -70,6 +75,18 @@ def build_matrix(kind: str, size: int, seed: int) -> g.CSR:
     if kind == "st27":
         return g.stencil27_3d(size)
     raise ValueError(kind)
+
+
+def starting_block(spec: ConfigSpec, n: int | None = None):
+    """X0 (n x w): the config's seeded n x k Gaussian block (stream 0) followed by
+    q guard columns from stream 2 (R4, R11)."""
+    import numpy as np
+    n = spec.n if n is None else n
+    X0 = g.gaussian_block(n, spec.k, spec.seed)
+    if spec.q == 0:
+        return X0
+    G = g.gaussian_block(n, spec.q, spec.seed, stream=2)
+    return np.ascontiguousarray(np.hstack([X0, G]))
 
 
 def build_config(spec_or_id) -> tuple[g.CSR, ConfigSpec]:

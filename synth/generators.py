@@ -230,8 +230,9 @@ def zipf_random(n: int, seed: int, dmin: int = 2, dmax: int = 256, expo: float =
     return CSR(n, row_ptr, col, val, name=f"zipf_{n}_s{seed}")
 
 
-def gaussian_block_rows(n: int, w: int, seed: int, r0: int, r1: int) -> np.ndarray:
-    """Rows [r0, r1) of the n x w iid N(0,1) block of ``seed`` (stream 0).
+def gaussian_block_rows(n: int, w: int, seed: int, r0: int, r1: int, stream: int = 0) -> np.ndarray:
+    """Rows [r0, r1) of the n x w iid N(0,1) block of ``seed`` (stream 0; guard
+    columns use stream 2).
     Chunk c covers rows [c*ROW_CHUNK, (c+1)*ROW_CHUNK) and is drawn from
     default_rng([seed, 0, c]).standard_normal((rows, w))."""
     out = np.empty((r1 - r0, w), dtype=np.float64)
@@ -240,12 +241,12 @@ def gaussian_block_rows(n: int, w: int, seed: int, r0: int, r1: int) -> np.ndarr
     for c in range(c0, c1 + 1):
         a = c * ROW_CHUNK
         b = min(n, a + ROW_CHUNK)
-        blk = np.random.default_rng([seed, 0, c]).standard_normal((b - a, w))
+        blk = np.random.default_rng([seed, stream, c]).standard_normal((b - a, w))
         lo, hi = max(a, r0), min(b, r1)
         out[lo - r0:hi - r0] = blk[lo - a:hi - a]
     return out
 
 
-def gaussian_block(n: int, w: int, seed: int) -> np.ndarray:
-    """The full n x w starting block X0 (row-major, C-contiguous)."""
-    return gaussian_block_rows(n, w, seed, 0, n)
+def gaussian_block(n: int, w: int, seed: int, stream: int = 0) -> np.ndarray:
+    """The full n x w Gaussian block (row-major, C-contiguous)."""
+    return gaussian_block_rows(n, w, seed, 0, n, stream)

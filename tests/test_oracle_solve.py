@@ -20,7 +20,7 @@ def _check(res, ref, k, tol=1e-10):
 
 def test_solve_cfg1_closed_form():
     A, spec = configs.build_config(1)
-    X0 = synth.gaussian_block(A.n, spec.w, spec.seed)
+    X0 = synth.starting_block(spec)
     r = oracle.solve(A, spec.k, spec.d, spec.p, X0, tol=spec.tol)
     n = A.n
     lam = np.sort(2 - 2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1)))[::-1]
@@ -35,7 +35,7 @@ def test_solve_small_lap2d_closed_form():
     N = spec.size
     c = 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
     lam = np.sort((4 - c[:, None] - c[None, :]).ravel())[::-1]
-    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.starting_block(spec))
     _check(r, lam, spec.k)
 
 
@@ -45,7 +45,7 @@ def test_solve_small_st27_closed_form():
     N = spec.size
     t = 1 + 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
     lam = np.sort((27 - t[:, None, None] * t[None, :, None] * t[None, None, :]).ravel())[::-1]
-    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.starting_block(spec))
     _check(r, lam, spec.k)
 
 
@@ -55,7 +55,7 @@ def test_solve_small_lap3d_potential_weyl_and_dense():
     N = spec.size
     c = 2 * np.cos(np.arange(1, N + 1) * np.pi / (N + 1))
     L = np.sort((6 - c[:, None, None] - c[None, :, None] - c[None, None, :]).ravel())[::-1]
-    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.starting_block(spec))
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1]
     _check(r, lam, spec.k)
     # Weyl: lambda_i(L) <= lambda_i(L+V) <= lambda_i(L) + max V
@@ -65,6 +65,6 @@ def test_solve_small_lap3d_potential_weyl_and_dense():
 def test_solve_small_zipf_dense():
     spec = configs.SMALL_ANALOGS["zipf"]
     A, _ = configs.build_config(spec)
-    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.gaussian_block(A.n, spec.w, spec.seed))
+    r = oracle.solve(A, spec.k, spec.d, spec.p, synth.starting_block(spec))
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1]
     _check(r, lam, spec.k)
