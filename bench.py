@@ -11,7 +11,10 @@ value = eigenpairs/s = k * steps * N / (max-over-ranks device time).
 The filter's HBM GB/s (the metric's first half) is the `roofline` object.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N>1 (torchrun): each rank solves its own replica (no data-path collective).
+N>1 (torchrun): configs 1-2 (single-GPU problems in BASELINE.json) run one replica
+per rank (weak scaling, no data-path collective); configs 3-5 (or --partition) are
+row-partitioned over the ranks: halo / all-gather exchange before every SpMM and
+Gram allreduce over NCCL inside libarrabit (strong scaling).
 """
 from __future__ import annotations
 
@@ -45,6 +48,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="N>1: row-partition the config over the ranks even for configs 1-2")
     return ap.parse_args()
 
 
@@ -146,15 +151,20 @@ def run_reference(args):
     if rank != 0:
         return 0
     A, spec = configs.build_config(args.config)
-    X0 = synth.starting_block(spec)
+    X0 = synth.starting_block(spec) if args.config <= 2 else None
     cnt = oracle_counts(args.config)
     S, O = (cnt["sweeps"], cnt["outer"]) if cnt else (38, 10)
+    def sample():
+        if args.config <= 2:
+            return oracle_sample(A, spec, X0)
+        return oracle_filter_sample(A, spec) * spec.w / 16, 0.0
+
     for _ in range(args.warmup):
-        oracle_sample(A, spec, X0)
+        sample()
     sw, ar, wall = [], [], []
     for _ in range(args.steps):
         t = time.perf_counter()
-        s, r = oracle_sample(A, spec, X0)
+        s, r = sample()
         wall.append(time.perf_counter() - t)
         sw.append(s)
         ar.append(r)
@@ -163,7 +173,9 @@ def run_reference(args):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     sample = (f"{spec.name}: per step one MPM sweep (d={spec.d}) + one ARR(p={spec.p}) + residuals on the full "
               f"block; extrapolated to the oracle's own full solve ({S} sweeps, {O} ARR steps, "
-              f"tests/golden/oracle_cfg{args.config}_counts.json)")
+              f"tests/golden/oracle_cfg{args.config}_counts.json)") if args.config <= 2 else (
+              f"{spec.name}: per step one MPM sweep of 16 of the {spec.w} columns, x w/16, extrapolated to "
+              f"{S} sweeps (ARR not sampled: the oracle's QR at this size takes hours)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(wall), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -177,6 +189,16 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def _partition_spec(spec):
+    """How a config is row-partitioned over ranks: z-slabs of
+    whole grid planes for the stencils, nnz-balanced row blocks otherwise."""
+    if spec.kind in ("lap3dV", "st27"):
+        return ("planes", spec.size, spec.size ** 2)
+    if spec.kind == "lap2d":
+        return ("planes", spec.size, spec.size)
+    return ("balanced",)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -189,17 +211,43 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_1507_06078_b200 as arr
+    from paper_1507_06078_b200 import partition as pt
 
     A, spec = configs.build_config(args.config)
-    X0h = synth.starting_block(spec)
+    # N > 1: configs 3-5 are row-partitioned over the ranks (halo / all-gather exchange,
+    # Gram allreduce over NCCL: strong scaling); configs 1-2 are single-GPU problems
+    # (BASELINE.json) and run as independent replicas (weak scaling).
+    partitioned = world > 1 and (args.partition or args.config >= 3)
+    plan = comm = None
+    if partitioned:
+        ps = _partition_spec(spec)
+        bounds = pt.bounds_planes(ps[1], ps[2], world) if ps[0] == "planes" else pt.bounds_balanced(A.row_ptr, world)
+        plan = pt.local_plan(A, bounds, rank)
+        Aloc = plan
+        r0, r1 = plan.row_begin, plan.row_begin + plan.n_own
+        nrows = plan.n_rows_block
+    else:
+        Aloc = A
+        r0, r1, nrows = 0, A.n, A.n
+
+    def host_X0():
+        X = np.zeros((nrows, spec.w))
+        X[:r1 - r0, :spec.k] = synth.gaussian_block_rows(A.n, spec.k, spec.seed, r0, r1)
+        if spec.q:
+            X[:r1 - r0, spec.k:] = synth.gaussian_block_rows(A.n, spec.q, spec.seed, r0, r1, stream=2)
+        return X
+
+    X0h = host_X0()
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
-        Ad = arr.to_device_csr(A, device=dev)
+        Ad = arr.to_device_csr(Aloc, device=dev)
         X0 = torch.from_numpy(X0h).to(dev)
         X = torch.empty_like(X0)
         flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)  # > 126 MB L2
     stream.synchronize()
-    ctx = arr.eig_init(Ad, spec.k, spec.p, spec.d, stream=stream, w=spec.w)
+    if partitioned:
+        comm = arr.Comm.from_torch_distributed()
+    ctx = arr.eig_init(Ad, spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm, plan=plan)
 
     def one_solve():
         X.copy_(X0)
@@ -239,12 +287,15 @@ def run_ours(args):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = spec.k * args.steps * world / (total_ms / 1000.0)
+    # eigenpairs/s: each replica (or the one partitioned job) finds k pairs per step
+    jobs = 1 if partitioned else world
+    value = spec.k * args.steps * jobs / (total_ms / 1000.0)
 
-    # roofline of the dominant kernel (filter degree)
+    # roofline of the dominant kernel (filter degree), algorithmic bytes of this rank's rows
     peak, peak_src = load_peaks()
     deg_ms = phase_ms[0] / max(1, phase_cnt[0])
-    bpl = filter_bytes_per_degree(A.n, A.nnz, spec.w, spec.d)
+    nnz_loc = int(Aloc.nnz) if not partitioned else plan.nnz
+    bpl = filter_bytes_per_degree(r1 - r0, nnz_loc, spec.w, spec.d)
     achieved = bpl / (deg_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
@@ -255,68 +306,114 @@ def run_ours(args):
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "spmm_fused_kernel (one Chebyshev filter degree)",
+                "traffic": traffic, "kernel": "spmm_tile_kernel (one fused Chebyshev filter degree)",
                 "bytes_per_launch": bpl, "avg_launch_us": deg_ms * 1000.0, "launches": int(phase_cnt[0]),
                 "peak_source": peak_src,
-                "share_of_step": phase_ms[0] / total_ms if world == 1 else None,
+                "share_of_step": phase_ms[0] / sum(step_ms),
                 "phase_ms_per_step": {"filter_degrees": phase_ms[0] / args.steps, "arr_project": phase_ms[1] / args.steps,
                                       "arr_basis": phase_ms[3] / args.steps, "arr_H": phase_ms[4] / args.steps,
                                       "arr_small_eig": phase_ms[5] / args.steps,
                                       "residuals": phase_ms[2] / args.steps}}
+    if spec.kind == "zipf":
+        roofline["gather_model_bytes_per_launch"] = (12 * nnz_loc + 8 * (r1 - r0 + 1) + 8 * nnz_loc * spec.w
+                                                     + 16 * (r1 - r0) * spec.w)
+    ctx.close()
+    del X, X0, flush
+    torch.cuda.empty_cache()
 
-    # e2e through the host-buffer C-ABI entry (H2D inputs + D2H eigenpairs inside the timed region)
+    # e2e through the public API with HOST buffers: H2D of the CSR + X0 and D2H of the
+    # eigenpairs inside the timed region (one GPU: the eig_solve_host C-ABI call;
+    # partitioned: each rank uploads its local CSR + X0 rows, eig_init_dist, eig_solve)
     e2e = None
     if not args.no_e2e:
-        rp = torch.from_numpy(A.row_ptr).pin_memory()
-        ci = torch.from_numpy(A.col_idx).pin_memory()
-        va = torch.from_numpy(A.val).pin_memory()
-        x0p = torch.from_numpy(X0h).pin_memory()
-        evec = torch.empty((A.n, spec.k), dtype=torch.float64).pin_memory()
+        xp = torch.from_numpy(X0h).pin_memory()
+        evec = torch.empty((r1 - r0, spec.k), dtype=torch.float64).pin_memory()
+        rp = torch.from_numpy(np.ascontiguousarray(Aloc.row_ptr)).pin_memory()
+        ci = torch.from_numpy(np.ascontiguousarray(Aloc.col_idx)).pin_memory()
+        va = torch.from_numpy(np.ascontiguousarray(Aloc.val)).pin_memory()
         e2e_s = []
         for _ in range(max(1, args.steps)):
+            if world > 1:
+                dist.barrier()
             torch.cuda.synchronize(dev)
             t = time.perf_counter()
-            arr.eig_solve_host(A.n, rp, ci, va, spec.k, spec.p, spec.d, x0p, tol=spec.tol, maxit=spec.maxit,
-                               s_max=spec.s_max, evec=evec, stream=stream)
+            if not partitioned:
+                arr.eig_solve_host(A.n, rp, ci, va, spec.k, spec.p, spec.d, xp, tol=spec.tol, maxit=spec.maxit,
+                                   s_max=spec.s_max, evec=evec, stream=stream)
+            else:
+                with torch.cuda.stream(stream):
+                    Ad2 = arr.DeviceCSR(plan.n_own, rp.to(dev, non_blocking=True), ci.to(dev, non_blocking=True),
+                                        va.to(dev, non_blocking=True))
+                    Xd = xp.to(dev, non_blocking=True)
+                    c2 = arr.eig_init(Ad2, spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm, plan=plan)
+                    c2.eig_solve(Xd, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max)
+                    evec.copy_(Xd[:r1 - r0, :spec.k], non_blocking=True)
+                    stream.synchronize()
+                    c2.close()
+                    del Ad2, Xd
             e2e_s.append(time.perf_counter() - t)
         tot = float(sum(e2e_s))
         if world > 1:
             t = torch.tensor([tot], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot = float(t.item())
-        e2e = {"value": spec.k * len(e2e_s) * world / tot, "unit": UNIT,
-               "h2d_bytes_per_step": int(8 * (A.n + 1) + 12 * A.nnz + 8 * A.n * spec.w),
-               "d2h_bytes_per_step": int(16 * spec.k + 8 * A.n * spec.k),
-               "api": "eig_solve_host (C-ABI, pinned host buffers, device alloc + copies inside)"}
+        e2e = {"value": spec.k * len(e2e_s) * jobs / tot, "unit": UNIT,
+               "h2d_bytes_per_step": int(8 * (r1 - r0 + 1) + 12 * nnz_loc + 8 * nrows * spec.w),
+               "d2h_bytes_per_step": int(16 * spec.k + 8 * (r1 - r0) * spec.k),
+               "api": ("eig_solve_host (C-ABI, pinned host buffers, device alloc + copies inside)" if not partitioned
+                       else "per rank: H2D of local CSR + X0 rows, eig_init_dist + eig_solve, D2H of the local "
+                            "eigenvector rows (bytes of rank 0)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cnt = oracle_counts(args.config)
         S, O = (cnt["sweeps"], cnt["outer"]) if cnt else (infos[-1][2], infos[-1][1])
-        ts, ta = oracle_sample(A, spec, X0h)
+        if args.config <= 2:
+            ts, ta = oracle_sample(A, spec, synth.starting_block(spec))
+            smp = f"one MPM sweep ({ts:.2f} s) + one ARR+residuals ({ta:.2f} s) of {spec.name}"
+        else:  # bounded: a 16-column filter sweep, scaled to w columns; the ARR is not sampled
+            ts = oracle_filter_sample(A, spec) * spec.w / 16
+            ta = 0.0
+            smp = f"one MPM sweep of 16 of the {spec.w} columns of {spec.name}, x w/16 (ARR not sampled)"
         cpu = {"value": spec.k / (S * ts + O * ta), "unit": UNIT,
                "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "oracle",
-               "sample": f"one MPM sweep ({ts:.2f} s) + one ARR+residuals ({ta:.2f} s) of {spec.name}, "
-                         f"extrapolated to {S} sweeps / {O} ARR steps "
-                         f"({'oracle full-solve counts, tests/golden' if cnt else 'GPU solve counts'})"}
+               "sample": smp + f", extrapolated to {S} sweeps / {O} ARR steps "
+                               f"({'oracle full-solve counts, tests/golden' if cnt else 'GPU solve counts'})"}
 
     if rank == 0:
         conv, outer, sweeps, maxres = infos[-1]
+        par = ("1 GPU" if world == 1 else
+               (f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
+                if partitioned else f"{world} independent replicas (no collective)"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
                 "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "w": spec.w, "d": spec.d,
                            "p": spec.p, "tol": spec.tol, "step": "one full eig_solve from X0",
                            "l2": "flushed between timed steps (256 MiB write), outside the events",
-                           "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas (no collective)",
+                           "parallelism": par,
                            "converged": bool(conv), "outer": outer, "sweeps": sweeps, "maxres": maxres},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
-    ctx.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def oracle_filter_sample(A, spec):
+    """Seconds of one oracle MPM sweep on 16 columns of the workload."""
+    import oracle
+    X = synth.gaussian_block_rows(A.n, 16, spec.seed, 0, A.n)
+    a = oracle.gershgorin_lower(A)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    upper = float(np.bincount(rows, weights=np.abs(A.val), minlength=A.n).max())
+    t0 = time.perf_counter()
+    oracle.mpm_sweep(A, a, a + 0.9 * (upper - a), spec.d, X)
+    return time.perf_counter() - t0
 
 
 def main():

@@ -23,7 +23,7 @@
  *    return host data (ritz_host, rank, res_host, a_out, the solve outputs)
  *    synchronise that stream; all others are asynchronous.
  *  - Errors: bad sizes / pointers / interval -> ARR_EINVAL (context stays usable).
- *    A CUDA or cuSOLVER failure poisons the context: every later call returns
+ *    A CUDA, cuSOLVER or NCCL failure poisons the context: every later call returns
  *    the same code.  A zero or non-finite column norm after filtering ->
  *    ARR_ENUMERIC.  Rank loss is NOT an error; *rank reports it.
  *  - Determinism: fixed reduction trees, no floating-point atomics.  Identical
@@ -47,6 +47,7 @@ typedef enum {
     ARR_ENOMEM = 2,
     ARR_ECUDA = 3,
     ARR_ECUSOLVER = 5,
+    ARR_ENCCL = 6,
     ARR_ENUMERIC = 7
 } arr_status;
 
@@ -58,6 +59,56 @@ typedef struct {
     const int32_t *col_idx;  /* device [nnz], 0 <= col < n                    */
     const double *val;       /* device [nnz]                                  */
 } arr_csr;
+
+/* ---------------------------------------------------------------- multi-GPU (A7)
+ * Row partition (north star "A is row-partitioned with X rows
+ * co-located.  An NCCL halo exchange (or all-gather of X for irregular
+ * sparsity) runs before each SpMM ..., and a k x k NCCL allreduce handles the
+ * Gram blocks").  Rank r owns the contiguous global rows
+ * [row_begin, row_begin + A.n) of A and of every n x w block.  Its local CSR
+ * (arr_csr with n = owned rows) numbers columns locally: 0 .. A.n-1 are the
+ * owned rows, A.n .. A.n + n_ghost - 1 the ghost rows (rows owned elsewhere that
+ * its rows reference), grouped by owner in peer order.  EVERY block passed to
+ * a distributed context has A.n + n_ghost rows; the ghost rows are scratch the
+ * library fills before each SpMM.  A must be structurally symmetric, so the rows
+ * rank r sends to peer q are exactly q's ghost rows from r (in the same order).
+ * paper_1507_06078_b200/partition.py builds this plan from a global CSR. */
+typedef struct arr_comm arr_comm;
+
+typedef struct {
+    int64_t n_global;          /* rows of the global A                                   */
+    int64_t row_begin;         /* first owned global row                                 */
+    int64_t n_ghost;           /* ghost rows appended after the owned rows               */
+    int32_t npeers;            /* exchange partners                                      */
+    const int32_t *peer;       /* host [npeers] ranks (!= own rank)                      */
+    const int64_t *send_off;   /* host [npeers+1] offsets into send_rows                 */
+    const int32_t *send_rows;  /* host [send_off[npeers]] local owned rows sent to peer q */
+    const int64_t *recv_off;   /* host [npeers+1]; ghost rows from peer q are local rows
+                                  A.n + recv_off[q] .. A.n + recv_off[q+1]-1;
+                                  recv_off[npeers] == n_ghost                            */
+    const int64_t *int_row0;   /* host [n_int_tiles] interior row tiles (rows with no ghost
+                                  column; computed while the exchange is in flight)      */
+    const int32_t *int_len;    /* 1..64 rows each                                        */
+    int64_t n_int_tiles;
+    const int64_t *bnd_row0;   /* host [n_bnd_tiles] boundary row tiles (computed after   */
+    const int32_t *bnd_len;    /* the exchange); interior + boundary = every owned row once */
+    int64_t n_bnd_tiles;
+} arr_dist;
+
+/* NCCL communicator of one rank (one process per GPU; call with the rank's
+ * device current).  id: 128 bytes from comm_get_nccl_id on one rank, broadcast
+ * to all (e.g. with torch.distributed).  Collective over the size ranks. */
+arr_status comm_get_nccl_id(unsigned char *id_out /* [128] */);
+arr_status comm_init_nccl(arr_comm **out, const unsigned char *id, int32_t rank, int32_t size);
+/* size communicators for size ranks driven by size host threads of ONE
+ * process (any devices it can address; the same GPU is allowed).  The same
+ * exchange, reductions and broadcasts as NCCL, done with device copies and
+ * fixed-order reduction kernels ordered by host barriers and stream events.
+ * out: host array [size].  Used to test the distributed path on one GPU. */
+arr_status comm_init_local_group(arr_comm **out, int32_t size);
+arr_status comm_rank_size(const arr_comm *m, int32_t *rank, int32_t *size);
+/* Destroy after every context using it is destroyed. */
+arr_status comm_destroy(arr_comm *m);
 
 /* Options / report of the fixed-parameter driver eig_solve. */
 typedef struct {
@@ -88,6 +139,15 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
  * passed to filter_step / arr_project / eig_solve are then n x w; residuals and
  * the stop rule use the k leading pairs; b = mu_{w+1}. */
 arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w, int32_t p, int32_t d, void *stream);
+/* Distributed context (collective over the ranks of comm): A_local is this
+ * rank's local CSR (see arr_dist), k/w/p/d as eig_init_w with (p+1)w < n_global.
+ * Every later call on the context is collective: all ranks make the same
+ * sequence of calls.  Gram products, column norms, residual norms, Ritz values
+ * and eigenvalues are reduced over ranks and identical on every rank; blocks
+ * hold the owned rows (+ ghost scratch rows).  comm == NULL or a group of one
+ * behaves as eig_init_w.  The plan's host arrays are copied. */
+arr_status eig_init_dist(arr_ctx **out, const arr_csr *A_local, int32_t k, int32_t w, int32_t p, int32_t d,
+                         const arr_dist *dist, arr_comm *comm, void *stream);
 arr_status eig_destroy(arr_ctx *c);
 const char *eig_last_error(const arr_ctx *c);
 size_t eig_workspace_bytes(const arr_ctx *c);

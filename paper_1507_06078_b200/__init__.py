@@ -7,11 +7,14 @@ library on import and fails loudly if it is missing — there is no CPU path.
 from . import _lib
 from .api import (  # noqa: F401
     ArrError,
+    Comm,
     DeviceCSR,
     EigContext,
     eig_init,
     eig_solve_host,
     to_device_csr,
 )
+
+from . import partition  # noqa: F401,E402
 
 LIB = _lib.load()

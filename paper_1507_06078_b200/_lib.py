@@ -9,8 +9,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ARRABIT_LIB", os.path.join(HERE, "libarrabit.so"))  # override: tuning variants
 
-ARR_OK, ARR_EINVAL, ARR_ENOMEM, ARR_ECUDA, ARR_ECUSOLVER, ARR_ENUMERIC = 0, 1, 2, 3, 5, 7
-STATUS_NAMES = {0: "ARR_OK", 1: "ARR_EINVAL", 2: "ARR_ENOMEM", 3: "ARR_ECUDA", 5: "ARR_ECUSOLVER",
+ARR_OK, ARR_EINVAL, ARR_ENOMEM, ARR_ECUDA, ARR_ECUSOLVER, ARR_ENCCL, ARR_ENUMERIC = 0, 1, 2, 3, 5, 6, 7
+STATUS_NAMES = {0: "ARR_OK", 1: "ARR_EINVAL", 2: "ARR_ENOMEM", 3: "ARR_ECUDA", 5: "ARR_ECUSOLVER", 6: "ARR_ENCCL",
                 7: "ARR_ENUMERIC"}
 
 # Every symbol include/arrabit.h declares (checked by tests/test_abi.py).
@@ -19,12 +19,21 @@ EXPORTED = [
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
     "eig_set_timing", "eig_phase_times", "eig_set_schedule",
+    "eig_init_dist", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
 ]
 
 
 class arr_csr(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p),
                 ("col_idx", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class arr_dist(ctypes.Structure):
+    _fields_ = [("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("n_ghost", ctypes.c_int64),
+                ("npeers", ctypes.c_int32), ("peer", ctypes.c_void_p), ("send_off", ctypes.c_void_p),
+                ("send_rows", ctypes.c_void_p), ("recv_off", ctypes.c_void_p),
+                ("int_row0", ctypes.c_void_p), ("int_len", ctypes.c_void_p), ("n_int_tiles", ctypes.c_int64),
+                ("bnd_row0", ctypes.c_void_p), ("bnd_len", ctypes.c_void_p), ("n_bnd_tiles", ctypes.c_int64)]
 
 
 class arr_solve_opts(ctypes.Structure):
@@ -55,6 +64,13 @@ def load(path: str = LIB_PATH):
     sig = {
         "eig_init": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, vp], ctypes.c_int),
         "eig_init_w": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, vp], ctypes.c_int),
+        "eig_init_dist": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, ctypes.POINTER(arr_dist), vp, vp],
+                          ctypes.c_int),
+        "comm_get_nccl_id": ([ctypes.c_char_p], ctypes.c_int),
+        "comm_init_nccl": ([pvp, ctypes.c_char_p, i32, i32], ctypes.c_int),
+        "comm_init_local_group": ([pvp, i32], ctypes.c_int),
+        "comm_rank_size": ([vp, pi32, pi32], ctypes.c_int),
+        "comm_destroy": ([vp], ctypes.c_int),
         "eig_destroy": ([vp], ctypes.c_int),
         "eig_last_error": ([vp], ctypes.c_char_p),
         "eig_workspace_bytes": ([vp], ctypes.c_size_t),

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import arr_csr, arr_solve_info, arr_solve_opts
+from ._lib import arr_csr, arr_dist, arr_solve_info, arr_solve_opts
 
 
 class ArrError(RuntimeError):
@@ -55,18 +55,102 @@ def _stream_handle(stream):
     return ctypes.c_void_p(stream.cuda_stream), stream
 
 
-class EigContext:
-    """An arr_ctx (eig_init ... eig_destroy)."""
+class Comm:
+    """An arr_comm: NCCL (one process per GPU) or one rank of an in-process group."""
 
-    def __init__(self, A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None):
+    def __init__(self, handle: ctypes.c_void_p, owner=None):
+        self.lib = _lib.load()
+        self.h = handle
+        self._owner = owner
+        r, s = ctypes.c_int32(), ctypes.c_int32()
+        self.lib.comm_rank_size(self.h, ctypes.byref(r), ctypes.byref(s))
+        self.rank, self.size = r.value, s.value
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _lib.load()
+        buf = ctypes.create_string_buffer(128)
+        st = lib.comm_get_nccl_id(buf)
+        if st != 0:
+            raise ArrError(st, "comm_get_nccl_id failed")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, uid: bytes, rank: int, size: int) -> "Comm":
+        """Collective over the size ranks; the rank's device must be current."""
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        st = lib.comm_init_nccl(ctypes.byref(h), uid, int(rank), int(size))
+        if st != 0:
+            raise ArrError(st, "comm_init_nccl failed")
+        return cls(h)
+
+    @classmethod
+    def from_torch_distributed(cls) -> "Comm":
+        """NCCL communicator over the default torch.distributed group (rank 0's
+        unique id is broadcast with torch.distributed; the data path is NCCL
+        inside libarrabit)."""
+        import torch.distributed as dist
+        obj = [cls.nccl_unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls.nccl(obj[0], dist.get_rank(), dist.get_world_size())
+
+    @classmethod
+    def local_group(cls, size: int) -> list["Comm"]:
+        """size communicators of one in-process group (one host thread per rank)."""
+        lib = _lib.load()
+        arr = (ctypes.c_void_p * size)()
+        st = lib.comm_init_local_group(arr, int(size))
+        if st != 0:
+            raise ArrError(st, "comm_init_local_group failed")
+        return [cls(ctypes.c_void_p(arr[r])) for r in range(size)]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.comm_destroy(self.h)
+            self.h = None
+
+
+def _dist_struct(plan):
+    """arr_dist from a partition.LocalPlan (host arrays; the library copies them)."""
+    keep = []
+
+    def p(a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        keep.append(a)
+        return ctypes.c_void_p(a.ctypes.data) if a.size else None
+
+    d = arr_dist(plan.n_global, plan.row_begin, plan.n_ghost, len(plan.peer), p(plan.peer, np.int32),
+                 p(plan.send_off, np.int64), p(plan.send_rows, np.int32), p(plan.recv_off, np.int64),
+                 p(plan.int_row0, np.int64), p(plan.int_len, np.int32), len(plan.int_row0),
+                 p(plan.bnd_row0, np.int64), p(plan.bnd_len, np.int32), len(plan.bnd_row0))
+    return d, keep
+
+
+class EigContext:
+    """An arr_ctx (eig_init ... eig_destroy).  With ``comm`` and ``plan`` (a
+    partition.LocalPlan whose local CSR is ``A``) it is one rank of a
+    distributed context (eig_init_dist): every call is collective and every
+    block has plan.n_rows_block rows."""
+
+    def __init__(self, A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None, comm=None,
+                 plan=None):
         self.lib = _lib.load()
         self.A = A  # keep the borrowed arrays alive
         self.k, self.p, self.d = k, p, d
         self.w = k if w is None else w
+        self.comm, self.plan = comm, plan
         self.handle_stream, self.stream = _stream_handle(stream)
         self._csr = arr_csr(A.n, A.nnz, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.val.data_ptr())
         h = ctypes.c_void_p()
-        st = self.lib.eig_init_w(ctypes.byref(h), ctypes.byref(self._csr), k, self.w, p, d, self.handle_stream)
+        if comm is not None:
+            if plan is None:
+                raise ValueError("a distributed context needs the rank's partition plan")
+            ds, _keep = _dist_struct(plan)
+            st = self.lib.eig_init_dist(ctypes.byref(h), ctypes.byref(self._csr), k, self.w, p, d, ctypes.byref(ds),
+                                        comm.h, self.handle_stream)
+        else:
+            st = self.lib.eig_init_w(ctypes.byref(h), ctypes.byref(self._csr), k, self.w, p, d, self.handle_stream)
         if st != 0:
             raise ArrError(st, "eig_init failed")
         self.h = h
@@ -212,9 +296,10 @@ class EigContext:
         return ev, res, info
 
 
-def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None) -> EigContext:
-    """eig_init (w = k) / eig_init_w (w >= k guard columns)."""
-    return EigContext(A, k, p, d, stream, w)
+def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None, comm=None,
+             plan=None) -> EigContext:
+    """eig_init (w = k) / eig_init_w (w >= k guard columns) / eig_init_dist (comm + plan)."""
+    return EigContext(A, k, p, d, stream, w, comm, plan)
 
 
 def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, s_max=5, evec=None,

@@ -24,7 +24,7 @@ enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2, INFO_CHOL = 40 };  // dinfo
 arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
     if (c) {
         c->err = msg;
-        if (code == ARR_ECUDA || code == ARR_ECUSOLVER) c->poisoned = code;
+        if (code == ARR_ECUDA || code == ARR_ECUSOLVER || code == ARR_ENCCL) c->poisoned = code;
     }
     return code;
 }
@@ -41,12 +41,18 @@ arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
             return fail(c, ARR_ECUSOLVER, std::string(#expr) + " failed: " + std::to_string((int)s_)); \
     } while (0)
 #define CHECK_LAUNCH() CUDA_TRY(cudaGetLastError())
+#define ST_TRY(expr)                                                                                \
+    do {                                                                                            \
+        arr_status st_ = (expr);                                                                    \
+        if (st_ != ARR_OK) return st_;                                                              \
+    } while (0)
 #define GUARD(c)                                                                                    \
     do {                                                                                            \
         if (!(c)) return ARR_EINVAL;                                                                \
         if ((c)->poisoned != ARR_OK) return (c)->poisoned;                                          \
     } while (0)
 
+inline int64_t n_glob(const arr_ctx *c) { return c->nranks > 1 ? c->plan.n_global : c->A.n; }
 inline int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
 inline int32_t m_of(const arr_ctx *c, int p) { return (p + 1) * c->w; }
 inline int64_t ldQ(const arr_ctx *c) { return even_up(m_of(c, c->p)); }
@@ -100,6 +106,63 @@ double chebT(int d, double t) {  // host recursion, Eq. cheby-poly
     return r1;
 }
 
+// ---------------------------------------------------------------- distributed building blocks
+inline bool is_dist(const arr_ctx *c) { return c->nranks > 1; }
+
+// Fused SpMM over the owned rows.  Distributed: start the ghost-row exchange
+// of Yin, compute the interior rows while it is in flight, then the boundary
+// rows.  Column sums of squares (if requested) of the two launches are written
+// to consecutive partial rows.  Returns the number of partial rows (< 0: width
+// not supported).
+int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st) {
+    *st = ARR_OK;
+    if (!is_dist(c)) return launch_spmm(c, s);
+    DistPlan &P = c->plan;
+    if ((*st = comm_halo_begin(c, s.Yin, s.ld_in, s.w)) != ARR_OK) return 0;
+    int rows = 0;
+    const double *part0 = s.partials;
+    if (P.n_int_tiles > 0) {
+        SpmmArgs a = s;
+        a.tile_row0 = P.int_row0; a.tile_len = P.int_len; a.ntiles = P.n_int_tiles;
+        const int g = launch_spmm(c, a);
+        if (g < 0) return g;
+        rows += g;
+    }
+    if ((*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
+    if (P.n_bnd_tiles > 0) {
+        SpmmArgs a = s;
+        a.tile_row0 = P.bnd_row0; a.tile_len = P.bnd_len; a.ntiles = P.n_bnd_tiles;
+        if (part0) a.partials = const_cast<double *>(part0) + (int64_t)rows * s.w;
+        const int g = launch_spmm(c, a);
+        if (g < 0) return g;
+        rows += g;
+    }
+    return rows;
+}
+
+// G = X^T Y over the owned rows, summed over ranks.
+arr_status gram_x(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2, double *G,
+                  int64_t ldg) {
+    launch_gram(c, X, ldx, m1, Y, ldy, m2, c->A.n, G, ldg, c->part);
+    if (is_dist(c)) {
+        if (ldg != m2) return fail(c, ARR_EINVAL, "distributed gram needs ldg == m2");
+        ST_TRY(comm_allreduce(c, G, (size_t)m1 * m2, 0));
+    }
+    return ARR_OK;
+}
+
+// out[col] = sqrt(sum of the nblk partial rows, over ranks) / max(1,|mu_div|)
+arr_status colnorm_x(arr_ctx *c, const double *partials, int nblk, int w, double *out, const double *mu_div) {
+    if (!is_dist(c)) {
+        launch_colnorm_finalize(c, partials, nblk, w, out, mu_div);
+        return ARR_OK;
+    }
+    launch_colsum(c, partials, nblk, w, out);
+    ST_TRY(comm_allreduce(c, out, (size_t)w, 0));
+    launch_colnorm_root(c, out, w, mu_div);
+    return ARR_OK;
+}
+
 // ---------------------------------------------------------------- pieces
 // Filter degrees; result left in X (normalised) -- no host sync.
 arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
@@ -126,7 +189,9 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
         s.shift = cc;
         s.Yout = other; s.ld_out = ldother;
         s.partials = (normalize && j == c->d - 1) ? c->part : nullptr;
-        const int g = launch_spmm(c, s);
+        arr_status st;
+        const int g = spmm_x(c, s, &st);
+        if (st != ARR_OK) return st;
         if (g < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
         nblk = g;
         std::swap(cur, other);
@@ -136,7 +201,7 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
     CHECK_LAUNCH();
     if (normalize) {
         double *nrm = colnorm_dev ? colnorm_dev : NORM_buf(c);
-        launch_colnorm_finalize(c, c->part, nblk, w, nrm, nullptr);
+        ST_TRY(colnorm_x(c, c->part, nblk, w, nrm, nullptr));
         launch_check_norms(c, nrm, w, c->dinfo + INFO_BAD);
         launch_scale_cols(c, cur, ldcur, X, ldx, c->A.n, w, nrm);
     } else if (cur != X) {
@@ -150,12 +215,13 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
 arr_status svqb_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
                      int *rank_slot) {
     double *G = G_buf(c), *V = V_buf(c), *B = B_buf(c), *D = D_buf(c);
-    launch_gram(c, In, ldin, ncols, In, ldin, ncols, c->A.n, G, ncols, c->part);
+    ST_TRY(gram_x(c, In, ldin, ncols, In, ldin, ncols, G, ncols));
     launch_svqb_prep(c, G, ncols, D, V);
     CHECK_LAUNCH();
     SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ncols, V, ncols,
                                 c->evals, c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
     launch_svqb_build(c, D, V, c->evals, ncols, kSvqbTau, B, rank_slot);
+    ST_TRY(comm_bcast(c, B, (size_t)ncols * ncols, 0));  // one transform on every rank
     launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n);
     CHECK_LAUNCH();
     return ARR_OK;
@@ -169,8 +235,8 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
                        bool shifted, int *info2, int *rank_slot) {
     double *G = G_buf(c), *Gs = V_buf(c), *B = B_buf(c), *D = D_buf(c);
     const double u = 1.1102230246251565e-16;
-    const double shift = shifted ? 11.0 * ((double)c->A.n * ncols + (double)ncols * (ncols + 1)) * u * ncols : 0.0;
-    launch_gram(c, In, ldin, ncols, In, ldin, ncols, c->A.n, G, ncols, c->part);
+    const double shift = shifted ? 11.0 * ((double)n_glob(c) * ncols + (double)ncols * (ncols + 1)) * u * ncols : 0.0;
+    ST_TRY(gram_x(c, In, ldin, ncols, In, ldin, ncols, G, ncols));
     launch_chol_prep(c, G, ncols, shift, D, Gs);
     CHECK_LAUNCH();
     SOLVER_TRY(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_UPPER, ncols, Gs, ncols, c->solver_work, c->solver_lwork,
@@ -180,6 +246,7 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
                                 c->trtri_dwork, c->trtri_dbytes, c->trtri_hwork.data(), c->trtri_hwork.size(),
                                 info2 + 1));
     launch_chol_build(c, D, Gs, ncols, B, c->evals, 100.0 * shift, rank_slot);
+    ST_TRY(comm_bcast(c, B, (size_t)ncols * ncols, 0));  // one transform on every rank
     launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n);
     CHECK_LAUNCH();
     return ARR_OK;
@@ -251,9 +318,12 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
             s.Yin = Q + (int64_t)(j - 1) * w; s.ld_in = lq;
             s.alpha = 1.0; s.shift = 0.0;
             s.Yout = T; s.ld_out = lt;
-            if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+            arr_status st2;
+            const int g = spmm_x(c, s, &st2);
+            if (st2 != ARR_OK) return st2;
+            if (g < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
             for (int pass = 0; pass < 2; ++pass) {
-                launch_gram(c, Q, lq, jw, T, lt, w, c->A.n, G_buf(c), w, c->part);
+                ST_TRY(gram_x(c, Q, lq, jw, T, lt, w, G_buf(c), w));
                 launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
             }
             CHECK_LAUNCH();
@@ -280,16 +350,23 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         s.Yin = Q + (int64_t)j * w; s.ld_in = lq;
         s.alpha = 1.0; s.shift = 0.0;
         s.Yout = T; s.ld_out = lt;
-        if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+        const int g = spmm_x(c, s, &st);
+        if (st != ARR_OK) return st;
+        if (g < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
         // upper block triangle only: rows [0, (j+1)w) of column block j (H is symmetric)
         launch_gram(c, Q, lq, (j + 1) * w, T, lt, w, c->A.n, H + (int64_t)j * w, m, c->part);
     }
+    if (is_dist(c)) ST_TRY(comm_allreduce(c, H, (size_t)m * m, 0));
     launch_symmetrize(c, H, m, w);
     CHECK_LAUNCH();
     { const int e = t_mark(c); t_add(c, 4, evs, e, 1); evs = e; }
     // H = V Theta V^T (Alg. RR step 3): small dense eig on device (not graded)
     SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, H, m, c->evals,
                                 c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
+    if (is_dist(c)) {  // one eigendecomposition on every rank
+        ST_TRY(comm_bcast(c, H, (size_t)m * m, 0));
+        ST_TRY(comm_bcast(c, c->evals, (size_t)m, 0));
+    }
     { const int e = t_mark(c); t_add(c, 5, evs, e, 1); evs = e; }
     // Y = Q V[:, leading w] (Alg. RR step 4; Alg. ARR step 4)
     if (Y) {
@@ -327,9 +404,11 @@ arr_status residuals_core(arr_ctx *c, const double *Y, int64_t ldy, const double
     s.alpha = 1.0; s.shift = 0.0; s.colshift = shift;
     s.Yout = nullptr;
     s.partials = c->part;
-    const int g = launch_spmm(c, s);
+    arr_status st;
+    const int g = spmm_x(c, s, &st);
+    if (st != ARR_OK) return st;
     if (g < 0) return fail(c, ARR_EINVAL, "residuals: unsupported width");
-    launch_colnorm_finalize(c, c->part, g, ncols, out, shift);
+    ST_TRY(colnorm_x(c, c->part, g, ncols, out, shift));
     CHECK_LAUNCH();
     t_add(c, 2, ev0, t_mark(c), 1);
     CUDA_TRY(cudaMemcpyAsync(c->h_stage, out, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c->stream));
@@ -350,12 +429,21 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
     return eig_init_w(out, A, k, k, p, d, stream);
 }
 
-arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, int32_t p, int32_t d, void *stream) {
+arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, int32_t p, int32_t d,
+                         const arr_dist *dist, arr_comm *comm, void *stream) {
     if (!out || !A) return ARR_EINVAL;
     *out = nullptr;
     if (A->n < 1 || A->n >= (int64_t(1) << 31) || A->nnz < 0 || !A->row_ptr || (A->nnz > 0 && (!A->col_idx || !A->val)))
         return ARR_EINVAL;
-    if (k < 1 || w_in < k || p < 0 || d < 1 || (int64_t)(p + 1) * w_in >= A->n || w_in > ARR_MAX_W) return ARR_EINVAL;
+    int32_t crank = 0, csize = 1;
+    if (comm && comm_rank_size(comm, &crank, &csize) != ARR_OK) return ARR_EINVAL;
+    const bool multi = csize > 1;
+    if (multi && !dist) return ARR_EINVAL;
+    const int64_t n_global = multi ? dist->n_global : A->n;
+    if (multi && (dist->n_ghost < 0 || A->n + dist->n_ghost >= (int64_t(1) << 31) || dist->row_begin < 0 ||
+                  dist->row_begin + A->n > n_global))
+        return ARR_EINVAL;
+    if (k < 1 || w_in < k || p < 0 || d < 1 || (int64_t)(p + 1) * w_in >= n_global || w_in > ARR_MAX_W) return ARR_EINVAL;
     arr_ctx *c = new (std::nothrow) arr_ctx();
     if (!c) return ARR_ENOMEM;
     c->A = *A;
@@ -366,7 +454,7 @@ arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (c->num_sms <= 0) c->num_sms = 148;
-    const int64_t n = A->n, w = w_in, m = (int64_t)(p + 1) * w_in;
+    const int64_t n = A->n + (multi ? dist->n_ghost : 0), w = w_in, m = (int64_t)(p + 1) * w_in;
     const int64_t lq = even_up(m), lt = even_up(w);
     const int64_t mm = std::max<int64_t>(m, ARR_MAX_W);
     c->part_elems = (size_t)std::max<int64_t>(16 * m * w, 4096 * mm);
@@ -433,6 +521,14 @@ arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, 
         return ARR_ENOMEM;
     }
     c->ws_bytes = total;
+    if (multi) {
+        if (comm_setup_plan(c, dist, comm) != ARR_OK) {
+            const arr_status e = c->poisoned != ARR_OK ? c->poisoned : ARR_EINVAL;
+            fprintf(stderr, "eig_init_dist: %s\n", c->err.c_str());
+            eig_destroy(c);
+            return e;
+        }
+    }
     launch_rowlen_max(c, c->dinfo + 63);
     if (cudaMemcpyAsync(c->h_istage, c->dinfo + 63, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
         cudaStreamSynchronize(c->stream) != cudaSuccess) {
@@ -441,8 +537,23 @@ arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, 
         return ARR_ECUDA;
     }
     c->max_row_nnz = c->h_istage[0];
+    if (multi) {  // one chunk size on every rank (the per-row arithmetic does not depend on it)
+        c->h_stage[0] = (double)c->max_row_nnz;
+        if (cudaMemcpyAsync(c->vecw, c->h_stage, sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+            comm_allreduce(c, c->vecw, 1, 2) != ARR_OK ||
+            cudaMemcpyAsync(c->h_stage, c->vecw, sizeof(double), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+            cudaStreamSynchronize(c->stream) != cudaSuccess) {
+            eig_destroy(c);
+            return ARR_ENCCL;
+        }
+        c->max_row_nnz = (int)c->h_stage[0];
+    }
     *out = c;
     return ARR_OK;
+}
+
+arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, int32_t p, int32_t d, void *stream) {
+    return eig_init_dist(out, A, k, w_in, p, d, nullptr, nullptr, stream);
 }
 
 arr_status eig_destroy(arr_ctx *c) {
@@ -456,6 +567,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_istage) cudaFreeHost(c->h_istage);
     if (c->solver) cusolverDnDestroy(c->solver);
+    comm_free_plan(c);
     delete c;
     return ARR_OK;
 }
@@ -471,6 +583,7 @@ arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out) {
     launch_gershgorin(c, c->part, &nb);
     launch_min_finalize(c, c->part, nb, NORM_buf(c));
     CHECK_LAUNCH();
+    ST_TRY(comm_allreduce(c, NORM_buf(c), 1, 1));
     CUDA_TRY(cudaMemcpyAsync(c->h_stage, NORM_buf(c), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     *a_out = c->h_stage[0];
@@ -486,6 +599,7 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b) {
 
 arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles) {
     GUARD(c);
+    if (is_dist(c)) return fail(c, ARR_EINVAL, "schedule: not supported on a distributed context");
     if (!tile_row0) {
         c->tile_row0 = nullptr; c->tile_len = nullptr; c->ntiles = 0;
         return ARR_OK;
@@ -563,7 +677,7 @@ arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const doub
                 double *G, int64_t ldg) {
     GUARD(c);
     if (!block_ok(X, ldx, m1) || !block_ok(Y, ldy, m2) || !G || ldg < m2) return fail(c, ARR_EINVAL, "bad gram args");
-    launch_gram(c, X, ldx, m1, Y, ldy, m2, c->A.n, G, ldg, c->part);
+    ST_TRY(gram_x(c, X, ldx, m1, Y, ldy, m2, G, ldg));
     CHECK_LAUNCH();
     return ARR_OK;
 }

@@ -12,6 +12,25 @@
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
 constexpr int kPhases = 6;  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
 
+// Row-partition plan of one rank (comm.cu; arr_dist in include/arrabit.h).
+struct DistPlan {
+    int64_t n_global = 0, row_begin = 0, n_ghost = 0;
+    std::vector<int> peer;                 // exchange partners (ranks)
+    std::vector<int64_t> send_off, recv_off;
+    std::vector<char> send_contig;         // rows sent to peer q are one contiguous range
+    std::vector<int64_t> send_first;       // first row of that range
+    int32_t *send_rows_dev = nullptr;
+    double *sendbuf = nullptr, *recvbuf = nullptr;  // packed rows (ld = even ncols)
+    int64_t *int_row0 = nullptr, *bnd_row0 = nullptr;
+    int32_t *int_len = nullptr, *bnd_len = nullptr;
+    int64_t n_int_tiles = 0, n_bnd_tiles = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+    bool cur_direct = true;                // state of the exchange in flight
+    int cur_ncols = 0;
+    int64_t cur_ld = 0;
+};
+
 struct arr_ctx {
     // problem
     arr_csr A;
@@ -56,6 +75,12 @@ struct arr_ctx {
     std::vector<Pending> pending;
     double phase_ms[6];
     int64_t phase_cnt[6];
+    // multi-GPU (eig_init_dist): communicator, partition plan, allreduce staging
+    arr_comm *comm;
+    int nranks;  // size of comm (1 without one)
+    DistPlan plan;
+    double *stage;
+    size_t stage_elems;
     // pinned host staging
     double *h_stage;   // [m + 2*ARR_MAX_W + 16]
     int *h_istage;     // [16]
@@ -89,6 +114,10 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a);
 // out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)
 void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,
                              const double *mu_div);
+// out[col] = sum_b partials[b*w + col] (no root; multi-GPU: allreduced, then launch_colnorm_root)
+void launch_colsum(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out);
+// x[col] = sqrt(x[col]) / (mu_div ? max(1,|mu_div[col]|) : 1)
+void launch_colnorm_root(arr_ctx *c, double *x, int32_t w, const double *mu_div);
 // X[i, col] *= 1/norm[col] (in place) or Out = In / norm
 void launch_scale_cols(arr_ctx *c, const double *In, int64_t ld_in, double *Out, int64_t ld_out,
                        int64_t n, int32_t w, const double *norms);
@@ -98,6 +127,16 @@ void launch_rowlen_max(arr_ctx *c, int *dev_out);
 void launch_schedule_check(arr_ctx *c, const int64_t *row0, const int32_t *len, int64_t ntiles, int *marks,
                            int *bad);
 void launch_min_finalize(arr_ctx *c, const double *partial, int nblk, double *out);
+
+// ---------------------------------------------------------------- multi-GPU (comm.cu)
+// All are no-ops when the context has no communicator or a group of one.
+// op: 0 sum, 1 min, 2 max.  Results are identical on every rank.
+arr_status comm_allreduce(arr_ctx *c, double *buf, size_t count, int op);
+arr_status comm_bcast(arr_ctx *c, double *buf, size_t count, int root);
+arr_status comm_halo_begin(arr_ctx *c, const double *Y, int64_t ld, int ncols);
+arr_status comm_halo_end(arr_ctx *c, double *Y);
+arr_status comm_setup_plan(arr_ctx *c, const arr_dist *d, arr_comm *m);
+void comm_free_plan(arr_ctx *c);
 
 // ---------------------------------------------------------------- dense (DMMA)
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms);

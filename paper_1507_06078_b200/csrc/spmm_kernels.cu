@@ -493,6 +493,22 @@ __global__ void colnorm_finalize_kernel(const double *__restrict__ part, int nbl
     out[col] = r;
 }
 
+__global__ void colsum_kernel(const double *__restrict__ part, int nblk, int w, double *__restrict__ out) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= w) return;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * w + col];
+    out[col] = s;
+}
+
+__global__ void colnorm_root_kernel(double *x, int w, const double *__restrict__ mu_div) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= w) return;
+    double r = sqrt(x[col]);
+    if (mu_div) r /= fmax(1.0, fabs(mu_div[col]));
+    x[col] = r;
+}
+
 template <int VEC>
 __global__ void scale_cols_kernel(const double *In, int64_t ld_in, double *Out, int64_t ld_out, int64_t n,
                                   int wv, const double *__restrict__ norms) {
@@ -576,7 +592,7 @@ void launch_rowlen_max(arr_ctx *c, int *dev_out) {
 int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     SpmmArgs a = a_in;
     a.sched = c->sched;
-    if (c->tile_row0 && a.n == c->A.n) {
+    if (!a.tile_row0 && c->tile_row0 && a.n == c->A.n) {
         a.tile_row0 = c->tile_row0;
         a.tile_len = c->tile_len;
         a.ntiles = c->ntiles;
@@ -591,6 +607,16 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
 void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,
                              const double *mu_div) {
     colnorm_finalize_kernel<<<(w + 127) / 128, 128, 0, c->stream>>>(partials, nblk, w, out, mu_div);
+    c->launches++;
+}
+
+void launch_colsum(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out) {
+    colsum_kernel<<<(w + 127) / 128, 128, 0, c->stream>>>(partials, nblk, w, out);
+    c->launches++;
+}
+
+void launch_colnorm_root(arr_ctx *c, double *x, int32_t w, const double *mu_div) {
+    colnorm_root_kernel<<<(w + 127) / 128, 128, 0, c->stream>>>(x, w, mu_div);
     c->launches++;
 }
 
