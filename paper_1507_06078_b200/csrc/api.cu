@@ -247,7 +247,7 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
                                 info2 + 1));
     launch_chol_build(c, D, Gs, ncols, B, c->evals, 100.0 * shift, rank_slot);
     ST_TRY(comm_bcast(c, B, (size_t)ncols * ncols, 0));  // one transform on every rank
-    launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n);
+    launch_gemm(c, 1.0, In, ldin, ncols, B, ncols, ncols, 0.0, nullptr, 0, Out, ldout, c->A.n, /*upper=*/1);
     CHECK_LAUNCH();
     return ARR_OK;
 }

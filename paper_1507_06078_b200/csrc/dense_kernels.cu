@@ -62,6 +62,9 @@ __global__ void __launch_bounds__(THREADS) gram_kernel(const double *__restrict_
             Ys[buf][rr][cc] = ry[q];
         }
     };
+    // warps whose 32 x 32 sub-tile is out of range, or (symmetric) strictly below
+    // the diagonal, only help with the loads (their results are never read)
+    const bool work = (a0 + wm * 32 < m1) && (b0 + wn * 32 < m2) && !(sym && ta == tb && wm > wn);
     if (k0 < k1) {
         gload(k0);
         sstore(0);
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(THREADS) gram_kernel(const double *__restrict_
             if (more) gload(kb + KS);
 #pragma unroll
             for (int kk = 0; kk < KS / 4; ++kk) {
+                if (!work) continue;
                 double af[4], bf[4];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * 32 + mt * 8 + (lane >> 2)];
@@ -115,13 +119,16 @@ __global__ void gram_reduce_kernel(const double *__restrict__ part, int nsplit, 
     G[(int64_t)ra * ldg + cb] = s;
 }
 
-// Out[n x m2] = beta*Cin + alpha*X[n x m1] * B[m1 x m2]
+// Out[n x m2] = beta*Cin + alpha*X[n x m1] * B[m1 x m2].  upper != 0: B is upper
+// triangular (B[k][c] == 0 for k > c), so column tile c0 only needs k < c0 + TILE
+// (the skipped terms are exact zeros: same result).
 __global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const double *__restrict__ X, int64_t ldx,
                                                        int m1, const double *__restrict__ B, int64_t ldb, int m2,
                                                        double beta, const double *Cin, int64_t ldc, double *Out,
-                                                       int64_t ldo, int64_t n) {
+                                                       int64_t ldo, int64_t n, int upper) {
     const int64_t r0 = (int64_t)blockIdx.x * TILE;
     const int c0 = blockIdx.y * TILE;
+    if (upper && c0 + TILE < m1) m1 = c0 + TILE;
     __shared__ double Xs[2][TILE][KS + PAD];
     __shared__ double Bs[2][KS][TILE + PAD];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -279,9 +286,9 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
 
 void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
-                 int64_t n) {
+                 int64_t n, int upper) {
     dim3 grid((unsigned)((n + TILE - 1) / TILE), (m2 + TILE - 1) / TILE);
-    gemm_kernel<<<grid, THREADS, 0, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n);
+    gemm_kernel<<<grid, THREADS, 0, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
     c->launches++;
 }
 

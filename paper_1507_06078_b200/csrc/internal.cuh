@@ -142,9 +142,10 @@ void comm_free_plan(arr_ctx *c);
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms);
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
                  int32_t m2, int64_t n, double *G, int64_t ldg, double *partials);
+// upper != 0: B is upper triangular (exact zeros below the diagonal are skipped)
 void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out,
-                 int64_t ldo, int64_t n);
+                 int64_t ldo, int64_t n, int upper = 0);
 // small dense helpers (single CTA-ish kernels)
 void launch_svqb_prep(arr_ctx *c, const double *G, int32_t w, double *D, double *Gs);
 void launch_svqb_build(arr_ctx *c, const double *D, const double *Vcm, const double *lam, int32_t w,
