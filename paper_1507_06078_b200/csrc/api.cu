@@ -508,6 +508,8 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         return ARR_ENOMEM;
     }
     c->orth_mode = getenv("ARRABIT_ORTH_SVQB") ? 1 : 0;
+    c->tile_rows = 64;
+    if (const char *tr = getenv("ARRABIT_TILE")) c->tile_rows = std::min(64, std::max(1, atoi(tr)));
     if (cudaMalloc(&c->solver_work, sizeof(double) * (size_t)c->solver_lwork) != cudaSuccess) {
         cudaGetLastError();
         eig_destroy(c);

@@ -38,6 +38,7 @@ struct arr_ctx {
     cudaStream_t stream;
     int num_sms;
     int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
+    int tile_rows;    // SpMM rows per tile in natural order (1..64; env ARRABIT_TILE)
     // interval
     double a, b;
     bool have_interval;

@@ -22,6 +22,12 @@ namespace {
 #ifndef ARR_SPMM_PAIR
 #define ARR_SPMM_PAIR 0
 #endif
+#ifndef ARR_SPMM_V4
+#define ARR_SPMM_V4 0  // 1: 256-bit accesses when the block is 32-byte aligned with ld % 4 == 0
+#endif
+#ifndef ARR_SPMM_SEQ
+#define ARR_SPMM_SEQ 0  // 1: each row slot walks a contiguous run of the tile's rows (L1 reuse of x-neighbours)
+#endif
 constexpr int kMaxThreads = ARR_SPMM_MAXT;  // fused SpMM CTA size (R x TX rounded to warps)
 
 #ifndef ARR_L2HINT
@@ -105,6 +111,54 @@ struct Vec<2> {
     }
 };
 
+struct __align__(32) d4 {
+    double x, y, z, w;
+};
+template <>
+struct Vec<4> {  // 256-bit accesses (sm_100: LDG/STG .ENL2.256)
+    using T = d4;
+    static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0}; }
+    static __device__ __forceinline__ T ldg(const double *p) {
+        d4 r;
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+        return r;
+    }
+    static __device__ __forceinline__ T ldcs(const double *p) {
+        d4 r;
+        asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+        return r;
+    }
+    static __device__ __forceinline__ void stcs(double *p, T v) {
+        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                     : "memory");
+    }
+    static __device__ __forceinline__ T ldg_h(const double *p, uint64_t pol) {
+        d4 r;
+        asm("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+            : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+            : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ T ldcs_h(const double *p, uint64_t pol) {
+        d4 r;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+                     : "l"(p), "l"(pol));
+        return r;
+    }
+    static __device__ __forceinline__ void stcs_h(double *p, T v, uint64_t pol) {
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                     "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol)
+                     : "memory");
+    }
+    static __device__ __forceinline__ double get(const T &v, int e) {
+        return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+    }
+    static __device__ __forceinline__ void set(T &v, int e, double x) {
+        if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
+    }
+};
+
 template <int VEC>
 __device__ __forceinline__ void fma_vec(typename Vec<VEC>::T &acc, double a, const typename Vec<VEC>::T &x);
 template <>
@@ -113,6 +167,13 @@ template <>
 __device__ __forceinline__ void fma_vec<2>(double2 &acc, double a, const double2 &x) {
     acc.x = fma(a, x.x, acc.x);
     acc.y = fma(a, x.y, acc.y);
+}
+template <>
+__device__ __forceinline__ void fma_vec<4>(d4 &acc, double a, const d4 &x) {
+    acc.x = fma(a, x.x, acc.x);
+    acc.y = fma(a, x.y, acc.y);
+    acc.z = fma(a, x.z, acc.z);
+    acc.w = fma(a, x.w, acc.w);
 }
 
 constexpr int kTile = 64;  // rows per tile (the unit of the processing order)
@@ -163,6 +224,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
     using V = Vec<VEC>;
     using T = typename V::T;
     constexpr int P = (ARR_SPMM_PAIR && NV == 1 && K <= 7) ? 2 : 1;  // rows in flight per thread
+    RR = (nrows + R - 1) / R;  // rows per slot for this (pass of the) tile
     const double *yin_v[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -171,7 +233,8 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
     }
     if constexpr (P == 2) {
         for (int rr = 0; rr < RR; rr += 2) {
-            const int lr0 = rr * R + r, lr1 = lr0 + R;
+            const int lr0 = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
+            const int lr1 = ARR_SPMM_SEQ ? lr0 + 1 : lr0 + R;
             if (lr0 >= nrows) break;
             const bool has1 = (rr + 1 < RR) && (lr1 < nrows);
             const int64_t i0 = r0 + lr0, i1 = r0 + (has1 ? lr1 : lr0);
@@ -209,7 +272,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
         }
     } else {
         for (int rr = 0; rr < RR; ++rr) {
-            const int lr = rr * R + r;
+            const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
             if (lr >= nrows) break;
             const int64_t i = r0 + lr;
             T yp[NV];
@@ -260,10 +323,10 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
 // A tile whose slice exceeds the staging capacity is staged in several passes
 // of whole rows.
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
-__global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RR, int wv,
+__global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
                                                                     int64_t ntiles, int nnz_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int RT = kTile;
+    const int RR = 0;  // recomputed per tile in tile_rows
     Ent *s_ent = reinterpret_cast<Ent *>(smem_raw);                      // [nnz_cap]
     int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [RT+1] (relative)
     __shared__ int64_t s_base;
@@ -416,8 +479,7 @@ template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool CO
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
     const int nthr = ((R * TX + 31) / 32) * 32;
-    const int RR = R >= kTile ? 1 : (kTile + R - 1) / R;
-    const int RT = kTile;
+    const int RT = c->tile_rows;  // rows per tile in natural order (<= kTile)
     // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
     size_t smem = sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(RT + 2);
     const size_t red = 8 * (size_t)nthr * VEC;
@@ -435,7 +497,7 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     int64_t G = (int64_t)c->num_sms * occ;
     if (G > ntiles) G = ntiles;
     if (G < 1) G = 1;
-    kern<<<(unsigned)G, nthr, smem, c->stream>>>(a, TX, R, RR, wv, ntiles, kNnzCap);
+    kern<<<(unsigned)G, nthr, smem, c->stream>>>(a, TX, R, RT, wv, ntiles, kNnzCap);
     c->launches++;
     return (int)G;
 }
@@ -577,6 +639,7 @@ __global__ void copy_rows_kernel(const double *__restrict__ src, int64_t lds, do
 }
 
 bool vec2_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
+bool vec4_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 32 == 0) && (ld % 4 == 0); }
 
 }  // namespace
 
@@ -601,6 +664,12 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     if (a.Yprev) v2 = v2 && vec2_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
     c->spmm_blocks++;
+#if ARR_SPMM_V4
+    bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
+    if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);
+    if (a.Yout) v4 = v4 && vec4_ok(a.Yout, a.ld_out);
+    if (v4) return dispatch_nv<4>(c, a);
+#endif
     return v2 ? dispatch_nv<2>(c, a) : dispatch_nv<1>(c, a);
 }
 

@@ -19,17 +19,17 @@ def natural(n: int):
     return r0, np.minimum(TILE, n - r0).astype(np.int32)
 
 
-def ranges_to_tiles(starts: np.ndarray, lens: np.ndarray):
-    """Split contiguous row ranges (in processing order) into tiles of <= TILE rows."""
+def ranges_to_tiles(starts: np.ndarray, lens: np.ndarray, tile: int = TILE):
+    """Split contiguous row ranges (in processing order) into tiles of <= tile rows."""
     r0_list, len_list = [], []
     for s, l in zip(starts.tolist(), lens.tolist()):
-        off = np.arange(0, l, TILE, dtype=np.int64)
+        off = np.arange(0, l, tile, dtype=np.int64)
         r0_list.append(s + off)
-        len_list.append(np.minimum(TILE, l - off))
+        len_list.append(np.minimum(tile, l - off))
     return np.concatenate(r0_list).astype(np.int64), np.concatenate(len_list).astype(np.int32)
 
 
-def yband_3d(nx: int, ny: int, nz: int, by: int):
+def yband_3d(nx: int, ny: int, nz: int, by: int, tile: int = TILE):
     """for each y-band of `by` lines: for z: the contiguous rows of that band at z."""
     starts, lens = [], []
     for yb in range(0, ny, by):
@@ -37,7 +37,7 @@ def yband_3d(nx: int, ny: int, nz: int, by: int):
         for z in range(nz):
             starts.append(nx * yb + nx * ny * z)
             lens.append(nx * h)
-    return ranges_to_tiles(np.array(starts, dtype=np.int64), np.array(lens, dtype=np.int64))
+    return ranges_to_tiles(np.array(starts, dtype=np.int64), np.array(lens, dtype=np.int64), tile)
 
 
 def auto_band(nx: int, ny: int, w: int, l2_bytes: float = 126e6, frac: float = 0.25) -> int:

@@ -1,16 +1,14 @@
 #!/bin/bash
-# One GPU session (round 1, call 2): tests (incl. distributed on one GPU and full sizes),
-# benches, per-config filter rates, ncu of the dominant filter-degree kernel.
+# Round 1, call 5: filter kernel variants x tile sizes; y-band with small tiles; L2 micro-benchmark.
 set -x
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_dist.py -x -q > gpurun_out/pytest_dist.log 2>&1; echo "exit $?" >> gpurun_out/pytest_dist.log
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?" >> gpurun_out/bench.err
-for c in 3 4 5; do timeout 900 python scripts/profile_step.py --config $c --filter-only --reps 3 > gpurun_out/filter_cfg$c.log 2>&1; done
-timeout 1200 python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
-PCMD="python scripts/profile_step.py --config 2 --filter-only"
-timeout 600 $PCMD > gpurun_out/plain_prof.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_tile -s 25 -c 3 -o gpurun_out/prof_spmm2 $PCMD > gpurun_out/ncu_full.log 2>&1
+./scripts/micro_l2 > gpurun_out/micro_l2.log 2>&1
+for lib in build/libarrabit_*.so; do
+  for c in 2 3; do
+    echo "== $lib cfg$c" >> gpurun_out/variants2.log
+    ARRABIT_LIB=$PWD/$lib timeout 400 python scripts/profile_step.py --config $c --filter-only --reps 3 --tiles 16 32 64 2>&1 | grep "filter degree" >> gpurun_out/variants2.log
+  done
+done
+timeout 900 python scripts/profile_step.py --config 3 --filter-only --reps 3 --tiles 8 16 32 --band 0 5 10 > gpurun_out/band2_cfg3.log 2>&1
+timeout 1200 python scripts/profile_step.py --config 5 --filter-only --reps 2 --tiles 16 32 --band 0 4 8 > gpurun_out/band2_cfg5.log 2>&1
 echo done

@@ -27,7 +27,9 @@ def main():
     ap.add_argument("--k", type=int, default=None, help="override block width (filter only)")
     ap.add_argument("--filter-only", action="store_true")
     ap.add_argument("--size", type=int, default=None, help="override the generator size (grid edge or n)")
-    ap.add_argument("--band", type=int, default=0, help="3-D y-band schedule height (0 natural, -1 auto)")
+    ap.add_argument("--tiles", type=int, nargs="*", default=[0], help="ARRABIT_TILE values to try (0: default)")
+    ap.add_argument("--band", type=int, nargs="*", default=[0],
+                    help="3-D y-band schedule heights to try in turn (0 natural, -1 auto)")
     args = ap.parse_args()
     spec = configs.CONFIGS[args.config]
     if args.size:
@@ -35,44 +37,56 @@ def main():
         spec = dataclasses.replace(spec, size=args.size, name=f"{spec.name}@{args.size}")
     A, spec = configs.build_config(spec)
     k = args.k or spec.w
-    ctx = arr.eig_init(arr.to_device_csr(A), k, spec.p if not args.filter_only else 0, spec.d)
+    Ad = arr.to_device_csr(A)
     X = torch.empty((A.n, k), dtype=torch.float64, device="cuda")
     for r0 in range(0, A.n, 1 << 21):  # seeded X0, uploaded in row chunks
         r1 = min(A.n, r0 + (1 << 21))
         X[r0:r1] = torch.from_numpy(synth.gaussian_block_rows(A.n, k, spec.seed, r0, r1))
-    if args.band and spec.kind in ("lap3dV", "st27"):
-        from paper_1507_06078_b200 import schedule
-        N = spec.size
-        by = schedule.auto_band(N, N, k) if args.band < 0 else args.band
-        ctx.eig_set_schedule(*schedule.yband_3d(N, N, N, by))
-        print(f"y-band schedule by={by}")
-    a = ctx.eig_gershgorin_lower()
     rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
     upper = float(np.bincount(rows, weights=np.abs(A.val), minlength=A.n).max())
-    ctx.eig_set_interval(a, a + 0.9 * (upper - a))
-    Y = torch.empty_like(X)
-    for _ in range(args.warmup):
-        ctx.filter_step(X, normalize=True)
-        if not args.filter_only:
-            ritz, _ = ctx.arr_project(X, Y)
-            ctx.residuals(Y, ritz[:k])
-    torch.cuda.synchronize()
-    ctx.eig_set_timing(True)
-    t = time.perf_counter()
-    for _ in range(args.reps):
-        ctx.filter_step(X, normalize=True)
-        if not args.filter_only:
-            ritz, _ = ctx.arr_project(X, Y)
-            ctx.residuals(Y, ritz[:k])
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t
-    ms, cnt = ctx.eig_phase_times()
-    deg_us = ms[0] / max(cnt[0], 1) * 1e3
-    bpl = (12 * A.nnz + 8 * (A.n + 1) + 16 * A.n * k + (spec.d - 1) * (12 * A.nnz + 8 * (A.n + 1) + 24 * A.n * k)) / spec.d
-    print(f"filter degree: {bpl/1e6:.1f} MB algorithmic / {deg_us:.1f} us = {bpl/deg_us/1e3:.0f} GB/s")
-    print(f"config {spec.name} k={k}: wall {wall*1e3:.2f} ms; filter {ms[0]:.3f} ms / {cnt[0]} degree launches "
-          f"({ms[0]/max(cnt[0],1)*1e3:.1f} us each); arr {ms[1]:.3f} ms / {cnt[1]} [basis {ms[3]:.3f} H {ms[4]:.3f} "
-          f"eig {ms[5]:.3f}]; residuals {ms[2]:.3f} ms / {cnt[2]}")
+    Y = torch.empty_like(X) if not args.filter_only else None
+    from paper_1507_06078_b200 import schedule
+    import itertools
+    ctx = None
+    for tile, band in itertools.product(args.tiles, args.band):
+      if tile:
+          os.environ["ARRABIT_TILE"] = str(tile)
+      if ctx is not None:
+          ctx.close()
+      ctx = arr.eig_init(Ad, k, spec.p if not args.filter_only else 0, spec.d)
+      a = ctx.eig_gershgorin_lower()
+      ctx.eig_set_interval(a, a + 0.9 * (upper - a))
+      if True:
+        if band and spec.kind in ("lap3dV", "st27"):
+            N = spec.size
+            by = schedule.auto_band(N, N, k) if band < 0 else band
+            ctx.eig_set_schedule(*schedule.yband_3d(N, N, N, by, tile or 64))
+            tag = f"tile={tile} y-band by={by}"
+        else:
+            ctx.eig_set_schedule(None)
+            tag = f"tile={tile} natural order"
+        for _ in range(args.warmup):
+            ctx.filter_step(X, normalize=True)
+            if not args.filter_only:
+                ritz, _ = ctx.arr_project(X, Y)
+                ctx.residuals(Y, ritz[:k])
+        torch.cuda.synchronize()
+        ctx.eig_set_timing(True)
+        t = time.perf_counter()
+        for _ in range(args.reps):
+            ctx.filter_step(X, normalize=True)
+            if not args.filter_only:
+                ritz, _ = ctx.arr_project(X, Y)
+                ctx.residuals(Y, ritz[:k])
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t
+        ms, cnt = ctx.eig_phase_times()
+        deg_us = ms[0] / max(cnt[0], 1) * 1e3
+        bpl = (12 * A.nnz + 8 * (A.n + 1) + 16 * A.n * k + (spec.d - 1) * (12 * A.nnz + 8 * (A.n + 1) + 24 * A.n * k)) / spec.d
+        print(f"[{tag}] filter degree: {bpl/1e6:.1f} MB algorithmic / {deg_us:.1f} us = {bpl/deg_us/1e3:.0f} GB/s")
+        print(f"[{tag}] config {spec.name} k={k}: wall {wall*1e3:.2f} ms; filter {ms[0]:.3f} ms / {cnt[0]} degree launches "
+              f"({deg_us:.1f} us each); arr {ms[1]:.3f} ms / {cnt[1]} [basis {ms[3]:.3f} H {ms[4]:.3f} "
+              f"eig {ms[5]:.3f}]; residuals {ms[2]:.3f} ms / {cnt[2]}", flush=True)
 
 
 if __name__ == "__main__":
