@@ -314,6 +314,36 @@ def run_ours(args):
                                       "arr_basis": phase_ms[3] / args.steps, "arr_H": phase_ms[4] / args.steps,
                                       "arr_small_eig": phase_ms[5] / args.steps,
                                       "residuals": phase_ms[2] / args.steps}}
+    # the DMMA Gram kernel of A4 (X^T Y, n x w by n x w, 2 n w^2 flops) timed alone on this block
+    dense = None
+    try:
+        G = torch.empty((spec.w, spec.w), dtype=torch.float64, device=dev)
+        nrow = r1 - r0
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                ctx.gram(X0[:nrow], X[:nrow], G)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            ev0.record(stream)
+            for _ in range(reps):
+                ctx.gram(X0[:nrow], X[:nrow], G)
+            ev1.record(stream)
+            ev1.synchronize()
+        gms = ev0.elapsed_time(ev1) / reps
+        fl = 2.0 * nrow * spec.w * spec.w
+        pk = None
+        pp = os.path.join(ROOT, "profiles", "peaks_fp64.json")
+        if os.path.exists(pp):
+            with open(pp) as f:
+                pk = json.load(f).get("fp64_dgemm_tflops_burst")
+        dense = {"bound": "tensor (FP64 DMMA)", "kernel": "gram_kernel + gram_reduce_kernel (X^T Y, n x w)",
+                 "achieved": fl / (gms / 1e3) / 1e12, "unit": "TFLOP/s", "peak": pk,
+                 "frac": (fl / (gms / 1e3) / 1e12 / pk) if pk else None,
+                 "peak_source": "profiles/peaks_fp64.json (cuBLAS DGEMM 8192^3, measured)" if pk else None,
+                 "avg_launch_us": gms * 1e3, "flops_per_launch": fl}
+    except Exception as e:  # noqa: BLE001
+        dense = {"error": str(e)}
+    roofline["dense_gram"] = dense
     if spec.kind == "zipf":
         roofline["gather_model_bytes_per_launch"] = (12 * nnz_loc + 8 * (r1 - r0 + 1) + 8 * nnz_loc * spec.w
                                                      + 16 * (r1 - r0) * spec.w)

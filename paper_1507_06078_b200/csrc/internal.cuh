@@ -93,6 +93,7 @@ struct SpmmArgs {
     const int32_t *col;
     const double *val;
     int64_t n;
+    int64_t nnz;           // entries of A (bounds the CSR prefetch)
     int32_t w;
     const double *Yin;     // gathered operand Y_j
     int64_t ld_in;
@@ -160,4 +161,5 @@ void launch_chol_prep(arr_ctx *c, const double *G, int32_t w, double shift, doub
 void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32_t w, double *B, const double *Rdiag,
                        double rank_thr, int *rank_out);
 void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d);
+
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out);

@@ -25,6 +25,9 @@ namespace {
 #ifndef ARR_SPMM_V4
 #define ARR_SPMM_V4 0  // 1: 256-bit accesses when the block is 32-byte aligned with ld % 4 == 0
 #endif
+#ifndef ARR_SPMM_PREFETCH
+#define ARR_SPMM_PREFETCH 0  // 1: bulk L2 prefetch (UBLKPF) of the next tile's Y_{j-1} rows, Y_j leading edge, CSR slice
+#endif
 #ifndef ARR_SPMM_SEQ
 #define ARR_SPMM_SEQ 0  // 1: each row slot walks a contiguous run of the tile's rows (L1 reuse of x-neighbours)
 #endif
@@ -177,6 +180,23 @@ __device__ __forceinline__ void fma_vec<4>(d4 &acc, double a, const d4 &x) {
 }
 
 constexpr int kTile = 64;  // rows per tile (the unit of the processing order)
+
+// Bulk L2 prefetch of [p, p + bytes) (TMA engine; no registers, no smem):
+// the range is widened to 16-byte boundaries.
+__device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
+    if (bytes <= 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    uintptr_t cur = a & ~uintptr_t(15);
+    const uintptr_t end = (a + (uint64_t)bytes) & ~uintptr_t(15);  // never past the range's end
+    if (end <= cur) return;
+    uint64_t total = end - cur;
+    while (total > 0) {  // the size operand is 32-bit
+        const uint32_t chunk = total > (1u << 30) ? (1u << 30) : (uint32_t)total;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cur), "r"(chunk) : "memory");
+        cur += chunk;
+        total -= chunk;
+    }
+}
 
 // One staged non-zero: element offset of the referenced Y row and the value.
 struct __align__(16) Ent {
@@ -353,8 +373,12 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
     // one contiguous window); SUMSQ launches keep the static grid-stride
     // assignment so their per-CTA partial sums are deterministic.
     constexpr bool DYN = !SUMSQ;
-    __shared__ int64_t s_next;
-    for (int64_t t = blockIdx.x; t < ntiles;) {
+    __shared__ int64_t s_next[2];
+    __shared__ int64_t s_bw;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; ++it) {
+        // next tile of this CTA, taken one tile ahead (read after the staging barriers)
+        if (tid == 0) s_next[it & 1] = DYN ? (int64_t)gridDim.x + (int64_t)atomicAdd(a.sched, 1ull) : t + gridDim.x;
         int64_t r0;
         int nrows;
         if (a.tile_row0) {  // caller-given processing order of contiguous row ranges
@@ -425,19 +449,44 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
                 s_ent[q] = e;
             }
             __syncthreads();
+#if ARR_SPMM_PREFETCH
+            if (done == 0 && tid == nthr - 1) {
+                // Warm L2 for this CTA's next tile while this one is computed: its Y_{j-1}
+                // rows (a stream), the leading edge of the Y_j rows it gathers (first
+                // touch; band estimate bw = last column of this tile - its last row),
+                // and its row_ptr / CSR slice (estimated from this tile's density).
+                const int64_t tn = s_next[it & 1];
+                if (tn < ntiles) {
+                    int64_t r0n;
+                    int nn;
+                    if (a.tile_row0) { r0n = __ldg(a.tile_row0 + tn); nn = __ldg(a.tile_len + tn); }
+                    else { r0n = tn * RT; nn = (int)min((int64_t)RT, a.n - r0n); }
+                    if (HAS_PREV) l2_prefetch(a.Yprev + r0n * a.ld_prev, ((int64_t)(nn - 1) * a.ld_prev + a.w) * 8);
+                    const int64_t lastcol = cnt > 0 && nnz_t > 0 ? s_ent[nnz_t - 1].off / ld : r0;
+                    const int64_t bw = lastcol - (r0 + cnt - 1);
+                    int64_t e0 = r0n + bw, e1 = r0n + nn + bw;
+                    if (e0 < 0) e0 = 0;
+                    if (e1 > a.n) e1 = a.n;
+                    if (e1 > e0 && bw > 0) l2_prefetch(a.Yin + e0 * ld, ((e1 - e0 - 1) * ld + a.w) * 8);
+                    l2_prefetch(rp + r0n, (int64_t)(nn + 1) * 8);
+                    const int64_t per = (int64_t)nnz_t * nn / (cnt > 0 ? cnt : 1);
+                    const int64_t est = base + (int64_t)((double)(r0n - r0) * ((double)nnz_t / (cnt > 0 ? cnt : 1)));
+                    int64_t cnt_e = per + per / 8 + 32;
+                    if (est >= 0 && est < a.nnz) {
+                        if (est + cnt_e > a.nnz) cnt_e = a.nnz - est;
+                        l2_prefetch(col + est, cnt_e * 4);
+                        l2_prefetch(val + est, cnt_e * 8);
+                    }
+                }
+            }
+#endif
             if (active)
                 tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
                                                                         s_rp, s_ent, ss, pol_keep, pol_stream);
             done += cnt;
         }
-        if (DYN) {
-            __syncthreads();
-            if (tid == 0) s_next = (int64_t)gridDim.x + (int64_t)atomicAdd(a.sched, 1ull);
-            __syncthreads();
-            t = s_next;
-        } else {
-            t += gridDim.x;
-        }
+        __syncthreads();  // every thread is done with this tile's staging and has s_next
+        t = s_next[it & 1];
     }
     if (DYN && tid == 0) {
         // the last CTA to finish resets the ticket for the next launch
@@ -654,6 +703,7 @@ void launch_rowlen_max(arr_ctx *c, int *dev_out) {
 
 int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     SpmmArgs a = a_in;
+    a.nnz = c->A.nnz;
     a.sched = c->sched;
     if (!a.tile_row0 && c->tile_row0 && a.n == c->A.n) {
         a.tile_row0 = c->tile_row0;
