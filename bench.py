@@ -248,6 +248,14 @@ def run_ours(args):
     if partitioned:
         comm = arr.Comm.from_torch_distributed()
     ctx = arr.eig_init(Ad, spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm, plan=plan)
+    sched = None
+    if spec.kind in ("lap3dV", "st27") and not partitioned:
+        # 3-D grids: y-band processing order (results unchanged; shorter L2 reuse distance of the
+        # z-neighbour rows), band height and tile rows measured on B200 (profiles/)
+        from paper_1507_06078_b200 import schedule
+        by, tile = {"lap3dV": (10, 16), "st27": (8, 32)}[spec.kind]
+        ctx.eig_set_schedule(*schedule.yband_3d(spec.size, spec.size, spec.size, by, tile))
+        sched = f"y-band by={by}, {tile}-row tiles"
 
     def one_solve():
         X.copy_(X0)
@@ -422,7 +430,7 @@ def run_ours(args):
                 "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "w": spec.w, "d": spec.d,
                            "p": spec.p, "tol": spec.tol, "step": "one full eig_solve from X0",
                            "l2": "flushed between timed steps (256 MiB write), outside the events",
-                           "parallelism": par,
+                           "parallelism": par, "row_order": sched or "natural",
                            "converged": bool(conv), "outer": outer, "sweeps": sweeps, "maxres": maxres},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}

@@ -28,6 +28,9 @@ namespace {
 #ifndef ARR_SPMM_PREFETCH
 #define ARR_SPMM_PREFETCH 0  // 1: bulk L2 prefetch (UBLKPF) of the next tile's Y_{j-1} rows, Y_j leading edge, CSR slice
 #endif
+#ifndef ARR_SPMM_ASYNC
+#define ARR_SPMM_ASYNC 0  // 1: rows of <= 7 entries gathered by per-thread cp.async into shared-memory slots, one row ahead
+#endif
 #ifndef ARR_SPMM_SEQ
 #define ARR_SPMM_SEQ 0  // 1: each row slot walks a contiguous run of the tile's rows (L1 reuse of x-neighbours)
 #endif
@@ -204,6 +207,20 @@ struct __align__(16) Ent {
     double val;
 };
 
+__device__ __forceinline__ void cp_async16_ca(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kAsyncStages = 2;  // rows per thread in shared memory: one computed, one in flight
+
 // Epilogue of one row: out = alpha*(acc - shift*y_i) + beta*y_prev, column
 // sums of squares, evict-first store.
 template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
@@ -240,7 +257,8 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nrows, int R, int RR, int r, int TX,
                                           int v0, int wv, const int *s_rp, const Ent *s_ent,
-                                          double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream) {
+                                          double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream,
+                                          unsigned char *slots) {
     using V = Vec<VEC>;
     using T = typename V::T;
     constexpr int P = (ARR_SPMM_PAIR && NV == 1 && K <= 7) ? 2 : 1;  // rows in flight per thread
@@ -251,7 +269,59 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
         const int vv = v0 + v * TX;
         yin_v[v] = a.Yin + (vv < wv ? vv : 0) * VEC;
     }
-    if constexpr (P == 2) {
+    if constexpr (ARR_SPMM_ASYNC && VEC == 2 && NV == 1 && K <= 7) {
+        // Per-thread software pipeline through shared memory: the K gathers of
+        // Y_j, the Y_{j-1} element and y_i of row rr+1 are issued as cp.async
+        // (no registers held while in flight) before row rr is computed from its
+        // slots.  Each thread reads only the slots it filled: no block barrier.
+        constexpr int SL = K + 1;  // slots per row: K gathers, Y_{j-1} (y_i is an L1 load)
+        double2 *my = reinterpret_cast<double2 *>(slots) + threadIdx.x;
+        const int nthr = blockDim.x;
+        auto issue = [&](int rr, int st) {
+            const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
+            if (rr < RR && lr < nrows) {
+                const int64_t i = r0 + lr;
+                const int p0 = s_rp[lr], p1 = s_rp[lr + 1];
+                const int64_t safe = p0 < p1 ? s_ent[p0].off : i * a.ld_in;
+#pragma unroll
+                for (int u = 0; u < K; ++u) {
+                    const int64_t o = (p0 + u < p1) ? s_ent[p0 + u].off : safe;
+                    cp_async16_ca(my + (st * SL + u) * nthr, yin_v[0] + o);
+                }
+                if (HAS_PREV) cp_async16_cg(my + (st * SL + K) * nthr, a.Yprev + i * a.ld_prev + v0 * 2);
+            }
+            cp_async_commit();
+        };
+        issue(0, 0);
+        for (int rr = 0; rr < RR; ++rr) {
+            const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
+            if (lr >= nrows) break;
+            issue(rr + 1, (rr + 1) % kAsyncStages);
+            cp_async_wait<1>();  // row rr's group has landed
+            const int st = rr % kAsyncStages;
+            const int64_t i = r0 + lr;
+            const int p0 = s_rp[lr], p1 = s_rp[lr + 1];
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                const double av = (p0 + u < p1) ? s_ent[p0 + u].val : 0.0;
+                fma_vec<2>(acc, av, my[(st * SL + u) * nthr]);
+            }
+            const double2 yp = HAS_PREV ? my[(st * SL + K) * nthr] : make_double2(0.0, 0.0);
+            const double2 yi = V::ldg(a.Yin + i * a.ld_in + v0 * 2);
+            double2 out;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double sh = COLSHIFT ? __ldg(a.colshift + v0 * 2 + e) : a.shift;
+                double o = a.alpha * (V::get(acc, e) - sh * V::get(yi, e));
+                if (HAS_PREV) o += a.beta * V::get(yp, e);
+                V::set(out, e, o);
+                if (SUMSQ) ss[0][e] = fma(o, o, ss[0][e]);
+            }
+            if (STORE) STREAM_ST(a.Yout + i * a.ld_out + v0 * 2, out);
+        }
+        cp_async_wait<0>();
+    } else if constexpr (P == 2) {
         for (int rr = 0; rr < RR; rr += 2) {
             const int lr0 = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
             const int lr1 = ARR_SPMM_SEQ ? lr0 + 1 : lr0 + R;
@@ -348,7 +418,8 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int RR = 0;  // recomputed per tile in tile_rows
     Ent *s_ent = reinterpret_cast<Ent *>(smem_raw);                      // [nnz_cap]
-    int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [RT+1] (relative)
+    int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [kTile+2] (relative)
+    unsigned char *slots = smem_raw + ((sizeof(Ent) * nnz_cap + 4 * (kTile + 2) + 15) & ~size_t(15));  // async slots
     __shared__ int64_t s_base;
 
     const int tid = threadIdx.x;
@@ -482,7 +553,8 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
 #endif
             if (active)
                 tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
-                                                                        s_rp, s_ent, ss, pol_keep, pol_stream);
+                                                                        s_rp, s_ent, ss, pol_keep, pol_stream,
+                                                                        slots);
             done += cnt;
         }
         __syncthreads();  // every thread is done with this tile's staging and has s_next
@@ -522,7 +594,10 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
     }
 }
 
-constexpr int kNnzCap = 2048;
+#ifndef ARR_SPMM_CAP
+#define ARR_SPMM_CAP (ARR_SPMM_ASYNC ? 1024 : 2048)
+#endif
+constexpr int kNnzCap = ARR_SPMM_CAP;  // staged CSR entries per tile pass
 
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
@@ -530,7 +605,8 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     const int nthr = ((R * TX + 31) / 32) * 32;
     const int RT = c->tile_rows;  // rows per tile in natural order (<= kTile)
     // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
-    size_t smem = sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(RT + 2);
+    size_t smem = ((sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
+    if (ARR_SPMM_ASYNC && VEC == 2 && NV == 1 && K <= 7) smem += (size_t)kAsyncStages * (K + 1) * nthr * 16;
     const size_t red = 8 * (size_t)nthr * VEC;
     if (smem < red) smem = red;
     static int occ = -1;  // per instantiation (one device per process)

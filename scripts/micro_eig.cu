@@ -80,6 +80,37 @@ int main() {
         timeit("syevd (values only)", [&] {
             cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, m, A, m, W, work, lw, info);
         });
+        {
+            cusolverDnParams_t prm;
+            cusolverDnCreateParams(&prm);
+            size_t dws = 0, hws = 0;
+            cusolverStatus_t bs = cusolverDnXsyevBatched_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                                                CUDA_R_64F, A, m, CUDA_R_64F, W, CUDA_R_64F, &dws, &hws, 1);
+            if (bs == CUSOLVER_STATUS_SUCCESS) {
+                void *dw = nullptr;
+                cudaMalloc(&dw, dws > 0 ? dws : 16);
+                std::vector<char> hw(hws > 0 ? hws : 16);
+                timeit("XsyevBatched (batch 1)", [&] {
+                    cusolverDnXsyevBatched(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F, A, m,
+                                           CUDA_R_64F, W, CUDA_R_64F, dw, dws, hw.data(), hws, info, 1);
+                });
+                cudaFree(dw);
+            } else {
+                printf("m=%5d XsyevBatched bufferSize status %d\n", m, (int)bs);
+            }
+            size_t dws2 = 0, hws2 = 0;
+            cusolverDnXsyevd_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F, A, m,
+                                        CUDA_R_64F, W, CUDA_R_64F, &dws2, &hws2);
+            void *dw2 = nullptr;
+            cudaMalloc(&dw2, dws2 > 0 ? dws2 : 16);
+            std::vector<char> hw2(hws2 > 0 ? hws2 : 16);
+            timeit("Xsyevd (64-bit API)", [&] {
+                cusolverDnXsyevd(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F, A, m, CUDA_R_64F,
+                                 W, CUDA_R_64F, dw2, dws2, hw2.data(), hws2, info);
+            });
+            cudaFree(dw2);
+            cusolverDnDestroyParams(prm);
+        }
         cusolverDnDestroySyevjInfo(jp);
         cudaFree(A); cudaFree(A0); cudaFree(W); cudaFree(work); cudaFree(info);
     }
