@@ -168,8 +168,8 @@ arr_status colnorm_x(arr_ctx *c, const double *partials, int nblk, int w, double
 arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
     const double cc = 0.5 * (c->a + c->b), e = 0.5 * (c->b - c->a);
     const int w = c->w;
-    double *T = c->T;
-    const int64_t lt = ldT(c);
+    double *T = c->T ? c->T : c->Q;  // lean context: the basis block Q[:, 0:w] is free during sweeps
+    const int64_t lt = c->T ? ldT(c) : ldQ(c);
     double *cur = X;
     int64_t ldcur = ldx;
     double *other = T;
@@ -252,16 +252,17 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
     return ARR_OK;
 }
 
-// Shifted CholeskyQR3 In -> Out (In != Out) through the scratch T; *ok = 0 if
-// a factorisation failed (numerically rank-deficient input after the shift):
-// the caller then falls back to SVQB.  Synchronises the stream.
+// Shifted CholeskyQR3 In -> Out (In != Out) through the scratch block S (may be
+// In itself: In is only read by the first pass); *ok = 0 if a factorisation
+// failed (numerically rank-deficient input after the shift): the caller then
+// falls back to SVQB.  Synchronises the stream.
 arr_status cholqr3(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols, int *rank_slot,
-                   bool *ok) {
+                   bool *ok, double *S, int64_t lds) {
     arr_status st;
     int *inf = c->dinfo + INFO_CHOL;
     CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(int) * 6, c->stream));
     if ((st = cholqr_pass(c, In, ldin, Out, ldout, ncols, true, inf, rank_slot)) != ARR_OK) return st;
-    if ((st = cholqr_pass(c, Out, ldout, c->T, ldT(c), ncols, false, inf + 2, nullptr)) != ARR_OK) return st;
+    if ((st = cholqr_pass(c, Out, ldout, S, lds, ncols, false, inf + 2, nullptr)) != ARR_OK) return st;
     // The second pass's factor R2 measures how far pass 1 was from orthonormal:
     // pass 2's output is orthonormal to O(u cond(R2)^2).  If R2^{-1} (left in V
     // by trtri) is within 1e-6 of I entrywise, the third pass is skipped.
@@ -274,23 +275,23 @@ arr_status cholqr3(arr_ctx *c, const double *In, int64_t ldin, double *Out, int6
     const double dev = c->h_stage[0];
     if (!*ok) return ARR_OK;
     if (!(dev <= 1e-6)) {
-        if ((st = cholqr_pass(c, c->T, ldT(c), Out, ldout, ncols, false, inf + 4, nullptr)) != ARR_OK) return st;
+        if ((st = cholqr_pass(c, S, lds, Out, ldout, ncols, false, inf + 4, nullptr)) != ARR_OK) return st;
         CUDA_TRY(cudaMemcpyAsync(c->h_istage + 44, inf + 4, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         *ok = c->h_istage[44] == 0 && c->h_istage[45] == 0;
     } else {
-        launch_copy_rows(c, c->T, ldT(c), Out, ldout, c->A.n, ncols);
+        launch_copy_rows(c, S, lds, Out, ldout, c->A.n, ncols);
         CHECK_LAUNCH();
     }
     return ARR_OK;
 }
 
-// Two SVQB passes In -> Out through the scratch T (In may equal Out).
+// Two SVQB passes In -> Out through the scratch block S (S != In, S != Out).
 arr_status svqb2(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
-                 int *rank_slot) {
+                 int *rank_slot, double *S, int64_t lds) {
     arr_status st;
-    if ((st = svqb_pass(c, In, ldin, c->T, ldT(c), ncols, rank_slot)) != ARR_OK) return st;
-    if ((st = svqb_pass(c, c->T, ldT(c), Out, ldout, ncols, nullptr)) != ARR_OK) return st;
+    if ((st = svqb_pass(c, In, ldin, S, lds, ncols, rank_slot)) != ARR_OK) return st;
+    if ((st = svqb_pass(c, S, lds, Out, ldout, ncols, nullptr)) != ARR_OK) return st;
     return ARR_OK;
 }
 
@@ -298,15 +299,26 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
                     double *ritz_host, int32_t *rank) {
     const int w = c->w;
     const int m = m_of(c, p_use);
-    const int64_t lq = ldQ(c), lt = ldT(c);
-    double *Q = c->Q, *T = c->T;
+    const int64_t lq = ldQ(c);
+    double *Q = c->Q;
+    // scratch blocks: the context's T; without one (lean context) the spare block
+    // Q[:, w:2w] while U_0 is built, then the output block Y (== X) once X is consumed
+    double *S0 = c->T, *T = c->T;
+    int64_t ls0 = ldT(c), lt = ldT(c);
+    if (!c->T) {
+        S0 = Q + w;
+        ls0 = lq;
+        T = (p_use == 0) ? S0 : Y;
+        lt = (p_use == 0) ? lq : ldy;
+    }
     arr_status st;
     const int ev0 = t_mark(c);
     int evs = ev0;
     // U_0 = orth(X): Alg. RR step 1 on the first block
     bool ok = false;
-    if (c->orth_mode == 0 && (st = cholqr3(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0, &ok)) != ARR_OK) return st;
-    if (!ok && (st = svqb2(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
+    if (c->orth_mode == 0 && (st = cholqr3(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0, &ok, S0, ls0)) != ARR_OK)
+        return st;
+    if (!ok && (st = svqb2(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0, S0, ls0)) != ARR_OK) return st;
     // U_j = orth((I - Q Q^T) A U_{j-1}): the block-Krylov augmentation of Eq. S:ARR
     for (int j = 1; j <= p_use; ++j) {
         const int jw = j * w;
@@ -324,6 +336,10 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
             if (g < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
             for (int pass = 0; pass < 2; ++pass) {
                 ST_TRY(gram_x(c, Q, lq, jw, T, lt, w, G_buf(c), w));
+                // The first pass's coefficients Q[:, :jw]^T (A U_{j-1}) ARE rows [0, jw) of
+                // block column j-1 of H = Q^T A Q (same SpMM output, same Gram kernel on the
+                // same operands: bitwise what the H loop would compute), so H keeps them.
+                if (pass == 0 && !is_dist(c)) launch_copy_rows(c, G_buf(c), w, H_buf(c) + (int64_t)(j - 1) * w, m, jw, w);
                 launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
             }
             CHECK_LAUNCH();
@@ -331,7 +347,8 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         };
         if ((st = make_W()) != ARR_OK) return st;
         ok = false;
-        if (c->orth_mode == 0 && (st = cholqr3(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j, &ok)) != ARR_OK)
+        if (c->orth_mode == 0 &&
+            (st = cholqr3(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j, &ok, T, lt)) != ARR_OK)
             return st;
         if (!ok) {
             if (c->orth_mode == 0 && (st = make_W()) != ARR_OK) return st;  // T was reused by CholeskyQR3
@@ -343,7 +360,8 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
     { const int e = t_mark(c); t_add(c, 3, evs, e, 1); evs = e; }
     // H = Q^T (A Q), one w-column block of AQ at a time (AQ never stored whole)
     double *H = H_buf(c);
-    for (int j = 0; j <= p_use; ++j) {
+    // block columns 0..p_use-1 came from the CGS passes (one GPU); multi-GPU recomputes them
+    for (int j = is_dist(c) ? 0 : p_use; j <= p_use; ++j) {
         SpmmArgs s{};
         s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
         s.n = c->A.n; s.w = w;
@@ -459,8 +477,14 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     const int64_t mm = std::max<int64_t>(m, ARR_MAX_W);
     c->part_elems = (size_t)std::max<int64_t>(16 * m * w, 4096 * mm);
     struct Alloc { void **p; size_t bytes; };
+    // Lean context (no scratch block T; Section "Memory" of DESIGN.md): when T and
+    // the basis do not fit next to the caller's blocks, or on request (ARRABIT_LEAN)
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t need = sizeof(double) * (size_t)n * (size_t)(lt + lq) + ((size_t)1 << 30);
+    const bool lean = p >= 1 && (getenv("ARRABIT_LEAN") != nullptr || need > free_b);
     std::vector<Alloc> al = {
-        {(void **)&c->T, sizeof(double) * (size_t)n * lt},
+        {(void **)&c->T, lean ? 0 : sizeof(double) * (size_t)n * lt},
         {(void **)&c->Q, sizeof(double) * (size_t)n * lq},
         {(void **)&c->part, sizeof(double) * c->part_elems},
         {(void **)&c->small, sizeof(double) * 4 * (size_t)m * m},
@@ -471,6 +495,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     };
     size_t total = 0;
     for (auto &x : al) {
+        if (x.bytes == 0) { *x.p = nullptr; continue; }
         if (cudaMalloc(x.p, x.bytes) != cudaSuccess) {
             cudaGetLastError();
             eig_destroy(c);
@@ -607,7 +632,7 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
         return ARR_OK;
     }
     if (!tile_len || ntiles < 1) return fail(c, ARR_EINVAL, "schedule: null lengths or no tiles");
-    int *marks = reinterpret_cast<int *>(c->T);  // scratch block holds >= n ints
+    int *marks = reinterpret_cast<int *>(c->T ? c->T : c->Q);  // a scratch block holds >= n ints
     launch_schedule_check(c, tile_row0, tile_len, ntiles, marks, c->dinfo + INFO_BAD);
     CHECK_LAUNCH();
     CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -702,9 +727,12 @@ arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int
     launch_copy_rows(c, X, ldx, c->Q, ldQ(c), c->A.n, ncols);
     bool ok = false;
     arr_status st;
-    if (c->orth_mode == 0 && (st = cholqr3(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0, &ok)) != ARR_OK)
+    double *S = c->T ? c->T : c->Q + c->w;  // lean: the spare basis block (p >= 1)
+    const int64_t ls = c->T ? ldT(c) : ldQ(c);
+    if (c->orth_mode == 0 &&
+        (st = cholqr3(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0, &ok, S, ls)) != ARR_OK)
         return st;
-    if (!ok && (st = svqb2(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0)) != ARR_OK) return st;
+    if (!ok && (st = svqb2(c, c->Q, ldQ(c), X, ldx, ncols, c->dinfo + INFO_RANK0, S, ls)) != ARR_OK) return st;
     CUDA_TRY(cudaMemcpyAsync(c->h_istage, c->dinfo, sizeof(int) * (INFO_RANK0 + 1), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->h_istage[INFO_SYEVD] != 0) return fail(c, ARR_ECUSOLVER, "syevd failed");
@@ -718,6 +746,8 @@ arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx
     if (p_use < 0 || p_use > c->p) return fail(c, ARR_EINVAL, "p_use out of range");
     if (!block_ok(X, ldx, c->w) || (Y && !block_ok(Y, ldy, c->w)) || !ritz_host)
         return fail(c, ARR_EINVAL, "bad arr_project args");
+    if (!c->T && p_use > 0 && (Y != X || ldy != ldx))
+        return fail(c, ARR_EINVAL, "lean context (no scratch block): arr_project with p > 0 needs Y == X");
     return arr_core(c, p_use, X, ldx, Y, ldy, ritz_host, rank);
 }
 

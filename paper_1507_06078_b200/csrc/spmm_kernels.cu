@@ -31,6 +31,15 @@ namespace {
 #ifndef ARR_SPMM_ASYNC
 #define ARR_SPMM_ASYNC 0  // 1: rows of <= 7 entries gathered by per-thread cp.async into shared-memory slots, one row ahead
 #endif
+#ifndef ARR_SPMM_WS
+#define ARR_SPMM_WS 1  // warp-specialised kernel: a producer warp stages the CSR of the next tile (2-stage ring)
+#endif
+#ifndef ARR_SPMM_FLAT
+#define ARR_SPMM_FLAT 0  // 1: row-cyclic "flat" kernel (no tiles; every thread a fixed column vector) in natural order
+#endif
+#ifndef ARR_SPMM_FLAT_U
+#define ARR_SPMM_FLAT_U 2  // rows in flight per thread in the flat kernel
+#endif
 #ifndef ARR_SPMM_SEQ
 #define ARR_SPMM_SEQ 0  // 1: each row slot walks a contiguous run of the tile's rows (L1 reuse of x-neighbours)
 #endif
@@ -598,9 +607,239 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
 #define ARR_SPMM_CAP (ARR_SPMM_ASYNC ? 1024 : 2048)
 #endif
 constexpr int kNnzCap = ARR_SPMM_CAP;  // staged CSR entries per tile pass
+#ifndef ARR_SPMM_WS_CAP
+#define ARR_SPMM_WS_CAP 1792
+#endif
+constexpr int kWsCap = ARR_SPMM_WS_CAP;  // entries per stage of the warp-specialised kernel (2 stages)
+
+// ---------------------------------------------------------------- warp-specialised tiles
+// Named barriers (bar.sync / bar.arrive with a thread count): FULL[s] (ids 1,2)
+// and EMPTY[s] (ids 3,4) of the two shared-memory stages.
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct WsInfo {
+    int64_t r0;  // first row (-1: no more work)
+    int nrows;   // rows of this item
+    int mode;    // 0: staged slice, 1: one row longer than the stage (read from global memory)
+};
+
+// Same arithmetic and per-row CSR order as spmm_tile_kernel.  The last warp is a
+// producer: it takes this CTA's tiles in order (atomic ticket, or the static
+// grid-stride order for launches that reduce column norms), splits a tile whose
+// slice exceeds the stage capacity into row ranges that fit, and stages each
+// range's row pointers and {col*ld, val} entries into one of two shared-memory
+// stages while the consumer warps compute the other: the CSR round trips of the
+// next tile are hidden behind the current one.
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+__global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
+                                                                      int64_t ntiles, int nnz_cap, int ncons) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const size_t stage_bytes = ((sizeof(Ent) * (size_t)nnz_cap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
+    __shared__ WsInfo s_info[2];
+    const int tid = threadIdx.x;
+    const int nall = ncons + 32;
+    const bool producer = tid >= ncons;
+    const int64_t *__restrict__ rp = a.row_ptr;
+    const int64_t ld = a.ld_in;
+    if (producer) {
+        const int lane = tid - ncons;
+        int st = 0, k = 0;
+        // Stage rows [r0, r0 + nrows) (their CSR slice fits) into stage st: the row
+        // pointers were already loaded by the lanes (rpv[h] = rp[r0 + lane + 32h] - base).
+        auto wait_stage = [&]() {
+            if (k >= 2) nb_sync(3 + st, nall);  // consumers released this stage
+        };
+        auto release = [&](int64_t r0, int nrows, int mode) {
+            if (lane == 0) s_info[st] = WsInfo{r0, nrows, mode};
+            __syncwarp();
+            nb_arrive(1 + st, nall);
+            st ^= 1;
+            ++k;
+        };
+        constexpr bool DYN = !SUMSQ;
+        constexpr int UN = 8;  // entries in flight per lane
+        for (int64_t t = blockIdx.x; t < ntiles;) {
+            int64_t r0;
+            int nrows;
+            if (a.tile_row0) { r0 = __ldg(a.tile_row0 + t); nrows = __ldg(a.tile_len + t); }
+            else { r0 = t * RT; nrows = (int)min((int64_t)RT, a.n - r0); }
+            int done = 0;
+            while (done < nrows) {
+                const int left = nrows - done;  // <= kTile = 64
+                const int64_t base = __ldg(rp + r0 + done);
+                // rp of rows done+1 .. done+left, two per lane, loaded together
+                int64_t e0 = lane + 1 <= left ? __ldg(rp + r0 + done + lane + 1) - base : INT64_MAX;
+                int64_t e1 = lane + 33 <= left ? __ldg(rp + r0 + done + lane + 33) - base : INT64_MAX;
+                const unsigned m0 = __ballot_sync(0xffffffffu, e0 <= nnz_cap);
+                const unsigned m1 = __ballot_sync(0xffffffffu, e1 <= nnz_cap);
+                const int cnt = __popc(m0) + (m0 == 0xffffffffu ? __popc(m1) : 0);  // rp nondecreasing
+                wait_stage();
+                Ent *s_ent = reinterpret_cast<Ent *>(smem_raw + st * stage_bytes);
+                int *s_rp = reinterpret_cast<int *>(smem_raw + st * stage_bytes + sizeof(Ent) * nnz_cap);
+                if (cnt == 0) {  // one row longer than a stage
+                    release(r0 + done, 1, 1);
+                    done += 1;
+                    continue;
+                }
+                if (lane == 0) s_rp[0] = 0;
+                if (lane + 1 <= cnt) s_rp[lane + 1] = (int)e0;
+                if (lane + 33 <= cnt) s_rp[lane + 33] = (int)e1;
+                const int64_t nnz_t = __shfl_sync(0xffffffffu, cnt <= 32 ? e0 : e1, (cnt <= 32 ? cnt : cnt - 32) - 1);
+                for (int64_t q0 = 0; q0 < nnz_t; q0 += 32 * UN) {
+                    int32_t cv[UN];
+                    double vv[UN];
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) {
+                        const int64_t q = q0 + u * 32 + lane;
+                        cv[u] = q < nnz_t ? __ldg(a.col + base + q) : 0;
+                        vv[u] = q < nnz_t ? __ldg(a.val + base + q) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) {
+                        const int64_t q = q0 + u * 32 + lane;
+                        if (q < nnz_t) {
+                            Ent e;
+                            e.off = (int64_t)cv[u] * ld;
+                            e.val = vv[u];
+                            s_ent[q] = e;
+                        }
+                    }
+                }
+                release(r0 + done, cnt, 0);
+                done += cnt;
+            }
+            if (DYN) {
+                int64_t nx = 0;
+                if (lane == 0) nx = (int64_t)gridDim.x + (int64_t)atomicAdd(a.sched, 1ull);
+                t = __shfl_sync(0xffffffffu, nx, 0);
+            } else {
+                t += gridDim.x;
+            }
+        }
+        wait_stage();
+        release(-1, 0, 0);
+        if (DYN && lane == 0) {
+            __threadfence();
+            if (atomicAdd(a.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+                a.sched[0] = 0;
+                a.sched[1] = 0;
+                __threadfence();
+            }
+        }
+    } else {
+        const int r = tid / TX;
+        const int v0 = tid - r * TX;
+        const bool active = r < R;
+        double ss[NV][VEC];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) ss[v][e] = 0.0;
+        const uint64_t pol_keep = policy_evict_last();
+        const uint64_t pol_stream = policy_evict_first();
+        int st = 0;
+        for (;;) {
+            nb_sync(1 + st, nall);
+            const WsInfo info = s_info[st];
+            if (info.r0 < 0) break;
+            const Ent *s_ent = reinterpret_cast<const Ent *>(smem_raw + st * stage_bytes);
+            const int *s_rp = reinterpret_cast<const int *>(smem_raw + st * stage_bytes + sizeof(Ent) * nnz_cap);
+            if (info.mode == 0) {
+                if (active)
+                    tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, info.r0, info.nrows, R, 0, r, TX, v0, wv,
+                                                                            s_rp, s_ent, ss, pol_keep, pol_stream,
+                                                                            nullptr);
+            } else if (active && r == 0) {
+                // one row longer than a stage: CSR order straight from global memory
+                using Vv = Vec<VEC>;
+                using T = typename Vv::T;
+                const int64_t i = info.r0;
+                const int64_t p0 = __ldg(rp + i), p1 = __ldg(rp + i + 1);
+                for (int v = 0; v < NV; ++v) {
+                    const int vv = v0 + v * TX;
+                    if (vv >= wv) continue;
+                    T acc = Vv::zero();
+                    for (int64_t p = p0; p < p1; ++p)
+                        fma_vec<VEC>(acc, __ldg(a.val + p), Vv::ldg(a.Yin + (int64_t)__ldg(a.col + p) * ld + vv * VEC));
+                    const T yi = Vv::ldg(a.Yin + i * ld + vv * VEC);
+                    T yp = Vv::zero();
+                    if (HAS_PREV) yp = Vv::ldcs(a.Yprev + i * a.ld_prev + vv * VEC);
+                    T out;
+                    for (int e = 0; e < VEC; ++e) {
+                        const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
+                        double o = a.alpha * (Vv::get(acc, e) - sh * Vv::get(yi, e));
+                        if (HAS_PREV) o += a.beta * Vv::get(yp, e);
+                        Vv::set(out, e, o);
+                        if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
+                    }
+                    if (STORE) Vv::stcs(a.Yout + i * a.ld_out + vv * VEC, out);
+                }
+            }
+            nb_arrive(3 + st, nall);
+            st ^= 1;
+        }
+        if (SUMSQ) {
+            // fixed-order reduction over the R row slots of each column (consumer threads only)
+            double *red = reinterpret_cast<double *>(smem_raw);
+            nb_sync(5, ncons);  // every consumer is past the last stage (the producer has exited the ring)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if (active) {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) red[(r * TX + v0) * VEC + e] = ss[v][e];
+                }
+                nb_sync(5, ncons);
+                const int vv = v0 + v * TX;
+                if (active && r == 0 && vv < wv) {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) {
+                        double sum = 0.0;
+                        for (int q = 0; q < R; ++q) sum += red[(q * TX + v0) * VEC + e];
+                        const int colid = vv * VEC + e;
+                        if (colid < a.w) a.partials[(int64_t)blockIdx.x * a.w + colid] = sum;
+                    }
+                }
+                nb_sync(5, ncons);
+            }
+        }
+    }
+}
 
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
+#if ARR_SPMM_WS
+    // warp-specialised kernel where it measured faster on B200: >= 4 rows in flight per
+    // CTA and single-chunk rows (cfg2: 116 -> 105 us); slower for R = 1 (cfg3, w = 550) and
+    // for 27-point rows (cfg5), which keep spmm_tile_kernel
+    if (R >= 4 && K <= 7) {
+        auto kern = spmm_ws_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
+        const int ncons = ((R * TX + 31) / 32) * 32;
+        const int RT = c->tile_rows;
+        const size_t stage = ((sizeof(Ent) * (size_t)kWsCap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
+        size_t smem = 2 * stage;
+        const size_t red = 8 * (size_t)ncons * VEC;
+        if (smem < red) smem = red;
+        static int occ = -1;
+        static size_t occ_smem = 0;
+        if (occ < 0 || occ_smem != smem) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int o = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, ncons + 32, smem);
+            occ = o > 0 ? o : 1;
+            occ_smem = smem;
+        }
+        const int64_t ntiles = a.tile_row0 ? a.ntiles : (a.n + RT - 1) / RT;
+        int64_t G = (int64_t)c->num_sms * occ;
+        if (G > ntiles) G = ntiles;
+        if (G < 1) G = 1;
+        kern<<<(unsigned)G, ncons + 32, smem, c->stream>>>(a, TX, R, RT, wv, ntiles, kWsCap, ncons);
+        c->launches++;
+        return (int)G;
+    }
+#endif
     auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
     const int nthr = ((R * TX + 31) / 32) * 32;
     const int RT = c->tile_rows;  // rows per tile in natural order (<= kTile)
@@ -658,6 +897,153 @@ int dispatch_nv(arr_ctx *c, const SpmmArgs &a) {
     }
     if (nv == 2) return dispatch_flags<VEC, 2, 4>(c, a, TX, R, wv);
     if (nv <= 4) return dispatch_flags<VEC, 4, 2>(c, a, TX, R, wv);
+    return -1;
+}
+
+
+// Row-cyclic fused SpMM ("flat"): the grid's T threads are cut into RS = T / wv
+// row slots of wv threads; thread g owns column vector v = g % wv of rows
+// g / wv, g / wv + RS, ... (U rows in flight), so at any moment the whole GPU
+// streams one contiguous window of ~U*RS rows, like a copy.  The CSR of a row
+// is read straight from global memory (broadcast within the row's threads, L1
+// hits across them).  Per-row sums in CSR order, same arithmetic as the tiled
+// kernel.  Column sums of squares: fixed thread -> (column, rows) assignment,
+// so the per-CTA partials are deterministic.
+template <int VEC, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+__global__ void __launch_bounds__(512, 2) spmm_flat_kernel(SpmmArgs a, int wv, int64_t RS) {
+    using V = Vec<VEC>;
+    using T = typename V::T;
+    constexpr int U = ARR_SPMM_FLAT_U;
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t slot = g / wv;
+    const int v = (int)(g - slot * wv);
+    const bool act = slot < RS;
+    double ss[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ss[e] = 0.0;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    const double *yin_v = a.Yin + v * VEC;
+    if (act) {
+        for (int64_t i0 = slot; i0 < a.n; i0 += (int64_t)U * RS) {
+            int64_t p0[U], p1[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * RS;
+                p0[u] = i < a.n ? __ldg(a.row_ptr + i) : 0;
+                p1[u] = i < a.n ? __ldg(a.row_ptr + i + 1) : 0;
+            }
+            T yp[U];
+            if (HAS_PREV) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t i = i0 + u * RS;
+                    yp[u] = i < a.n ? STREAM_LD(a.Yprev + i * a.ld_prev + v * VEC) : V::zero();
+                }
+            }
+            T acc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = V::zero();
+            // chunks of K entries (one chunk for stencil rows)
+            int64_t q[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) q[u] = p0[u];
+            bool more = true;
+            while (more) {
+                int64_t off[U][K];
+                double av[U][K];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const bool ok = q[u] + k < p1[u];
+                        const int64_t idx = ok ? q[u] + k : (p0[u] < p1[u] ? p0[u] : 0);
+                        off[u][k] = (int64_t)__ldg(a.col + idx) * a.ld_in;
+                        av[u][k] = ok ? __ldg(a.val + idx) : 0.0;
+                    }
+                T x[U][K];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) x[u][k] = GATHER(yin_v + off[u][k]);
+                more = false;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) fma_vec<VEC>(acc[u], av[u][k], x[u][k]);
+                    q[u] += K;
+                    more = more || (q[u] < p1[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + u * RS;
+                if (i >= a.n) continue;
+                const T yi = V::ldg(a.Yin + i * a.ld_in + v * VEC);
+                T out;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    const double sh = COLSHIFT ? __ldg(a.colshift + v * VEC + e) : a.shift;
+                    double o = a.alpha * (V::get(acc[u], e) - sh * V::get(yi, e));
+                    if (HAS_PREV) o += a.beta * V::get(yp[u], e);
+                    V::set(out, e, o);
+                    if (SUMSQ) ss[e] = fma(o, o, ss[e]);
+                }
+                if (STORE) STREAM_ST(a.Yout + i * a.ld_out + v * VEC, out);
+            }
+        }
+    }
+    if (SUMSQ) {
+        // per CTA: sum over its threads of the same column, fixed order (thread order)
+        extern __shared__ double red_f[];
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) red_f[tid * VEC + e] = act ? ss[e] : 0.0;
+        __syncthreads();
+        // columns present in this CTA: threads g in [g0, g0+B); thread with lowest g per column sums
+        const int64_t g0 = blockIdx.x * (int64_t)blockDim.x;
+        for (int cv = tid; cv < wv; cv += blockDim.x) {
+            double sum[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
+            // first local thread index with column cv
+            int64_t first = cv - (g0 % wv);
+            if (first < 0) first += wv;
+            for (int64_t t = first; t < blockDim.x; t += wv)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) sum[e] += red_f[t * VEC + e];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const int colid = cv * VEC + e;
+                if (colid < a.w) a.partials[(int64_t)blockIdx.x * a.w + colid] = sum[e];
+            }
+        }
+    }
+}
+
+template <int VEC, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+int launch_flat(arr_ctx *c, const SpmmArgs &a, int wv) {
+    auto kern = spmm_flat_kernel<VEC, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
+    const int B = 512;
+    int64_t G = (int64_t)c->num_sms * 2;
+    int64_t RS = G * B / wv;
+    if (RS > a.n) { RS = a.n; G = (RS * wv + B - 1) / B; }
+    const size_t smem = SUMSQ ? sizeof(double) * B * VEC : 0;
+    kern<<<(unsigned)G, B, smem, c->stream>>>(a, wv, RS);
+    c->launches++;
+    return (int)G;
+}
+
+template <int VEC, int K>
+int dispatch_flat(arr_ctx *c, const SpmmArgs &a) {
+    const int wv = (a.w + VEC - 1) / VEC;
+    const bool prev = a.Yprev != nullptr, store = a.Yout != nullptr, ss = a.partials != nullptr,
+               cs = a.colshift != nullptr;
+    if (prev && store && !ss && !cs) return launch_flat<VEC, K, true, true, false, false>(c, a, wv);
+    if (prev && store && ss && !cs) return launch_flat<VEC, K, true, true, true, false>(c, a, wv);
+    if (!prev && store && !ss && !cs) return launch_flat<VEC, K, false, true, false, false>(c, a, wv);
+    if (!prev && store && ss && !cs) return launch_flat<VEC, K, false, true, true, false>(c, a, wv);
+    if (!prev && !store && ss && cs) return launch_flat<VEC, K, false, false, true, true>(c, a, wv);
     return -1;
 }
 
@@ -790,6 +1176,15 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     if (a.Yprev) v2 = v2 && vec2_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
     c->spmm_blocks++;
+#if ARR_SPMM_FLAT
+    if (!a.tile_row0 && v2 && a.w <= 2 * 512 * 148) {
+        const int L = c->max_row_nnz;
+        if (L <= 3) return dispatch_flat<2, 3>(c, a);
+        if (L <= 5) return dispatch_flat<2, 5>(c, a);
+        if (L <= 7) return dispatch_flat<2, 7>(c, a);
+        return dispatch_flat<2, 9>(c, a);
+    }
+#endif
 #if ARR_SPMM_V4
     bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
     if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);

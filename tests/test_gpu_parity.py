@@ -316,3 +316,29 @@ def test_solve_host_entry(arr):
     assert info.converged == 1
     cert = oracle.residuals(A, evec, ev)
     assert np.all(cert <= 1.01 * spec.tol)
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "st27"])
+def test_lean_context_is_bitwise_identical(arr, kind, monkeypatch):
+    """A context without the scratch block (lean: the spare basis block and the
+    output block serve as scratch, DESIGN.md §5 Memory) computes exactly the
+    same solve: only buffer locations change, never the arithmetic."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    out = []
+    for lean in (False, True):
+        if lean:
+            monkeypatch.setenv("ARRABIT_LEAN", "1")
+        ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+        Xd = dev_block(X0)
+        ev, res, info = ctx.eig_solve(Xd, tol=spec.tol)
+        out.append((ev, res, info.outer, host(Xd)))
+        if lean:
+            Y = torch.empty_like(Xd)
+            with pytest.raises(arr.ArrError):
+                ctx.arr_project(Xd, Y)  # lean: the Ritz vectors must overwrite X
+        ctx.close()
+    assert out[0][2] == out[1][2]
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][3], out[1][3])
