@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -16,6 +17,55 @@
 #include "internal.cuh"
 
 namespace {
+
+// Process-wide pool of cuSOLVER handles (creating one costs tens of ms; the
+// host-buffer entry creates a context per call).  A handle is bound to the
+// device current at creation: pooled per device.
+std::mutex g_pool_mu;
+std::vector<std::pair<int, cusolverDnHandle_t>> g_solver_pool;
+
+cusolverStatus_t solver_acquire(cusolverDnHandle_t *h) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_solver_pool.size(); ++i)
+            if (g_solver_pool[i].first == dev) {
+                *h = g_solver_pool[i].second;
+                g_solver_pool.erase(g_solver_pool.begin() + i);
+                return CUSOLVER_STATUS_SUCCESS;
+            }
+    }
+    return cusolverDnCreate(h);
+}
+
+void solver_release(cusolverDnHandle_t h) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_solver_pool.size() < 16) g_solver_pool.push_back({dev, h});
+    else cusolverDnDestroy(h);
+}
+
+// Device memory of contexts and of the host-buffer entry: stream-ordered
+// allocations from the device's default pool, which keeps up to 4 GiB between
+// calls (repeated eig_solve_host calls reuse it instead of cudaMalloc/cudaFree).
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t s) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = (uint64_t)4 << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    return cudaMallocAsync(p, bytes, s);
+}
+void dev_free(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
 
 constexpr double kSvqbTau = 1e-14;  // eigenvalue floor of the SVQB Gram (relative)
 enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2, INFO_CHOL = 40 };  // dinfo slots (INFO_RANK0.. per block;
@@ -496,7 +546,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     size_t total = 0;
     for (auto &x : al) {
         if (x.bytes == 0) { *x.p = nullptr; continue; }
-        if (cudaMalloc(x.p, x.bytes) != cudaSuccess) {
+        if (dev_alloc(x.p, x.bytes, c->stream) != cudaSuccess) {
             cudaGetLastError();
             eig_destroy(c);
             return ARR_ENOMEM;
@@ -505,7 +555,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     }
     cudaMemsetAsync(c->dinfo, 0, sizeof(int) * 64, c->stream);
     cudaMemsetAsync(c->sched, 0, sizeof(unsigned long long) * 2, c->stream);
-    if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) { eig_destroy(c); return ARR_ECUSOLVER; }
+    if (solver_acquire(&c->solver) != CUSOLVER_STATUS_SUCCESS) { c->solver = nullptr; eig_destroy(c); return ARR_ECUSOLVER; }
     cusolverDnSetStream(c->solver, c->stream);
     int lwork = 0;
     if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)m, c->small,
@@ -527,7 +577,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     }
     c->trtri_dbytes = std::max<size_t>(tdb, 16);
     c->trtri_hwork.resize(std::max<size_t>(thb, 16));
-    if (cudaMalloc(&c->trtri_dwork, c->trtri_dbytes) != cudaSuccess) {
+    if (dev_alloc(&c->trtri_dwork, c->trtri_dbytes, c->stream) != cudaSuccess) {
         cudaGetLastError();
         eig_destroy(c);
         return ARR_ENOMEM;
@@ -535,7 +585,9 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     c->orth_mode = getenv("ARRABIT_ORTH_SVQB") ? 1 : 0;
     c->tile_rows = 64;
     if (const char *tr = getenv("ARRABIT_TILE")) c->tile_rows = std::min(64, std::max(1, atoi(tr)));
-    if (cudaMalloc(&c->solver_work, sizeof(double) * (size_t)c->solver_lwork) != cudaSuccess) {
+    c->col_split = 1;
+    if (const char *cs = getenv("ARRABIT_SPLIT")) c->col_split = std::min(4, std::max(1, atoi(cs)));
+    if (dev_alloc((void **)&c->solver_work, sizeof(double) * (size_t)c->solver_lwork, c->stream) != cudaSuccess) {
         cudaGetLastError();
         eig_destroy(c);
         return ARR_ENOMEM;
@@ -590,10 +642,11 @@ arr_status eig_destroy(arr_ctx *c) {
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
                     c->trtri_dwork};
     for (void *p : ptrs)
-        if (p) cudaFree(p);
+        dev_free(p, c->stream);
+    cudaStreamSynchronize(c->stream);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_istage) cudaFreeHost(c->h_istage);
-    if (c->solver) cusolverDnDestroy(c->solver);
+    if (c->solver) solver_release(c->solver);
     comm_free_plan(c);
     delete c;
     return ARR_OK;
@@ -833,12 +886,13 @@ arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const 
     const int64_t ldx = even_up(w);
     auto cleanup = [&]() {
         if (c) eig_destroy(c);
-        cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_val); cudaFree(d_X);
+        dev_free(d_rp, s); dev_free(d_ci, s); dev_free(d_val, s); dev_free(d_X, s);
+        cudaStreamSynchronize(s);
     };
-    if (cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
-        cudaMalloc(&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
-        cudaMalloc(&d_val, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
-        cudaMalloc(&d_X, sizeof(double) * n * ldx) != cudaSuccess) {
+    if (dev_alloc((void **)&d_rp, sizeof(int64_t) * (n + 1), s) != cudaSuccess ||
+        dev_alloc((void **)&d_ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1), s) != cudaSuccess ||
+        dev_alloc((void **)&d_val, sizeof(double) * std::max<int64_t>(nnz, 1), s) != cudaSuccess ||
+        dev_alloc((void **)&d_X, sizeof(double) * n * ldx, s) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
         return ARR_ENOMEM;

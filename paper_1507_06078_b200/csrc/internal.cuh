@@ -39,6 +39,7 @@ struct arr_ctx {
     int num_sms;
     int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
     int tile_rows;    // SpMM rows per tile in natural order (1..64; env ARRABIT_TILE)
+    int col_split;    // column vectors per SpMM thread (1 default; env ARRABIT_SPLIT, tuning)
     // interval
     double a, b;
     bool have_interval;

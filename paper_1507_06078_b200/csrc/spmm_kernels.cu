@@ -884,7 +884,8 @@ int dispatch_flags(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
 template <int VEC>
 int dispatch_nv(arr_ctx *c, const SpmmArgs &a) {
     const int wv = (a.w + VEC - 1) / VEC;
-    const int TX = wv < kMaxThreads ? wv : kMaxThreads;
+    int TX = wv < kMaxThreads ? wv : kMaxThreads;
+    if (c->col_split > 1 && wv / c->col_split >= 32) TX = (wv + c->col_split - 1) / c->col_split;  // NV > 1 per thread
     const int R = kMaxThreads / TX;
     const int nv = (wv + TX - 1) / TX;
     const int L = c->max_row_nnz;

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--filter-only", action="store_true")
     ap.add_argument("--size", type=int, default=None, help="override the generator size (grid edge or n)")
     ap.add_argument("--tiles", type=int, nargs="*", default=[0], help="ARRABIT_TILE values to try (0: default)")
+    ap.add_argument("--split", type=int, nargs="*", default=[1], help="ARRABIT_SPLIT values to try")
     ap.add_argument("--band", type=int, nargs="*", default=[0],
                     help="3-D y-band schedule heights to try in turn (0 natural, -1 auto)")
     args = ap.parse_args()
@@ -48,9 +49,10 @@ def main():
     from paper_1507_06078_b200 import schedule
     import itertools
     ctx = None
-    for tile, band in itertools.product(args.tiles, args.band):
+    for tile, band, split in itertools.product(args.tiles, args.band, args.split):
       if tile:
           os.environ["ARRABIT_TILE"] = str(tile)
+      os.environ["ARRABIT_SPLIT"] = str(split)
       if ctx is not None:
           ctx.close()
       ctx = arr.eig_init(Ad, k, spec.p if not args.filter_only else 0, spec.d)
@@ -61,10 +63,10 @@ def main():
             N = spec.size
             by = schedule.auto_band(N, N, k) if band < 0 else band
             ctx.eig_set_schedule(*schedule.yband_3d(N, N, N, by, tile or 64))
-            tag = f"tile={tile} y-band by={by}"
+            tag = f"tile={tile} split={split} y-band by={by}"
         else:
             ctx.eig_set_schedule(None)
-            tag = f"tile={tile} natural order"
+            tag = f"tile={tile} split={split} natural order"
         for _ in range(args.warmup):
             ctx.filter_step(X, normalize=True)
             if not args.filter_only:
