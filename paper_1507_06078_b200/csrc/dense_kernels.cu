@@ -260,11 +260,22 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 
 }  // namespace
 
-int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms) {
-    const int64_t tiles = (int64_t)((m1 + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE);
-    int64_t target = (int64_t)num_sms * 4;
-    int64_t ns = (target + tiles - 1) / tiles;
-    int64_t maxns = n / 512;  // at least 512 rows per split
+// Row splits of a Gram launch: as many as fill ONE wave of resident CTAs (a
+// partial second wave would idle most SMs for a whole CTA lifetime), at least 512
+// rows each.  sym: only the upper tiles do work.
+int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
+    const int64_t ta = (m1 + TILE - 1) / TILE, tb = (m2 + TILE - 1) / TILE;
+    const int64_t tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gram_kernel, THREADS, 0);
+        per_sm = o > 0 ? o : 1;
+    }
+    const int64_t slots = (int64_t)num_sms * per_sm;
+    int64_t ns = slots / tiles;
+    if (ns < 1) ns = (tiles > slots) ? 1 : 1;
+    const int64_t maxns = n / 512;
     if (ns > maxns) ns = maxns;
     if (ns < 1) ns = 1;
     if (ns > 64) ns = 64;
@@ -273,11 +284,11 @@ int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms) {
 
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
                  int32_t m2, int64_t n, double *G, int64_t ldg, double *partials) {
-    int ns = gram_nsplit(n, m1, m2, c->num_sms);
+    const bool sym = (X == Y) && (m1 == m2) && (ldx == ldy);
+    int ns = gram_nsplit(n, m1, m2, c->num_sms, sym);
     while ((size_t)ns * m1 * m2 > c->part_elems && ns > 1) --ns;
     int64_t rps = (n + ns - 1) / ns;
     rps = (rps + KS - 1) / KS * KS;
-    const bool sym = (X == Y) && (m1 == m2) && (ldx == ldy);
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
     gram_kernel<<<grid, THREADS, 0, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
     gram_reduce_kernel<<<nblk((int64_t)m1 * m2, 256), 256, 0, c->stream>>>(partials, ns, m1, m2, sym, G, ldg);
@@ -352,31 +363,31 @@ __global__ void diag_copy_kernel(const double *__restrict__ A_cm, int w, double 
 
 namespace {
 // out = max over the upper triangle of |M_ij - delta_ij| (M column-major w x w), one CTA
+// out = max_{i <= j} |M(i, j) - delta_ij| (M column-major, upper triangle); NaN wins.
+// One CTA per column; the CTA maxima are combined with an integer atomicMax on the
+// IEEE bits (order-preserving for non-negative doubles, NaN above +inf): the max is
+// order independent, so the result is deterministic.  *out must be zeroed first.
 __global__ void dev_from_identity_kernel(const double *__restrict__ M_cm, int w, double *out) {
+    const int j = blockIdx.x;
     double m = 0.0;
-    const int total = w * w;  // w <= ARR_MAX_W: fits int
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-        const int j = t / w, i = t - j * w;  // column-major: t = j*w + i
-        if (i > j) continue;
-        const double v = fabs(M_cm[t] - (i == j ? 1.0 : 0.0));
-        m = (v > m || v != v) ? v : m;  // NaN propagates
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+        const double v = fabs(M_cm[(int64_t)j * w + i] - (i == j ? 1.0 : 0.0));
+        m = (v > m || v != v) ? v : m;
     }
-    __shared__ double red[256];
-    red[threadIdx.x] = m;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            const double o = red[threadIdx.x + s];
-            if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = (v > m || v != v) ? v : m;
     }
-    if (threadIdx.x == 0) *out = red[0];
+    if ((threadIdx.x & 31) == 0) {
+        const double a = m != m ? __longlong_as_double(0x7ff8000000000000ll) : m;
+        atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(a));
+    }
 }
 }  // namespace
 
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out) {
-    dev_from_identity_kernel<<<1, 256, 0, c->stream>>>(M_cm, w, out);  // 32-bit index math: ~5 us at w = 220
+    cudaMemsetAsync(out, 0, sizeof(double), c->stream);
+    dev_from_identity_kernel<<<w, 64, 0, c->stream>>>(M_cm, w, out);
     c->launches++;
 }
 

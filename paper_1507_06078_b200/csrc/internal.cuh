@@ -142,7 +142,7 @@ arr_status comm_setup_plan(arr_ctx *c, const arr_dist *d, arr_comm *m);
 void comm_free_plan(arr_ctx *c);
 
 // ---------------------------------------------------------------- dense (DMMA)
-int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms);
+int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym);
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
                  int32_t m2, int64_t n, double *G, int64_t ldg, double *partials);
 // upper != 0: B is upper triangular (exact zeros below the diagonal are skipped)
