@@ -137,7 +137,7 @@ arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32
 /* Same with an explicit block width w >= k: w - k guard vectors (P:1291-1299,
  * "the number of columns in iterate matrix X to k+q"); (p+1)w < n.  Blocks
  * passed to filter_step / arr_project / eig_solve are then n x w; residuals and
- * the stop rule use the k leading pairs; b = mu_{w+1}. */
+ * the stop rule use the k leading pairs; b = mu_{w+1} (R3). */
 arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w, int32_t p, int32_t d, void *stream);
 /* Distributed context (collective over the ranks of comm): A_local is this
  * rank's local CSR (see arr_dist), k/w/p/d as eig_init_w with (p+1)w < n_global.
@@ -249,7 +249,7 @@ arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_
  * lines disabled; R3, R6, R10):
  *   a = Gershgorin lower bound; b = smallest Ritz value of RR(A, X0);
  *   repeat: s = sweeps rule; s x filter_step(normalize);  ARR;  residuals;
- *           stop if max res <= tol;  b = mu_{w+1};  X = leading Ritz vectors.
+ *           stop if max res <= tol;  b = mu_{w+1} (monotone once the residual grew, R3);  X = leading Ritz vectors.
  * X: in = X0 (n x w), out = the k Ritz vectors.  eigval_host/res_host: host [k].
  * Returns ARR_OK also when not converged (info->converged = 0). */
 arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts,

@@ -233,7 +233,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
         loop: s := sweeps_rule(mu_1);  s x { X := T_d((A-cI)/e) X; normalise }
               (mu, Y) := ARR(A, X, p)                                          (P:1502-1507)
               res_i, i <= k  (Eq. resi)  ;  stop if max res <= tol              (Eq. out-stop)
-              b := mu_{w+1};  X := Y[:, :w]
+              b := mu_{w+1} (monotone once maxres grew);  X := Y[:, :w]   (R3)
     """
     n = A.n
     w = X0.shape[1] if w is None else w  # w - k guard vectors (P:1291-1299)
@@ -250,6 +250,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     mu = mu0
     Y = X
     res = np.full(k, np.inf)
+    mono, prev_maxres = False, None
     for outer in range(1, limit + 1):
         s = sweeps_rule(mu1, a, b, d, s_max)
         for _ in range(s):
@@ -261,7 +262,13 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
         log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres))
         if maxres <= tol:
             return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log)
-        b = float(mu[min(w, r - 1)])
+        # b := mu_{w+1}, an under-estimate of lambda_{k+q} (mu_{w+1} <= lambda_{w+1} by
+        # interlacing); once the max residual has grown between two outer
+        # iterations (b fell and amplified the guard range), b only increases (R3)
+        mono = mono or (prev_maxres is not None and maxres > prev_maxres)
+        prev_maxres = maxres
+        bn = float(mu[min(w, r - 1)])
+        b = max(b, bn) if mono else bn
         if not a < b:
             a = b - 1e-8 * (abs(b) + 1.0)
         mu1 = float(mu[0])

@@ -835,7 +835,8 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
     double b = r0[w - 1], mu1 = r0[0];
     if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
     const int64_t spmm0 = c->spmm_blocks;
-    bool done = false;
+    bool done = false, mono = false;
+    double prev_maxres = 0.0;
     int32_t rank = 0;
     for (int outer = 1; outer <= opts->maxit; ++outer) {
         if ((st = eig_set_interval(c, a, b)) != ARR_OK) return st;
@@ -862,7 +863,12 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         inf.last_rank = rank;
         inf.a = a; inf.b = b;
         if (maxres <= opts->tol) { done = true; break; }  // Eq. out-stop
-        b = ritz[std::min(w, m - 1)];
+        // b = mu_{w+1}, an under-estimate of lambda_{k+q} (interlacing); once
+        // the max residual has grown between two outer iterations, b only increases (R3)
+        mono = mono || (outer > 1 && maxres > prev_maxres);
+        prev_maxres = maxres;
+        const double bn = ritz[std::min(w, m - 1)];
+        b = mono ? std::max(b, bn) : bn;
         mu1 = ritz[0];
         if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
     }

@@ -51,6 +51,7 @@ def main():
     if not a < b:
         a = b - 1e-8 * (abs(b) + 1)
     print(f"init: a={a:.6g} b={b:.6g} mu1={mu1:.6g} ({time.perf_counter() - t0:.1f} s)", flush=True)
+    mono, prev = False, 0.0
     for outer in range(1, args.maxit + 1):
         ctx.eig_set_interval(a, b)
         c, e = (a + b) / 2, (b - a) / 2
@@ -68,7 +69,10 @@ def main():
               f"mu1={ritz[0]:.10g} mu_k={ritz[k - 1]:.10g}  filter {t2 - t1:.2f} s, arr {t3 - t2:.2f} s", flush=True)
         if res.max() <= spec.tol:
             break
-        b, mu1 = ritz[min(w, len(ritz) - 1)], ritz[0]
+        mono = mono or (outer > 1 and res.max() > prev)
+        prev = res.max()
+        bn = ritz[min(w, len(ritz) - 1)]
+        b, mu1 = (max(b, bn) if mono else bn), ritz[0]
         if not a < b:
             a = b - 1e-8 * (abs(b) + 1)
 
