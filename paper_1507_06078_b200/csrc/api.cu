@@ -406,6 +406,32 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
             if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
             launch_copy_rows(c, T, lt, Qj, lq, c->A.n, w);
         }
+        // A nearly invariant Krylov block makes W numerically rank deficient; its
+        // orthonormalisation blows rounding errors up to unit columns that are no longer
+        // orthogonal to Q[:, :jw] (loss ~ u / sigma_min).  Check max |Q[:, :jw]^T U_j| and,
+        // above 1e-12, project U_j out of Q twice and re-orthonormalise (CholeskyQR2; U_j is
+        // then nearly orthonormal): H = Q^T A Q stays a true Rayleigh quotient (without it the
+        // cfg4 solve stalls at residuals ~1e-7).
+        ST_TRY(gram_x(c, Q, lq, jw, Qj, lq, w, G_buf(c), w));
+        launch_maxabs(c, G_buf(c), (int64_t)jw * w, c->evals);
+        CHECK_LAUNCH();
+        CUDA_TRY(cudaMemcpyAsync(c->h_stage, c->evals, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (!(c->h_stage[0] <= 1e-12)) {
+            for (int pass = 0; pass < 2; ++pass) {
+                if (pass > 0) ST_TRY(gram_x(c, Q, lq, jw, Qj, lq, w, G_buf(c), w));
+                launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, Qj, lq, Qj, lq, c->A.n);
+            }
+            int *inf = c->dinfo + INFO_CHOL;
+            CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(int) * 4, c->stream));
+            if ((st = cholqr_pass(c, Qj, lq, T, lt, w, false, inf, nullptr)) != ARR_OK) return st;
+            if ((st = cholqr_pass(c, T, lt, Qj, lq, w, false, inf + 2, nullptr)) != ARR_OK) return st;
+            CUDA_TRY(cudaMemcpyAsync(c->h_istage + 48, inf, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            for (int q = 0; q < 4; ++q)
+                if (c->h_istage[48 + q] != 0)
+                    return fail(c, ARR_ENUMERIC, "arr_project: re-orthonormalisation of an augmentation block failed");
+        }
     }
     { const int e = t_mark(c); t_add(c, 3, evs, e, 1); evs = e; }
     // H = Q^T (A Q), one w-column block of AQ at a time (AQ never stored whole)

@@ -385,6 +385,35 @@ __global__ void dev_from_identity_kernel(const double *__restrict__ M_cm, int w,
 }
 }  // namespace
 
+namespace {
+// out = max |x_i| over count elements (NaN wins); integer atomicMax on the IEEE bits
+// (order-preserving for non-negative doubles): deterministic.  *out zeroed first.
+__global__ void maxabs_kernel(const double *__restrict__ x, int64_t count, double *out) {
+    double m = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const double v = fabs(x[t]);
+        m = (v > m || v != v) ? v : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = (v > m || v != v) ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        const double a = m != m ? __longlong_as_double(0x7ff8000000000000ll) : m;
+        atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(a));
+    }
+}
+}  // namespace
+
+void launch_maxabs(arr_ctx *c, const double *x, int64_t count, double *out) {
+    cudaMemsetAsync(out, 0, sizeof(double), c->stream);
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > (int64_t)c->num_sms * 4) blocks = (int64_t)c->num_sms * 4;
+    if (blocks < 1) blocks = 1;
+    maxabs_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(x, count, out);
+    c->launches++;
+}
+
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out) {
     cudaMemsetAsync(out, 0, sizeof(double), c->stream);
     dev_from_identity_kernel<<<w, 64, 0, c->stream>>>(M_cm, w, out);

@@ -164,3 +164,4 @@ void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32
 void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d);
 
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out);
+void launch_maxabs(arr_ctx *c, const double *x, int64_t count, double *out);

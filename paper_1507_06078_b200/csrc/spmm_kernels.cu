@@ -40,6 +40,12 @@ namespace {
 #ifndef ARR_SPMM_FLAT_U
 #define ARR_SPMM_FLAT_U 2  // rows in flight per thread in the flat kernel
 #endif
+#ifndef ARR_SPMM_PF
+#define ARR_SPMM_PF 0  // per-thread L2 prefetch of the next row's DRAM-bound operands (Y_{j-1} row, leading-edge gather)
+#endif
+#ifndef ARR_SPMM_PF_AHEAD
+#define ARR_SPMM_PF_AHEAD 1  // rows ahead
+#endif
 #ifndef ARR_SPMM_SEQ
 #define ARR_SPMM_SEQ 0  // 1: each row slot walks a contiguous run of the tile's rows (L1 reuse of x-neighbours)
 #endif
@@ -374,6 +380,22 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
             const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
             if (lr >= nrows) break;
             const int64_t i = r0 + lr;
+#if ARR_SPMM_PF
+            {
+                // Only two of a row's loads miss L2 (the Y_{j-1} row and the first touch of
+                // its leading-edge gather); pull a later row's into L2 now, without registers.
+                const int rn = rr + ARR_SPMM_PF_AHEAD;
+                const int lrn = ARR_SPMM_SEQ ? r * RR + rn : rn * R + r;
+                if (rn < RR && lrn < nrows) {
+                    const int64_t in = r0 + lrn;
+                    if (HAS_PREV)
+                        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a.Yprev + in * a.ld_prev + v0 * VEC));
+                    const int q1 = s_rp[lrn + 1];
+                    if (q1 > s_rp[lrn])
+                        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(yin_v[0] + s_ent[q1 - 1].off));
+                }
+            }
+#endif
             T yp[NV];
             if (HAS_PREV) {
 #pragma unroll

@@ -102,3 +102,25 @@ def test_fullsize_cfg3_solve_certified(arr):
     # orthonormal Ritz vectors
     G = Y.T @ Y
     assert np.abs(G - np.eye(spec.k)).max() <= 1e-10
+
+
+def test_fullsize_cfg4_solve_certified(arr):
+    """cfg4 (random Zipf rows, n = 4e6, k = 1000) at full size: the solve converges
+    and the oracle recomputes every returned pair's residual with its own SpMM
+    (Eq. resi; full-scale cfg4 parity is residual
+    certificates + the reduced-n oracle solve of tests/test_gpu_parity.py)."""
+    A, spec = configs.build_config(4)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    Xd, _ = upload_X0(spec, A.n, [0])
+    ev, res, info = ctx.eig_solve(Xd, tol=spec.tol, maxit=60, s_max=spec.s_max)
+    assert info.converged == 1 and np.all(res <= spec.tol)
+    Y = Xd[:, :spec.k].cpu().numpy()
+    del Xd
+    ctx.close()
+    cert = oracle.residuals(A, Y, ev)
+    assert np.all(cert <= 1.01 * spec.tol)
+    assert np.all(np.diff(ev) <= 0)  # descending
+    # Gershgorin: every eigenvalue of A lies in [a, max_i sum_j |A_ij|]
+    assert ev[0] <= gersh_upper(A) and ev[-1] >= oracle.gershgorin_lower(A)
+    G = Y.T @ Y
+    assert np.abs(G - np.eye(spec.k)).max() <= 1e-10
