@@ -371,7 +371,8 @@ def run_ours(args):
         roofline["gather_model_bytes_per_launch"] = (12 * nnz_loc + 8 * (r1 - r0 + 1) + 8 * nnz_loc * spec.w
                                                      + 16 * (r1 - r0) * spec.w)
     ctx.close()
-    del X, X0, flush, Ad
+    Y2 = G = None  # the dense-Gram measurement held X (or X0)
+    del X, X0, flush, Ad, Y2, G
     torch.cuda.empty_cache()
 
     # e2e through the public API with HOST buffers: H2D of the CSR + X0 and D2H of the
