@@ -6,6 +6,10 @@
 
 #include "internal.cuh"
 
+#ifndef ARR_DMMA_CA
+#define ARR_DMMA_CA 1  // cp.async multi-stage pipelines for the Gram / GEMM kernels
+#endif
+
 namespace {
 
 constexpr int TILE = 64;   // CTA tile edge (4 warps, 2x2, 32x32 each)
@@ -202,6 +206,175 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const doubl
             }
 }
 
+
+// ---------------------------------------------------------------- cp.async pipelined versions
+// Same tiles, fragments, DMMA order and reduction as gram_kernel / gemm_kernel (so the
+// results are bitwise identical), with the global -> shared copies done by cp.async
+// 16-byte chunks into an S-stage ring: S-1 stages in flight while one is computed,
+// no staging registers.  Needs 16-byte aligned rows (even ld, even column offsets).
+constexpr int S_CA = 4;
+
+__device__ __forceinline__ void ca16(void *smem, const void *gmem, int bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ca_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ca_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(THREADS) gram_kernel_ca(const double *__restrict__ X, int64_t ldx, int m1,
+                                                          const double *__restrict__ Y, int64_t ldy, int m2,
+                                                          int64_t n, int64_t rows_per_split, bool sym,
+                                                          double *__restrict__ part) {
+    const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
+    if (sym && tb < ta) return;
+    const int a0 = ta * TILE, b0 = tb * TILE;
+    const int64_t k0 = (int64_t)split * rows_per_split;
+    int64_t k1 = k0 + rows_per_split;
+    if (k1 > n) k1 = n;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[KS][TILE + PAD] = reinterpret_cast<double (*)[KS][TILE + PAD]>(dsm);
+    double (*Ys)[KS][TILE + PAD] = reinterpret_cast<double (*)[KS][TILE + PAD]>(dsm + S_CA * KS * (TILE + PAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const bool work = (a0 + wm * 32 < m1) && (b0 + wn * 32 < m2) && !(sym && ta == tb && wm > wn);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // one stage = KS rows x 64 columns of X and of Y = 2 x 512 chunks of 16 bytes, 4 + 4 per thread
+    auto load = [&](int64_t kb, int st) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int idx = tid + q * THREADS;
+            const int rr = idx >> 5, cc = (idx & 31) * 2;
+            const int64_t row = kb + rr;
+            const bool rok = row < k1;
+            const int nx = rok ? max(0, min(2, m1 - (a0 + cc))) : 0;
+            const int ny = rok ? max(0, min(2, m2 - (b0 + cc))) : 0;
+            ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
+            ca16(&Ys[st][rr][cc], ny ? Y + row * ldy + b0 + cc : Y, ny * 8);
+        }
+    };
+    const int64_t nk = (k1 - k0 + KS - 1) / KS;
+#pragma unroll
+    for (int st = 0; st < S_CA - 1; ++st) {
+        if (st < nk) load(k0 + st * KS, st);
+        ca_commit();
+    }
+    for (int64_t it = 0; it < nk; ++it) {
+        ca_wait<S_CA - 2>();
+        __syncthreads();
+        const int64_t nx = it + S_CA - 1;
+        if (nx < nk) load(k0 + nx * KS, (int)(nx % S_CA));
+        ca_commit();
+        const int buf = (int)(it % S_CA);
+        if (work) {
+#pragma unroll
+            for (int kk = 0; kk < KS / 4; ++kk) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * 32 + mt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+            }
+        }
+    }
+    ca_wait<0>();
+    double *P = part + (int64_t)split * m1 * m2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int ra = a0 + wm * 32 + mt * 8 + (lane >> 2);
+                const int cb = b0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
+                if (ra < m1 && cb < m2) P[(int64_t)ra * m2 + cb] = acc[mt][nt][e];
+            }
+}
+
+__global__ void __launch_bounds__(THREADS) gemm_kernel_ca(double alpha, const double *__restrict__ X, int64_t ldx,
+                                                          int m1, const double *__restrict__ B, int64_t ldb, int m2,
+                                                          double beta, const double *Cin, int64_t ldc, double *Out,
+                                                          int64_t ldo, int64_t n, int upper) {
+    const int64_t r0 = (int64_t)blockIdx.x * TILE;
+    const int c0 = blockIdx.y * TILE;
+    if (upper && c0 + TILE < m1) m1 = c0 + TILE;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[TILE][KS + PAD] = reinterpret_cast<double (*)[TILE][KS + PAD]>(dsm);
+    double (*Bs)[KS][TILE + PAD] = reinterpret_cast<double (*)[KS][TILE + PAD]>(dsm + S_CA * TILE * (KS + PAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // one stage = 64 rows x 16 k of X (8 chunks per row) and 16 k x 64 columns of B (32 chunks per row)
+    auto load = [&](int kb, int st) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int idx = tid + q * THREADS;
+            const int xr = idx >> 3, xk = (idx & 7) * 2;
+            const int64_t row = r0 + xr;
+            const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
+            ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
+            const int bk = idx >> 5, bc = (idx & 31) * 2;
+            const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
+            ca16(&Bs[st][bk][bc], nb ? B + (int64_t)(kb + bk) * ldb + c0 + bc : B, nb * 8);
+        }
+    };
+    const int nk = (m1 + KS - 1) / KS;
+#pragma unroll
+    for (int st = 0; st < S_CA - 1; ++st) {
+        if (st < nk) load(st * KS, st);
+        ca_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        ca_wait<S_CA - 2>();
+        __syncthreads();
+        const int nx = it + S_CA - 1;
+        if (nx < nk) load(nx * KS, nx % S_CA);
+        ca_commit();
+        const int buf = it % S_CA;
+#pragma unroll
+        for (int kk = 0; kk < KS / 4; ++kk) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * 32 + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+        }
+    }
+    ca_wait<0>();
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t row = r0 + wm * 32 + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
+                if (row < n && cb < m2) {
+                    double v = alpha * acc[mt][nt][e];
+                    if (beta != 0.0) v += beta * Cin[row * ldc + cb];
+                    Out[row * ldo + cb] = v;
+                }
+            }
+}
+
+bool ca_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
+
 // ---------------------------------------------------------------- small dense
 __global__ void svqb_prep_kernel(const double *__restrict__ G, int w, double *__restrict__ D,
                                  double *__restrict__ Gs) {
@@ -290,6 +463,17 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     int64_t rps = (n + ns - 1) / ns;
     rps = (rps + KS - 1) / KS * KS;
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
+#if ARR_DMMA_CA
+    if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
+        const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(gram_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        gram_kernel_ca<<<grid, THREADS, smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    } else
+#endif
     gram_kernel<<<grid, THREADS, 0, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
     gram_reduce_kernel<<<nblk((int64_t)m1 * m2, 256), 256, 0, c->stream>>>(partials, ns, m1, m2, sym, G, ldg);
     c->launches += 2;
@@ -299,6 +483,18 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
                  int64_t n, int upper) {
     dim3 grid((unsigned)((n + TILE - 1) / TILE), (m2 + TILE - 1) / TILE);
+#if ARR_DMMA_CA
+    if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
+        const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(gemm_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        gemm_kernel_ca<<<grid, THREADS, smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n,
+                                                           upper);
+    } else
+#endif
     gemm_kernel<<<grid, THREADS, 0, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
     c->launches++;
 }
