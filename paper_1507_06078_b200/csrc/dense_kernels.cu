@@ -212,7 +212,13 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const doubl
 // results are bitwise identical), with the global -> shared copies done by cp.async
 // 16-byte chunks into an S-stage ring: S-1 stages in flight while one is computed,
 // no staging registers.  Needs 16-byte aligned rows (even ld, even column offsets).
-constexpr int S_CA = 4;
+#ifndef ARR_DMMA_STAGES
+#define ARR_DMMA_STAGES 2  // measured on B200: 2 stages at 5 CTAs/SM beat 4 stages at 3 (cfg3 ARR basis 623 -> 576 ms)
+#endif
+#ifndef ARR_DMMA_MINB
+#define ARR_DMMA_MINB 5
+#endif
+constexpr int S_CA = ARR_DMMA_STAGES;
 
 __device__ __forceinline__ void ca16(void *smem, const void *gmem, int bytes) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -222,7 +228,7 @@ __device__ __forceinline__ void ca_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void ca_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(THREADS) gram_kernel_ca(const double *__restrict__ X, int64_t ldx, int m1,
+__global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gram_kernel_ca(const double *__restrict__ X, int64_t ldx, int m1,
                                                           const double *__restrict__ Y, int64_t ldy, int m2,
                                                           int64_t n, int64_t rows_per_split, bool sym,
                                                           double *__restrict__ part) {
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(THREADS) gram_kernel_ca(const double *__restri
             }
 }
 
-__global__ void __launch_bounds__(THREADS) gemm_kernel_ca(double alpha, const double *__restrict__ X, int64_t ldx,
+__global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gemm_kernel_ca(double alpha, const double *__restrict__ X, int64_t ldx,
                                                           int m1, const double *__restrict__ B, int64_t ldb, int m2,
                                                           double beta, const double *Cin, int64_t ldc, double *Out,
                                                           int64_t ldo, int64_t n, int upper) {
@@ -442,7 +448,13 @@ int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     static int per_sm = 0;
     if (per_sm == 0) {
         int o = 0;
+#if ARR_DMMA_CA
+        cudaFuncSetAttribute(gram_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * 2 * S_CA * KS * (TILE + PAD)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
+#else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gram_kernel, THREADS, 0);
+#endif
         per_sm = o > 0 ? o : 1;
     }
     const int64_t slots = (int64_t)num_sms * per_sm;
