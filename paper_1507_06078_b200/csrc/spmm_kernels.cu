@@ -25,20 +25,8 @@ namespace {
 #ifndef ARR_SPMM_V4
 #define ARR_SPMM_V4 0  // 1: 256-bit accesses when the block is 32-byte aligned with ld % 4 == 0
 #endif
-#ifndef ARR_SPMM_PREFETCH
-#define ARR_SPMM_PREFETCH 0  // 1: bulk L2 prefetch (UBLKPF) of the next tile's Y_{j-1} rows, Y_j leading edge, CSR slice
-#endif
-#ifndef ARR_SPMM_ASYNC
-#define ARR_SPMM_ASYNC 0  // 1: rows of <= 7 entries gathered by per-thread cp.async into shared-memory slots, one row ahead
-#endif
 #ifndef ARR_SPMM_WS
 #define ARR_SPMM_WS 1  // warp-specialised kernel: a producer warp stages the CSR of the next tile (2-stage ring)
-#endif
-#ifndef ARR_SPMM_FLAT
-#define ARR_SPMM_FLAT 0  // 1: row-cyclic "flat" kernel (no tiles; every thread a fixed column vector) in natural order
-#endif
-#ifndef ARR_SPMM_FLAT_U
-#define ARR_SPMM_FLAT_U 2  // rows in flight per thread in the flat kernel
 #endif
 #ifndef ARR_SPMM_PF
 #define ARR_SPMM_PF 1  // per-thread L2 prefetch of a later row's DRAM-bound operands (Y_{j-1} row, leading-edge gather)
@@ -199,42 +187,12 @@ __device__ __forceinline__ void fma_vec<4>(d4 &acc, double a, const d4 &x) {
 
 constexpr int kTile = 64;  // rows per tile (the unit of the processing order)
 
-// Bulk L2 prefetch of [p, p + bytes) (TMA engine; no registers, no smem):
-// the range is widened to 16-byte boundaries.
-__device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
-    if (bytes <= 0) return;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    uintptr_t cur = a & ~uintptr_t(15);
-    const uintptr_t end = (a + (uint64_t)bytes) & ~uintptr_t(15);  // never past the range's end
-    if (end <= cur) return;
-    uint64_t total = end - cur;
-    while (total > 0) {  // the size operand is 32-bit
-        const uint32_t chunk = total > (1u << 30) ? (1u << 30) : (uint32_t)total;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cur), "r"(chunk) : "memory");
-        cur += chunk;
-        total -= chunk;
-    }
-}
 
 // One staged non-zero: element offset of the referenced Y row and the value.
 struct __align__(16) Ent {
     int64_t off;  // col * ld_in
     double val;
 };
-
-__device__ __forceinline__ void cp_async16_ca(void *smem, const void *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16_cg(void *smem, const void *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-constexpr int kAsyncStages = 2;  // rows per thread in shared memory: one computed, one in flight
 
 // Epilogue of one row: out = alpha*(acc - shift*y_i) + beta*y_prev, column
 // sums of squares, evict-first store.
@@ -272,8 +230,7 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
 __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nrows, int R, int RR, int r, int TX,
                                           int v0, int wv, const int *s_rp, const Ent *s_ent,
-                                          double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream,
-                                          unsigned char *slots) {
+                                          double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream) {
     using V = Vec<VEC>;
     using T = typename V::T;
     constexpr int P = (ARR_SPMM_PAIR && NV == 1 && K <= 7) ? 2 : 1;  // rows in flight per thread
@@ -284,59 +241,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
         const int vv = v0 + v * TX;
         yin_v[v] = a.Yin + (vv < wv ? vv : 0) * VEC;
     }
-    if constexpr (ARR_SPMM_ASYNC && VEC == 2 && NV == 1 && K <= 7) {
-        // Per-thread software pipeline through shared memory: the K gathers of
-        // Y_j, the Y_{j-1} element and y_i of row rr+1 are issued as cp.async
-        // (no registers held while in flight) before row rr is computed from its
-        // slots.  Each thread reads only the slots it filled: no block barrier.
-        constexpr int SL = K + 1;  // slots per row: K gathers, Y_{j-1} (y_i is an L1 load)
-        double2 *my = reinterpret_cast<double2 *>(slots) + threadIdx.x;
-        const int nthr = blockDim.x;
-        auto issue = [&](int rr, int st) {
-            const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
-            if (rr < RR && lr < nrows) {
-                const int64_t i = r0 + lr;
-                const int p0 = s_rp[lr], p1 = s_rp[lr + 1];
-                const int64_t safe = p0 < p1 ? s_ent[p0].off : i * a.ld_in;
-#pragma unroll
-                for (int u = 0; u < K; ++u) {
-                    const int64_t o = (p0 + u < p1) ? s_ent[p0 + u].off : safe;
-                    cp_async16_ca(my + (st * SL + u) * nthr, yin_v[0] + o);
-                }
-                if (HAS_PREV) cp_async16_cg(my + (st * SL + K) * nthr, a.Yprev + i * a.ld_prev + v0 * 2);
-            }
-            cp_async_commit();
-        };
-        issue(0, 0);
-        for (int rr = 0; rr < RR; ++rr) {
-            const int lr = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
-            if (lr >= nrows) break;
-            issue(rr + 1, (rr + 1) % kAsyncStages);
-            cp_async_wait<1>();  // row rr's group has landed
-            const int st = rr % kAsyncStages;
-            const int64_t i = r0 + lr;
-            const int p0 = s_rp[lr], p1 = s_rp[lr + 1];
-            double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < K; ++u) {
-                const double av = (p0 + u < p1) ? s_ent[p0 + u].val : 0.0;
-                fma_vec<2>(acc, av, my[(st * SL + u) * nthr]);
-            }
-            const double2 yp = HAS_PREV ? my[(st * SL + K) * nthr] : make_double2(0.0, 0.0);
-            const double2 yi = V::ldg(a.Yin + i * a.ld_in + v0 * 2);
-            double2 out;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double sh = COLSHIFT ? __ldg(a.colshift + v0 * 2 + e) : a.shift;
-                double o = a.alpha * (V::get(acc, e) - sh * V::get(yi, e));
-                if (HAS_PREV) o += a.beta * V::get(yp, e);
-                V::set(out, e, o);
-                if (SUMSQ) ss[0][e] = fma(o, o, ss[0][e]);
-            }
-            if (STORE) STREAM_ST(a.Yout + i * a.ld_out + v0 * 2, out);
-        }
-        cp_async_wait<0>();
-    } else if constexpr (P == 2) {
+    if constexpr (P == 2) {
         for (int rr = 0; rr < RR; rr += 2) {
             const int lr0 = ARR_SPMM_SEQ ? r * RR + rr : rr * R + r;
             const int lr1 = ARR_SPMM_SEQ ? lr0 + 1 : lr0 + R;
@@ -450,7 +355,6 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
     const int RR = 0;  // recomputed per tile in tile_rows
     Ent *s_ent = reinterpret_cast<Ent *>(smem_raw);                      // [nnz_cap]
     int *s_rp = reinterpret_cast<int *>(smem_raw + sizeof(Ent) * nnz_cap);  // [kTile+2] (relative)
-    unsigned char *slots = smem_raw + ((sizeof(Ent) * nnz_cap + 4 * (kTile + 2) + 15) & ~size_t(15));  // async slots
     __shared__ int64_t s_base;
 
     const int tid = threadIdx.x;
@@ -476,7 +380,6 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
     // assignment so their per-CTA partial sums are deterministic.
     constexpr bool DYN = !SUMSQ;
     __shared__ int64_t s_next[2];
-    __shared__ int64_t s_bw;
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; ++it) {
         // next tile of this CTA, taken one tile ahead (read after the staging barriers)
@@ -551,41 +454,9 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
                 s_ent[q] = e;
             }
             __syncthreads();
-#if ARR_SPMM_PREFETCH
-            if (done == 0 && tid == nthr - 1) {
-                // Warm L2 for this CTA's next tile while this one is computed: its Y_{j-1}
-                // rows (a stream), the leading edge of the Y_j rows it gathers (first
-                // touch; band estimate bw = last column of this tile - its last row),
-                // and its row_ptr / CSR slice (estimated from this tile's density).
-                const int64_t tn = s_next[it & 1];
-                if (tn < ntiles) {
-                    int64_t r0n;
-                    int nn;
-                    if (a.tile_row0) { r0n = __ldg(a.tile_row0 + tn); nn = __ldg(a.tile_len + tn); }
-                    else { r0n = tn * RT; nn = (int)min((int64_t)RT, a.n - r0n); }
-                    if (HAS_PREV) l2_prefetch(a.Yprev + r0n * a.ld_prev, ((int64_t)(nn - 1) * a.ld_prev + a.w) * 8);
-                    const int64_t lastcol = cnt > 0 && nnz_t > 0 ? s_ent[nnz_t - 1].off / ld : r0;
-                    const int64_t bw = lastcol - (r0 + cnt - 1);
-                    int64_t e0 = r0n + bw, e1 = r0n + nn + bw;
-                    if (e0 < 0) e0 = 0;
-                    if (e1 > a.n) e1 = a.n;
-                    if (e1 > e0 && bw > 0) l2_prefetch(a.Yin + e0 * ld, ((e1 - e0 - 1) * ld + a.w) * 8);
-                    l2_prefetch(rp + r0n, (int64_t)(nn + 1) * 8);
-                    const int64_t per = (int64_t)nnz_t * nn / (cnt > 0 ? cnt : 1);
-                    const int64_t est = base + (int64_t)((double)(r0n - r0) * ((double)nnz_t / (cnt > 0 ? cnt : 1)));
-                    int64_t cnt_e = per + per / 8 + 32;
-                    if (est >= 0 && est < a.nnz) {
-                        if (est + cnt_e > a.nnz) cnt_e = a.nnz - est;
-                        l2_prefetch(col + est, cnt_e * 4);
-                        l2_prefetch(val + est, cnt_e * 8);
-                    }
-                }
-            }
-#endif
             if (active)
                 tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
-                                                                        s_rp, s_ent, ss, pol_keep, pol_stream,
-                                                                        slots);
+                                                                        s_rp, s_ent, ss, pol_keep, pol_stream);
             done += cnt;
         }
         __syncthreads();  // every thread is done with this tile's staging and has s_next
@@ -626,7 +497,7 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
 }
 
 #ifndef ARR_SPMM_CAP
-#define ARR_SPMM_CAP (ARR_SPMM_ASYNC ? 1024 : 2048)
+#define ARR_SPMM_CAP 2048
 #endif
 constexpr int kNnzCap = ARR_SPMM_CAP;  // staged CSR entries per tile pass
 #ifndef ARR_SPMM_WS_CAP
@@ -772,8 +643,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a
             if (info.mode == 0) {
                 if (active)
                     tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, info.r0, info.nrows, R, 0, r, TX, v0, wv,
-                                                                            s_rp, s_ent, ss, pol_keep, pol_stream,
-                                                                            nullptr);
+                                                                            s_rp, s_ent, ss, pol_keep, pol_stream);
             } else if (active && r == 0) {
                 // one row longer than a stage: CSR order straight from global memory
                 using Vv = Vec<VEC>;
@@ -867,7 +737,6 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     const int RT = c->tile_rows;  // rows per tile in natural order (<= kTile)
     // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
     size_t smem = ((sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
-    if (ARR_SPMM_ASYNC && VEC == 2 && NV == 1 && K <= 7) smem += (size_t)kAsyncStages * (K + 1) * nthr * 16;
     const size_t red = 8 * (size_t)nthr * VEC;
     if (smem < red) smem = red;
     static int occ = -1;  // per instantiation (one device per process)
@@ -924,151 +793,6 @@ int dispatch_nv(arr_ctx *c, const SpmmArgs &a) {
 }
 
 
-// Row-cyclic fused SpMM ("flat"): the grid's T threads are cut into RS = T / wv
-// row slots of wv threads; thread g owns column vector v = g % wv of rows
-// g / wv, g / wv + RS, ... (U rows in flight), so at any moment the whole GPU
-// streams one contiguous window of ~U*RS rows, like a copy.  The CSR of a row
-// is read straight from global memory (broadcast within the row's threads, L1
-// hits across them).  Per-row sums in CSR order, same arithmetic as the tiled
-// kernel.  Column sums of squares: fixed thread -> (column, rows) assignment,
-// so the per-CTA partials are deterministic.
-template <int VEC, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
-__global__ void __launch_bounds__(512, 2) spmm_flat_kernel(SpmmArgs a, int wv, int64_t RS) {
-    using V = Vec<VEC>;
-    using T = typename V::T;
-    constexpr int U = ARR_SPMM_FLAT_U;
-    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t slot = g / wv;
-    const int v = (int)(g - slot * wv);
-    const bool act = slot < RS;
-    double ss[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) ss[e] = 0.0;
-    const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_stream = policy_evict_first();
-    const double *yin_v = a.Yin + v * VEC;
-    if (act) {
-        for (int64_t i0 = slot; i0 < a.n; i0 += (int64_t)U * RS) {
-            int64_t p0[U], p1[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t i = i0 + u * RS;
-                p0[u] = i < a.n ? __ldg(a.row_ptr + i) : 0;
-                p1[u] = i < a.n ? __ldg(a.row_ptr + i + 1) : 0;
-            }
-            T yp[U];
-            if (HAS_PREV) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int64_t i = i0 + u * RS;
-                    yp[u] = i < a.n ? STREAM_LD(a.Yprev + i * a.ld_prev + v * VEC) : V::zero();
-                }
-            }
-            T acc[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] = V::zero();
-            // chunks of K entries (one chunk for stencil rows)
-            int64_t q[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) q[u] = p0[u];
-            bool more = true;
-            while (more) {
-                int64_t off[U][K];
-                double av[U][K];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const bool ok = q[u] + k < p1[u];
-                        const int64_t idx = ok ? q[u] + k : (p0[u] < p1[u] ? p0[u] : 0);
-                        off[u][k] = (int64_t)__ldg(a.col + idx) * a.ld_in;
-                        av[u][k] = ok ? __ldg(a.val + idx) : 0.0;
-                    }
-                T x[U][K];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int k = 0; k < K; ++k) x[u][k] = GATHER(yin_v + off[u][k]);
-                more = false;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) fma_vec<VEC>(acc[u], av[u][k], x[u][k]);
-                    q[u] += K;
-                    more = more || (q[u] < p1[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t i = i0 + u * RS;
-                if (i >= a.n) continue;
-                const T yi = V::ldg(a.Yin + i * a.ld_in + v * VEC);
-                T out;
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    const double sh = COLSHIFT ? __ldg(a.colshift + v * VEC + e) : a.shift;
-                    double o = a.alpha * (V::get(acc[u], e) - sh * V::get(yi, e));
-                    if (HAS_PREV) o += a.beta * V::get(yp[u], e);
-                    V::set(out, e, o);
-                    if (SUMSQ) ss[e] = fma(o, o, ss[e]);
-                }
-                if (STORE) STREAM_ST(a.Yout + i * a.ld_out + v * VEC, out);
-            }
-        }
-    }
-    if (SUMSQ) {
-        // per CTA: sum over its threads of the same column, fixed order (thread order)
-        extern __shared__ double red_f[];
-        const int tid = threadIdx.x;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) red_f[tid * VEC + e] = act ? ss[e] : 0.0;
-        __syncthreads();
-        // columns present in this CTA: threads g in [g0, g0+B); thread with lowest g per column sums
-        const int64_t g0 = blockIdx.x * (int64_t)blockDim.x;
-        for (int cv = tid; cv < wv; cv += blockDim.x) {
-            double sum[VEC];
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
-            // first local thread index with column cv
-            int64_t first = cv - (g0 % wv);
-            if (first < 0) first += wv;
-            for (int64_t t = first; t < blockDim.x; t += wv)
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) sum[e] += red_f[t * VEC + e];
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const int colid = cv * VEC + e;
-                if (colid < a.w) a.partials[(int64_t)blockIdx.x * a.w + colid] = sum[e];
-            }
-        }
-    }
-}
-
-template <int VEC, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
-int launch_flat(arr_ctx *c, const SpmmArgs &a, int wv) {
-    auto kern = spmm_flat_kernel<VEC, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
-    const int B = 512;
-    int64_t G = (int64_t)c->num_sms * 2;
-    int64_t RS = G * B / wv;
-    if (RS > a.n) { RS = a.n; G = (RS * wv + B - 1) / B; }
-    const size_t smem = SUMSQ ? sizeof(double) * B * VEC : 0;
-    kern<<<(unsigned)G, B, smem, c->stream>>>(a, wv, RS);
-    c->launches++;
-    return (int)G;
-}
-
-template <int VEC, int K>
-int dispatch_flat(arr_ctx *c, const SpmmArgs &a) {
-    const int wv = (a.w + VEC - 1) / VEC;
-    const bool prev = a.Yprev != nullptr, store = a.Yout != nullptr, ss = a.partials != nullptr,
-               cs = a.colshift != nullptr;
-    if (prev && store && !ss && !cs) return launch_flat<VEC, K, true, true, false, false>(c, a, wv);
-    if (prev && store && ss && !cs) return launch_flat<VEC, K, true, true, true, false>(c, a, wv);
-    if (!prev && store && !ss && !cs) return launch_flat<VEC, K, false, true, false, false>(c, a, wv);
-    if (!prev && store && ss && !cs) return launch_flat<VEC, K, false, true, true, false>(c, a, wv);
-    if (!prev && !store && ss && cs) return launch_flat<VEC, K, false, false, true, true>(c, a, wv);
-    return -1;
-}
 
 __global__ void rowlen_max_kernel(const int64_t *__restrict__ rp, int64_t n, int *out) {
     int m = 0;
@@ -1199,15 +923,6 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     if (a.Yprev) v2 = v2 && vec2_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
     c->spmm_blocks++;
-#if ARR_SPMM_FLAT
-    if (!a.tile_row0 && v2 && a.w <= 2 * 512 * 148) {
-        const int L = c->max_row_nnz;
-        if (L <= 3) return dispatch_flat<2, 3>(c, a);
-        if (L <= 5) return dispatch_flat<2, 5>(c, a);
-        if (L <= 7) return dispatch_flat<2, 7>(c, a);
-        return dispatch_flat<2, 9>(c, a);
-    }
-#endif
 #if ARR_SPMM_V4
     bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
     if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);
