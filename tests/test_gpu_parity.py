@@ -342,3 +342,31 @@ def test_lean_context_is_bitwise_identical(arr, kind, monkeypatch):
     assert out[0][2] == out[1][2]
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert np.array_equal(out[0][3], out[1][3])
+
+
+def test_cfg2_full_filter_and_arr_vs_oracle(arr):
+    """The bench workload (configs[1] = cfg2, n = 90,000, w = 220) in the launch
+    configuration eig_solve uses: one MPM sweep (d = 20) against the oracle's
+    element by element (rel. Frobenius <= 1e-12, BASELINE north star), then one ARR
+    (p = 1) on the filtered block against the oracle's paper-literal ARR (pivoted QR
+    of [X, AX]; same span, different orthonormalisation, R8): the leading w
+    Ritz values agree to 1e-11 relative."""
+    A, spec = configs.build_config(2)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    a = ctx.eig_gershgorin_lower()
+    mu0, _, _ = oracle.rayleigh_ritz(A, X0)
+    b = float(mu0[spec.w - 1])
+    ctx.eig_set_interval(a, b)
+    Xd = torch.from_numpy(X0).cuda()
+    ctx.filter_step(Xd, normalize=True)
+    ref = oracle.mpm_sweep(A, a, b, spec.d, X0)
+    assert relF(host(Xd), ref) <= 1e-12
+    Y = torch.empty_like(Xd)
+    ritz, rank = ctx.arr_project(Xd, Y)
+    mu, _, _ = oracle.arr(A, ref, spec.p)
+    w = spec.w
+    assert np.max(np.abs(ritz[:w] - mu[:w]) / np.abs(mu[:w])) <= 1e-11
+    res = ctx.residuals(Y[:, :spec.k], ritz[:spec.k])
+    res_o = oracle.residuals(A, host(Y)[:, :spec.k], ritz[:spec.k])
+    assert np.max(np.abs(res - res_o)) <= 1e-12 * max(1.0, res_o.max())
