@@ -10,9 +10,6 @@
 
 namespace {
 
-#ifndef ARR_SPMM_U
-#define ARR_SPMM_U 8  // gathers in flight per row (single column-vector case)
-#endif
 #ifndef ARR_SPMM_MAXT
 #define ARR_SPMM_MAXT 512
 #endif
