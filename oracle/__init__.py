@@ -25,6 +25,10 @@ from .core import (  # noqa: F401
     mpm_sweep,
     gershgorin_lower,
     chebyshev_T,
+    interp_coeffs,
+    psi,
+    poly_filter,
+    poly_sweep,
     orthonormalize,
     rayleigh_ritz,
     arr,

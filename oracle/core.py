@@ -136,6 +136,71 @@ def chebyshev_T(d: int, t):
     return r1
 
 
+def interp_coeffs(d: int) -> np.ndarray:
+    """Chebyshev coefficients a_0..a_d of psi_d(t) = sum_k a_k T_k(t), the degree-d
+    Chebyshev interpolant of f_d(t) = max(0, t)^{10 d} (Eq. def:fN,
+    P:1198-1202) at the points of the second kind t_j = -cos(j pi / d), j = 0..d
+    (P:1186-1189).  The interpolant is unique, so it is written as the solution of
+    the square collocation system sum_k a_k T_k(t_j) = f_d(t_j) (one library solve).
+    Reading (R18): psi_d is kept in the Chebyshev basis; the paper's
+    monomial coefficients Gamma_d (Eq. chebfun-f) reach 1e5 (d = 20) and 3e8 (d = 30)
+    with alternating signs, so two fp64 computations of them differ by 1e-11 to 1e-7
+    relative and Alg. poly's Horner output by up to 1e-4 — not a reproducible target."""
+    if d < 1:
+        raise ValueError("d >= 1")
+    t = -np.cos(np.arange(d + 1) * np.pi / d)
+    f = np.maximum(0.0, t) ** (10 * d)
+    return np.linalg.solve(chebyshev_basis(d, t), f)
+
+
+def chebyshev_basis(d: int, t) -> np.ndarray:
+    """[T_0(t), .., T_d(t)] as columns (three-term recursion, Eq. cheby-poly)."""
+    t = np.asarray(t, dtype=np.float64)
+    B = np.empty((t.size, d + 1))
+    for k in range(d + 1):
+        B[:, k] = chebyshev_T(k, t)
+    return B
+
+
+def psi(coef: np.ndarray, t):
+    """psi_d(t) = sum_k a_k T_k(t) (plain sum over the basis)."""
+    t = np.asarray(t, dtype=np.float64)
+    return chebyshev_basis(len(coef) - 1, t.ravel()).dot(coef).reshape(t.shape)
+
+
+def poly_filter(A, a: float, b: float, coef: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Y = rho_d(A) X with rho_d(t) = psi_d(c_0 + c_1 t), c_0 = (a+b)/(a-b),
+    c_1 = 2/(b-a) (Eq. rhod; the map of Alg. poly), evaluated by
+    Clenshaw's recurrence in the Chebyshev basis with S = c_1 A + c_0 I:
+        b_{d+1} = b_{d+2} = 0,  b_k = a_k X + 2 S b_{k+1} - b_{k+2}  (k = d .. 1),
+        Y = a_0 X + S b_1 - b_2."""
+    if not a < b:
+        raise ValueError("need a < b")
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    c0 = (a + b) / (a - b)
+    c1 = 2.0 / (b - a)
+    d = len(coef) - 1
+
+    def S(V):
+        return c1 * spmm(A, V) + c0 * V
+
+    b2 = np.zeros_like(X)
+    b1 = np.zeros_like(X)
+    for k in range(d, 0, -1):
+        b1, b2 = coef[k] * X + 2.0 * S(b1) - b2, b1
+    return coef[0] * X + S(b1) - b2
+
+
+def poly_sweep(A, a: float, b: float, coef: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """One multi-power sweep with the paper's filter: rho_d(A) then column normalisation
+    (Alg. Arrabit2)."""
+    Y = poly_filter(A, a, b, coef, X)
+    nrm = col_norms(Y)
+    if np.any(nrm == 0) or not np.all(np.isfinite(nrm)):
+        raise FloatingPointError("zero or non-finite column after filtering")
+    return Y / nrm
+
+
 # --------------------------------------------------------------------------- dense
 def orthonormalize(Z: np.ndarray):
     """U in orth(Z) (Alg. RR step 1): equilibrate columns (span unchanged),
@@ -199,13 +264,15 @@ def residuals(A, Y: np.ndarray, mu: np.ndarray) -> np.ndarray:
     return col_norms(R) / np.maximum(1.0, np.abs(mu))
 
 
-def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int) -> int:
+def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int, gamma=None) -> int:
     """Sweeps between ARR steps (DESIGN.md §4 R6, the dynamic-range rule that
-    replaces the paper's rcond inner stop P:1355-1388): amp = |T_d((mu_1-c)/e)|,
+    replaces the paper's rcond inner stop P:1355-1388): amp = |T_d((mu_1-c)/e)|
+    (|psi_d((mu_1-c)/e)| with the interpolant filter),
     s = s_max if amp <= 1 else clamp(floor(8/log10(amp)), 1, s_max)."""
     c = 0.5 * (a + b)
     e = 0.5 * (b - a)
-    amp = abs(float(chebyshev_T(d, (mu1 - c) / e)))
+    t = (mu1 - c) / e
+    amp = abs(float(chebyshev_T(d, t) if gamma is None else psi(gamma, np.array([t]))[0]))
     if not amp > 1.0:
         return s_max
     if not math.isfinite(amp):
@@ -225,7 +292,7 @@ class SolveResult:
 
 
 def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
-          s_max: int = 5, w: int | None = None, max_outer: int | None = None) -> SolveResult:
+          s_max: int = 5, w: int | None = None, max_outer: int | None = None, filter: str = "cheb") -> SolveResult:
     """Fixed-parameter ARRABIT-MPM (Alg. Arrabit2, with the
     adaptive lines disabled; DESIGN.md §4 R3/R6/R10):
 
@@ -237,6 +304,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     """
     n = A.n
     w = X0.shape[1] if w is None else w  # w - k guard vectors
+    gamma = None if filter == "cheb" else interp_coeffs(d)  # "interp": the paper's psi_d (R18)
     X = np.array(X0[:, :w], dtype=np.float64, copy=True)
     a = gershgorin_lower(A)
     mu0, _, _ = rayleigh_ritz(A, X)
@@ -252,9 +320,9 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     res = np.full(k, np.inf)
     mono, prev_maxres = False, None
     for outer in range(1, limit + 1):
-        s = sweeps_rule(mu1, a, b, d, s_max)
+        s = sweeps_rule(mu1, a, b, d, s_max, gamma)
         for _ in range(s):
-            X = mpm_sweep(A, a, b, d, X)
+            X = mpm_sweep(A, a, b, d, X) if gamma is None else poly_sweep(A, a, b, gamma, X)
         sweeps += s
         mu, Y, r = arr(A, X, p, keep=w)
         res = residuals(A, Y[:, :k], mu[:k])
