@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--filter", default="cheb", choices=["cheb", "interp"],
+                    help="cheb: T_d (default); interp: the paper's interpolant psi_d (Section 5)")
     ap.add_argument("--partition", action="store_true",
                     help="N>1: row-partition the config over the ranks even for configs 1-2")
     return ap.parse_args()
@@ -258,6 +260,8 @@ def run_ours(args):
         comm = arr.Comm.from_torch_distributed()
     ctx = arr.eig_init(Ad, spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm, plan=plan)
     ctx_lean = ctx.workspace_bytes < 8 * nrows * spec.w * (spec.p + 2)
+    if args.filter != "cheb":
+        ctx.eig_set_filter(args.filter)
     sched = None
     if spec.kind in ("lap3dV", "st27") and not partitioned:
         # 3-D grids: y-band processing order (results unchanged; shorter L2 reuse distance of the
@@ -318,6 +322,8 @@ def run_ours(args):
     deg_ms = phase_ms[0] / max(1, phase_cnt[0])
     nnz_loc = int(Aloc.nnz) if not partitioned else plan.nnz
     bpl = filter_bytes_per_degree(r1 - r0, nnz_loc, spec.w, spec.d)
+    if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
+        bpl += 8 * (r1 - r0) * spec.w
     achieved = bpl / (deg_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
@@ -379,7 +385,9 @@ def run_ours(args):
     # eigenpairs inside the timed region (one GPU: the eig_solve_host C-ABI call;
     # partitioned: each rank uploads its local CSR + X0 rows, eig_init_dist, eig_solve)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.filter != "cheb":
+        e2e = {"value": None, "unit": UNIT, "error": "the host-buffer entry eig_solve_host applies T_d only"}
+    elif not args.no_e2e:
         try:
             xp = torch.from_numpy(X0h).pin_memory()
             evec = torch.empty((r1 - r0, spec.k), dtype=torch.float64).pin_memory()
@@ -448,6 +456,7 @@ def run_ours(args):
                 "data": "synthetic",
                 "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "w": spec.w, "d": spec.d,
                            "p": spec.p, "tol": spec.tol, "step": "one full eig_solve from X0",
+                           "filter": {"cheb": "T_d (Eq. cheby-poly)", "interp": "psi_d (paper Section 5)"}[args.filter],
                            "l2": "flushed between timed steps (256 MiB write), outside the events",
                            "parallelism": par, "row_order": sched or "natural",
                            "context": "lean (no scratch block)" if ctx_lean else "standard",

@@ -184,6 +184,15 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b);
 arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles);
 /* Change the degree d used by filter_step (1 <= d). */
 arr_status eig_set_degree(arr_ctx *c, int32_t d);
+/* Polynomial of filter_step / eig_solve: kind 0 = the classic Chebyshev polynomial
+ * T_d of the mapped matrix (default, Eq. cheby-poly); kind 1 = the
+ * paper's default filter rho_d(t) = psi_d((2t - a - b)/(b - a)), psi_d the degree-d
+ * Chebyshev interpolant of max(0, t)^{10 d} at the Chebyshev points of the second
+ * kind (Section 5), applied in the Chebyshev basis by Clenshaw's
+ * recurrence (R18; one fused SpMM per degree with X as a fourth operand:
+ * 12 nnz + 8(n+1) + 32 n w bytes per degree).  Uses the basis buffer as a second
+ * scratch block (ARR_EINVAL in a lean context with p = 0). */
+arr_status eig_set_filter(arr_ctx *c, int32_t kind);
 
 /* ---------------------------------------------------------------- A1 + A2
  * X <- T_d((A - cI)/e) X by the three-term recurrence

@@ -218,6 +218,13 @@ class EigContext:
         self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
         self.d = d
 
+    FILTERS = {"cheb": 0, "interp": 1}
+
+    def eig_set_filter(self, kind: str = "cheb"):
+        """'cheb': T_d of the mapped matrix (default); 'interp': the paper's psi_d
+        (Chebyshev interpolant of max(0,t)^{10d}, see include/arrabit.h)."""
+        self._check(self.lib.eig_set_filter(self.h, self.FILTERS[kind]), "eig_set_filter")
+
     # -- A1/A2
     def filter_step(self, X: torch.Tensor, normalize: bool = True, colnorm: torch.Tensor | None = None):
         px, ld, _ = _blk(X, "X")

@@ -156,6 +156,41 @@ double chebT(int d, double t) {  // host recursion, Eq. cheby-poly
     return r1;
 }
 
+// Chebyshev coefficients of psi_d, the degree-d interpolant of f_d(t) = max(0,t)^{10d}
+// at the Chebyshev points of the second kind: the discrete cosine
+// transform of the node values, a_k = (2/d) sum''_j f_d(t_j) T_k(t_j) (first and last
+// terms halved), then a_0, a_d halved, so that psi_d = sum_k a_k T_k.
+std::vector<double> interp_coef(int d) {
+    std::vector<double> f(d + 1), a(d + 1, 0.0);
+    const double pi = 3.14159265358979323846;
+    for (int j = 0; j <= d; ++j) {
+        const double t = -cos(j * pi / d);
+        f[j] = t > 0.0 ? pow(t, 10.0 * d) : 0.0;
+    }
+    for (int k = 0; k <= d; ++k) {
+        double s = 0.0;
+        for (int j = 0; j <= d; ++j) {
+            const double wj = (j == 0 || j == d) ? 0.5 : 1.0;
+            s += wj * f[j] * cos(k * (pi - j * pi / d));  // T_k(-cos x) = cos(k (pi - x))
+        }
+        a[k] = 2.0 * s / d;
+    }
+    a[0] *= 0.5;
+    a[d] *= 0.5;
+    return a;
+}
+
+// psi_d(t) by Clenshaw's recurrence (host scalar)
+double psi_eval(const std::vector<double> &a, double t) {
+    double b1 = 0.0, b2 = 0.0;
+    for (int k = (int)a.size() - 1; k >= 1; --k) {
+        const double b0 = a[k] + 2.0 * t * b1 - b2;
+        b2 = b1;
+        b1 = b0;
+    }
+    return a[0] + t * b1 - b2;
+}
+
 // ---------------------------------------------------------------- distributed building blocks
 inline bool is_dist(const arr_ctx *c) { return c->nranks > 1; }
 
@@ -215,7 +250,60 @@ arr_status colnorm_x(arr_ctx *c, const double *partials, int nblk, int w, double
 
 // ---------------------------------------------------------------- pieces
 // Filter degrees; result left in X (normalised) -- no host sync.
+// rho_d(A) X with the paper's interpolant psi_d (eig_set_filter kind 1), by Clenshaw's
+// recurrence in the Chebyshev basis with S = c_1 A + c_0 I (c_0 = (a+b)/(a-b),
+// c_1 = 2/(b-a), Alg. poly; R18): b_k = a_k X + 2 S b_{k+1} - b_{k+2},
+// result a_0 X + S b_1 - b_2.  One fused SpMM per degree (the a_k X term is the kernel's
+// fourth operand); X stays intact; b_k ping-pongs between two scratch blocks with b_k
+// overwriting b_{k+2} in place.  Result (normalised) in X.
+arr_status filter_interp(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
+    const double c0 = (c->a + c->b) / (c->a - c->b), c1 = 2.0 / (c->b - c->a);
+    const std::vector<double> &a = c->coef;
+    const int d = (int)a.size() - 1;
+    const int w = c->w;
+    double *buf[2];
+    int64_t ldb[2];
+    if (c->T) { buf[0] = c->T; ldb[0] = ldT(c); buf[1] = c->Q; ldb[1] = ldQ(c); }
+    else { buf[0] = c->Q; ldb[0] = ldQ(c); buf[1] = c->Q + w; ldb[1] = ldQ(c); }
+    int nblk = 0;
+    const int ev0 = t_mark(c);
+    for (int k = d - 1; k >= 0; --k) {
+        SpmmArgs s{};
+        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+        s.n = c->A.n; s.w = w;
+        // S y = c_1 (A y + (c_0/c_1) y): alpha * (A y - shift * y) with shift = -c_0/c_1
+        s.shift = -c0 / c1;
+        s.alpha = (k == 0 ? 1.0 : 2.0) * c1;
+        double gx = a[k];
+        if (k == d - 1) { s.Yin = X; s.ld_in = ldx; s.alpha *= a[d]; }  // b_d = a_d X
+        else { s.Yin = buf[(k + 1) & 1]; s.ld_in = ldb[(k + 1) & 1]; }
+        if (k + 2 == d) gx -= a[d];  // - b_d = - a_d X folds into the X term
+        else if (k + 2 < d) { s.Yprev = buf[k & 1]; s.ld_prev = ldb[k & 1]; s.beta = -1.0; }
+        s.Xa = X; s.ld_xa = ldx; s.gxa = gx;
+        s.Yout = buf[k & 1]; s.ld_out = ldb[k & 1];
+        s.partials = (normalize && k == 0) ? c->part : nullptr;
+        arr_status st;
+        const int g = spmm_x(c, s, &st);
+        if (st != ARR_OK) return st;
+        if (g < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
+        nblk = g;
+    }
+    t_add(c, 0, ev0, t_mark(c), d);
+    CHECK_LAUNCH();
+    if (normalize) {
+        double *nrm = colnorm_dev ? colnorm_dev : NORM_buf(c);
+        ST_TRY(colnorm_x(c, c->part, nblk, w, nrm, nullptr));
+        launch_check_norms(c, nrm, w, c->dinfo + INFO_BAD);
+        launch_scale_cols(c, buf[0], ldb[0], X, ldx, c->A.n, w, nrm);
+    } else {
+        launch_copy_rows(c, buf[0], ldb[0], X, ldx, c->A.n, w);
+    }
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
 arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
+    if (c->filter_kind == 1) return filter_interp(c, X, ldx, normalize, colnorm_dev);
     const double cc = 0.5 * (c->a + c->b), e = 0.5 * (c->b - c->a);
     const int w = c->w;
     double *T = c->T ? c->T : c->Q;  // lean context: the basis block Q[:, 0:w] is free during sweeps
@@ -725,6 +813,17 @@ arr_status eig_set_degree(arr_ctx *c, int32_t d) {
     GUARD(c);
     if (d < 1) return fail(c, ARR_EINVAL, "degree must be >= 1");
     c->d = d;
+    if (c->filter_kind == 1) c->coef = interp_coef(d);
+    return ARR_OK;
+}
+
+arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
+    GUARD(c);
+    if (kind != 0 && kind != 1) return fail(c, ARR_EINVAL, "filter kind must be 0 (T_d) or 1 (psi_d)");
+    if (kind == 1 && !c->T && c->p < 1)
+        return fail(c, ARR_EINVAL, "the interpolant filter needs two scratch blocks (p >= 1 in a lean context)");
+    c->filter_kind = kind;
+    c->coef = kind == 1 ? interp_coef(c->d) : std::vector<double>();
     return ARR_OK;
 }
 
@@ -868,7 +967,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         if ((st = eig_set_interval(c, a, b)) != ARR_OK) return st;
         // sweeps between ARR steps: dynamic-range rule (R6)
         const double cc = 0.5 * (a + b), e = 0.5 * (b - a);
-        const double amp = fabs(chebT(c->d, (mu1 - cc) / e));
+        const double amp = fabs(c->filter_kind == 1 ? psi_eval(c->coef, (mu1 - cc) / e) : chebT(c->d, (mu1 - cc) / e));
         int s = opts->s_max;
         if (amp > 1.0) {
             if (!isfinite(amp)) s = 1;

@@ -40,6 +40,9 @@ struct arr_ctx {
     int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
     int tile_rows;    // SpMM rows per tile in natural order (1..64; env ARRABIT_TILE)
     int col_split;    // column vectors per SpMM thread (1 default; env ARRABIT_SPLIT, tuning)
+    // polynomial filter (eig_set_filter): 0 = T_d, 1 = psi_d (Chebyshev coefficients coef[0..d])
+    int filter_kind;
+    std::vector<double> coef;
     // interval
     double a, b;
     bool have_interval;
@@ -104,6 +107,9 @@ struct SpmmArgs {
     int64_t ld_out;
     double alpha, shift, beta;
     const double *colshift;  // per-column shift (overrides shift) or nullptr
+    const double *Xa;        // optional fourth operand: Yout += gxa * Xa (interpolant filter), or nullptr
+    int64_t ld_xa;
+    double gxa;
     double *partials;        // [gridDim.x * w] column sums of squares of the output, or nullptr
     unsigned long long *sched;  // [2] dynamic tile ticket + finished-CTA count (self-resetting)
     const int64_t *tile_row0;   // optional processing order: tile t = rows [tile_row0[t], +tile_len[t])

@@ -193,7 +193,7 @@ struct __align__(16) Ent {
 
 // Epilogue of one row: out = alpha*(acc - shift*y_i) + beta*y_prev, column
 // sums of squares, evict-first store.
-template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
 __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int TX, int v0, int wv,
                                              const typename Vec<VEC>::T (&acc)[NV],
                                              const typename Vec<VEC>::T (&yp)[NV], double (&ss)[NV][VEC],
@@ -205,12 +205,14 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
         const int vv = v0 + v * TX;
         if (vv >= wv) continue;
         const T yi = V::ldg(a.Yin + i * a.ld_in + vv * VEC);
+        const T xa = HAS_X ? STREAM_LD(a.Xa + i * a.ld_xa + vv * VEC) : V::zero();
         T out;
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
             double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
             if (HAS_PREV) o += a.beta * V::get(yp[v], e);
+            if (HAS_X) o += a.gxa * V::get(xa, e);
             V::set(out, e, o);
             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
         }
@@ -224,7 +226,7 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
 // from shared memory and K FMAs run in CSR order.  Slots past the row end
 // re-gather the row's first entry with value 0 (no branches).  When every row
 // fits one chunk (K >= longest row) two rows are kept in flight per thread.
-template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
 __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nrows, int R, int RR, int r, int TX,
                                           int v0, int wv, const int *s_rp, const Ent *s_ent,
                                           double (&ss)[NV][VEC], uint64_t pol_keep, uint64_t pol_stream) {
@@ -273,8 +275,8 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
                 fma_vec<VEC>(acc1[0], a1, x1[u]);
             }
             if (v0 < wv) {
-                row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i0, TX, v0, wv, acc0, yp0, ss, pol_stream);
-                if (has1) row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i1, TX, v0, wv, acc1, yp1, ss, pol_stream);
+                row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>(a, i0, TX, v0, wv, acc0, yp0, ss, pol_stream);
+                if (has1) row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>(a, i1, TX, v0, wv, acc1, yp1, ss, pol_stream);
             }
         }
     } else {
@@ -327,7 +329,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
                     for (int v = 0; v < NV; ++v) fma_vec<VEC>(acc[v], av, x[u][v]);
                 }
             }
-            row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, i, TX, v0, wv, acc, yp, ss, pol_stream);
+            row_epilogue<VEC, NV, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>(a, i, TX, v0, wv, acc, yp, ss, pol_stream);
         }
     }
 }
@@ -345,7 +347,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
 // in CSR order, so results do not depend on the partition or the tiling.
 // A tile whose slice exceeds the staging capacity is staged in several passes
 // of whole rows.
-template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
 __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
                                                                     int64_t ntiles, int nnz_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -433,6 +435,7 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
                             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
                             double o = a.alpha * (V::get(acc, e) - sh * V::get(yi, e));
                             if (HAS_PREV) o += a.beta * V::get(yp, e);
+                            if (HAS_X) o += a.gxa * a.Xa[i * a.ld_xa + vv * VEC + e];
                             V::set(out, e, o);
                             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                         }
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
             }
             __syncthreads();
             if (active)
-                tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
+                tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>(a, r0 + done, cnt, R, RR, r, TX, v0, wv,
                                                                         s_rp, s_ent, ss, pol_keep, pol_stream);
             done += cnt;
         }
@@ -523,7 +526,7 @@ struct WsInfo {
 // range's row pointers and {col*ld, val} entries into one of two shared-memory
 // stages while the consumer warps compute the other: the CSR round trips of the
 // next tile are hidden behind the current one.
-template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
 __global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
                                                                       int64_t ntiles, int nnz_cap, int ncons) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a
             const int *s_rp = reinterpret_cast<const int *>(smem_raw + st * stage_bytes + sizeof(Ent) * nnz_cap);
             if (info.mode == 0) {
                 if (active)
-                    tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>(a, info.r0, info.nrows, R, 0, r, TX, v0, wv,
+                    tile_rows<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>(a, info.r0, info.nrows, R, 0, r, TX, v0, wv,
                                                                             s_rp, s_ent, ss, pol_keep, pol_stream);
             } else if (active && r == 0) {
                 // one row longer than a stage: CSR order straight from global memory
@@ -661,6 +664,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a
                         const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
                         double o = a.alpha * (Vv::get(acc, e) - sh * Vv::get(yi, e));
                         if (HAS_PREV) o += a.beta * Vv::get(yp, e);
+                        if (HAS_X) o += a.gxa * a.Xa[i * a.ld_xa + vv * VEC + e];
                         Vv::set(out, e, o);
                         if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                     }
@@ -697,14 +701,14 @@ __global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a
     }
 }
 
-template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT>
+template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
 int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
 #if ARR_SPMM_WS
     // warp-specialised kernel where it measured faster on B200: >= 4 rows in flight per
     // CTA and single-chunk rows (cfg2: 116 -> 105 us); slower for R = 1 (cfg3, w = 550) and
     // for 27-point rows (cfg5), which keep spmm_tile_kernel
     if (R >= 4 && K <= 7) {
-        auto kern = spmm_ws_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
+        auto kern = spmm_ws_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>;
         const int ncons = ((R * TX + 31) / 32) * 32;
         const int RT = c->tile_rows;
         const size_t stage = ((sizeof(Ent) * (size_t)kWsCap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
@@ -729,7 +733,7 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
         return (int)G;
     }
 #endif
-    auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT>;
+    auto kern = spmm_tile_kernel<VEC, NV, K, HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>;
     const int nthr = ((R * TX + 31) / 32) * 32;
     const int RT = c->tile_rows;  // rows per tile in natural order (<= kTile)
     // smem: staged slice + relative row pointers; reused by the SUMSQ reduction
@@ -757,12 +761,19 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
 template <int VEC, int NV, int K>
 int dispatch_flags(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     const bool prev = a.Yprev != nullptr, store = a.Yout != nullptr, ss = a.partials != nullptr,
-               cs = a.colshift != nullptr;
-    if (prev && store && !ss && !cs) return launch_t<VEC, NV, K, true, true, false, false>(c, a, TX, R, wv);
-    if (prev && store && ss && !cs) return launch_t<VEC, NV, K, true, true, true, false>(c, a, TX, R, wv);
-    if (!prev && store && !ss && !cs) return launch_t<VEC, NV, K, false, true, false, false>(c, a, TX, R, wv);
-    if (!prev && store && ss && !cs) return launch_t<VEC, NV, K, false, true, true, false>(c, a, TX, R, wv);
-    if (!prev && !store && ss && cs) return launch_t<VEC, NV, K, false, false, true, true>(c, a, TX, R, wv);
+               cs = a.colshift != nullptr, xa = a.Xa != nullptr;
+    if (!xa) {
+        if (prev && store && !ss && !cs) return launch_t<VEC, NV, K, true, true, false, false, false>(c, a, TX, R, wv);
+        if (prev && store && ss && !cs) return launch_t<VEC, NV, K, true, true, true, false, false>(c, a, TX, R, wv);
+        if (!prev && store && !ss && !cs) return launch_t<VEC, NV, K, false, true, false, false, false>(c, a, TX, R, wv);
+        if (!prev && store && ss && !cs) return launch_t<VEC, NV, K, false, true, true, false, false>(c, a, TX, R, wv);
+        if (!prev && !store && ss && cs) return launch_t<VEC, NV, K, false, false, true, true, false>(c, a, TX, R, wv);
+    } else if (store && !cs) {  // the interpolant filter's Clenshaw steps (b_k = a_k X + 2 S b_{k+1} - b_{k+2})
+        if (prev && !ss) return launch_t<VEC, NV, K, true, true, false, false, true>(c, a, TX, R, wv);
+        if (prev && ss) return launch_t<VEC, NV, K, true, true, true, false, true>(c, a, TX, R, wv);
+        if (!prev && !ss) return launch_t<VEC, NV, K, false, true, false, false, true>(c, a, TX, R, wv);
+        if (!prev && ss) return launch_t<VEC, NV, K, false, true, true, false, true>(c, a, TX, R, wv);
+    }
     return -1;
 }
 
@@ -919,11 +930,13 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     bool v2 = (a.w % 2 == 0) && vec2_ok(a.Yin, a.ld_in);
     if (a.Yprev) v2 = v2 && vec2_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
+    if (a.Xa) v2 = v2 && vec2_ok(a.Xa, a.ld_xa);
     c->spmm_blocks++;
 #if ARR_SPMM_V4
     bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
     if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);
     if (a.Yout) v4 = v4 && vec4_ok(a.Yout, a.ld_out);
+    if (a.Xa) v4 = v4 && vec4_ok(a.Xa, a.ld_xa);
     if (v4) return dispatch_nv<4>(c, a);
 #endif
     return v2 ? dispatch_nv<2>(c, a) : dispatch_nv<1>(c, a);

@@ -370,3 +370,40 @@ def test_cfg2_full_filter_and_arr_vs_oracle(arr):
     res = ctx.residuals(Y[:, :spec.k], ritz[:spec.k])
     res_o = oracle.residuals(A, host(Y)[:, :spec.k], ritz[:spec.k])
     assert np.max(np.abs(res - res_o)) <= 1e-12 * max(1.0, res_o.max())
+
+
+@pytest.mark.parametrize("kind", list(SMALL))
+@pytest.mark.parametrize("d", [1, 2, 7, 20])
+def test_interp_filter_step_vs_oracle(arr, kind, d):
+    """The paper's interpolant filter rho_d (eig_set_filter 'interp') against the
+    oracle's Clenshaw evaluation (oracle.poly_filter), before and after normalisation."""
+    A = SMALL[kind]()
+    w = 24
+    X0 = synth.gaussian_block(A.n, w, 13)
+    ctx = arr.eig_init(arr.to_device_csr(A), w, 1, d)
+    ctx.eig_set_filter("interp")
+    a = ctx.eig_gershgorin_lower()
+    b = a + 0.6 * (2 * float(np.abs(A.val).max()) * 2 - a)
+    ctx.eig_set_interval(a, b)
+    coef = oracle.interp_coeffs(d)
+    ref = oracle.poly_filter(A, a, b, coef, X0)
+    Xd = dev_block(X0, ld=w + 2)
+    ctx.filter_step(Xd, normalize=False)
+    assert relF(host(Xd), ref) <= 1e-12
+    Xd = dev_block(X0)
+    ctx.filter_step(Xd, normalize=True)
+    assert relF(host(Xd), oracle.poly_sweep(A, a, b, coef, X0)) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "st27", "zipf"])
+def test_solve_with_interp_filter(arr, kind):
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    ctx.eig_set_filter("interp")
+    Xd = dev_block(X0)
+    ev, res, info = ctx.eig_solve(Xd, tol=spec.tol)
+    assert info.converged == 1 and np.all(res <= spec.tol)
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
