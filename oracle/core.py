@@ -331,9 +331,9 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
         if maxres <= tol:
             return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log)
         # b := mu_{w+1}, an under-estimate of lambda_{k+q} (mu_{w+1} <= lambda_{w+1} by
-        # interlacing); once the max residual has grown between two outer
-        # iterations (b fell and amplified the guard range), b only increases (R3)
-        mono = mono or (prev_maxres is not None and maxres > prev_maxres)
+        # interlacing); once the max residual has grown tenfold between two
+        # outer iterations (b fell and amplified the guard range), b only increases (R3)
+        mono = mono or (prev_maxres is not None and maxres > 10.0 * prev_maxres)
         prev_maxres = maxres
         bn = float(mu[min(w, r - 1)])
         b = max(b, bn) if mono else bn

@@ -989,8 +989,8 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         inf.a = a; inf.b = b;
         if (maxres <= opts->tol) { done = true; break; }  // Eq. out-stop
         // b = mu_{w+1}, an under-estimate of lambda_{k+q} (interlacing); once
-        // the max residual has grown between two outer iterations, b only increases (R3)
-        mono = mono || (outer > 1 && maxres > prev_maxres);
+        // the max residual has grown tenfold between two outer iterations, b only increases (R3)
+        mono = mono || (outer > 1 && maxres > 10.0 * prev_maxres);
         prev_maxres = maxres;
         const double bn = ritz[std::min(w, m - 1)];
         b = mono ? std::max(b, bn) : bn;

@@ -69,7 +69,7 @@ def main():
               f"mu1={ritz[0]:.10g} mu_k={ritz[k - 1]:.10g}  filter {t2 - t1:.2f} s, arr {t3 - t2:.2f} s", flush=True)
         if res.max() <= spec.tol:
             break
-        mono = mono or (outer > 1 and res.max() > prev)
+        mono = mono or (outer > 1 and res.max() > 10 * prev)
         prev = res.max()
         bn = ritz[min(w, len(ritz) - 1)]
         b, mu1 = (max(b, bn) if mono else bn), ritz[0]
