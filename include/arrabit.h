@@ -184,6 +184,14 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b);
 arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles);
 /* Change the degree d used by filter_step (1 <= d). */
 arr_status eig_set_degree(arr_ctx *c, int32_t d);
+/* Which end of the spectrum: smallest = 0 (default): the k algebraically largest
+ * eigenpairs; smallest != 0: the k algebraically smallest (the paper's
+ * second mode, Table 6) by running the whole method on -A.  In that mode the
+ * interval calls (eig_gershgorin_lower, eig_set_interval, the filter) refer to the
+ * spectrum of -A, while eigenvalues and Ritz values returned by eig_solve /
+ * arr_project and mu passed to residuals are those of A (ascending: smallest first).
+ * Clears the interval. */
+arr_status eig_set_mode(arr_ctx *c, int32_t smallest);
 /* Polynomial of filter_step / eig_solve: kind 0 = the classic Chebyshev polynomial
  * T_d of the mapped matrix (default, Eq. cheby-poly); kind 1 = the
  * paper's default filter rho_d(t) = psi_d((2t - a - b)/(b - a)), psi_d the degree-d

@@ -218,6 +218,10 @@ class EigContext:
         self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
         self.d = d
 
+    def eig_set_mode(self, which: str = "largest"):
+        """'largest' (default) or 'smallest' k eigenpairs (see include/arrabit.h)."""
+        self._check(self.lib.eig_set_mode(self.h, 1 if which == "smallest" else 0), "eig_set_mode")
+
     FILTERS = {"cheb": 0, "interp": 1}
 
     def eig_set_filter(self, kind: str = "cheb"):

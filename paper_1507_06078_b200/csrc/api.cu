@@ -201,6 +201,10 @@ inline bool is_dist(const arr_ctx *c) { return c->nranks > 1; }
 // not supported).
 int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st) {
     *st = ARR_OK;
+    if (c->sign < 0) {  // the solver's operator is -A: alpha (-A y - shift y) = (-alpha) (A y + shift y)
+        s.alpha = -s.alpha;
+        s.shift = -s.shift;
+    }
     if (!is_dist(c)) return launch_spmm(c, s);
     DistPlan &P = c->plan;
     if ((*st = comm_halo_begin(c, s.Yin, s.ld_in, s.w)) != ARR_OK) return 0;
@@ -576,7 +580,9 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
 arr_status residuals_core(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_host, int ncols,
                           double *res_host) {
     double *shift = SHIFT_buf(c), *out = NORM_buf(c);
-    memcpy(c->h_stage, mu_host, sizeof(double) * ncols);
+    // mu_host: Ritz values of the solver's operator sign*A; the kernel applies A with
+    // alpha = sign, so the per-column shift is sign*mu (the norm is unchanged)
+    for (int i = 0; i < ncols; ++i) c->h_stage[i] = c->sign * mu_host[i];
     CUDA_TRY(cudaMemcpyAsync(shift, c->h_stage, sizeof(double) * ncols, cudaMemcpyHostToDevice, c->stream));
     const int ev0 = t_mark(c);
     SpmmArgs s{};
@@ -697,6 +703,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         return ARR_ENOMEM;
     }
     c->orth_mode = getenv("ARRABIT_ORTH_SVQB") ? 1 : 0;
+    c->sign = 1;
     c->tile_rows = 32;  // measured best on B200 for cfg2 (with the L2 prefetch) and cfg3 natural order
     if (const char *tr = getenv("ARRABIT_TILE")) c->tile_rows = std::min(64, std::max(1, atoi(tr)));
     c->col_split = 1;
@@ -817,6 +824,13 @@ arr_status eig_set_degree(arr_ctx *c, int32_t d) {
     return ARR_OK;
 }
 
+arr_status eig_set_mode(arr_ctx *c, int32_t smallest) {
+    GUARD(c);
+    c->sign = smallest ? -1 : 1;
+    c->have_interval = false;  // an interval of A is not one of -A
+    return ARR_OK;
+}
+
 arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
     GUARD(c);
     if (kind != 0 && kind != 1) return fail(c, ARR_EINVAL, "filter kind must be 0 (T_d) or 1 (psi_d)");
@@ -926,7 +940,10 @@ arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx
         return fail(c, ARR_EINVAL, "bad arr_project args");
     if (!c->T && p_use > 0 && (Y != X || ldy != ldx))
         return fail(c, ARR_EINVAL, "lean context (no scratch block): arr_project with p > 0 needs Y == X");
-    return arr_core(c, p_use, X, ldx, Y, ldy, ritz_host, rank);
+    arr_status st = arr_core(c, p_use, X, ldx, Y, ldy, ritz_host, rank);
+    if (st == ARR_OK && c->sign < 0)
+        for (int i = 0; i < (p_use + 1) * c->w; ++i) ritz_host[i] = -ritz_host[i];  // eigenvalues of A, ascending
+    return st;
 }
 
 arr_status arr_project(arr_ctx *c, const double *X, int64_t ldx, double *Y, int64_t ldy, double *ritz_host,
@@ -940,7 +957,10 @@ arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_
     GUARD(c);
     if (!block_ok(Y, ldy, ncols) || ncols > std::max(m_of(c, c->p), ARR_MAX_W) || !mu_host || !res_host)
         return fail(c, ARR_EINVAL, "bad residual args");
-    return residuals_core(c, Y, ldy, mu_host, ncols, res_host);
+    if (c->sign > 0) return residuals_core(c, Y, ldy, mu_host, ncols, res_host);
+    std::vector<double> mu(mu_host, mu_host + ncols);  // eigenvalues of A -> of the operator -A
+    for (auto &x : mu) x = -x;
+    return residuals_core(c, Y, ldy, mu.data(), ncols, res_host);
 }
 
 arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts, double *eigval_host,
@@ -999,7 +1019,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
     }
     inf.converged = done ? 1 : 0;
     inf.spmm_blocks = c->spmm_blocks - spmm0;
-    for (int i = 0; i < k; ++i) { eigval_host[i] = ritz[i]; res_host[i] = res[i]; }
+    for (int i = 0; i < k; ++i) { eigval_host[i] = c->sign * ritz[i]; res_host[i] = res[i]; }
     if (info) *info = inf;
     return ARR_OK;
 }

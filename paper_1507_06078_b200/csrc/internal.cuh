@@ -40,6 +40,8 @@ struct arr_ctx {
     int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
     int tile_rows;    // SpMM rows per tile in natural order (1..64; env ARRABIT_TILE)
     int col_split;    // column vectors per SpMM thread (1 default; env ARRABIT_SPLIT, tuning)
+    // eig_set_mode: +1 = k largest eigenpairs of A, -1 = k smallest (the solver runs on -A)
+    int sign;
     // polynomial filter (eig_set_filter): 0 = T_d, 1 = psi_d (Chebyshev coefficients coef[0..d])
     int filter_kind;
     std::vector<double> coef;

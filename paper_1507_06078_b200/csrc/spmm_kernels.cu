@@ -854,7 +854,8 @@ __global__ void scale_cols_kernel(const double *In, int64_t ld_in, double *Out, 
 }
 
 __global__ void gershgorin_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                  const double *__restrict__ val, int64_t n, double *__restrict__ part) {
+                                  const double *__restrict__ val, int64_t n, double sign, double *__restrict__ part) {
+    // min_i (sign*A_ii - sum_{j != i} |A_ij|): the Gershgorin lower bound of sign*A
     double m = INFINITY;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -863,7 +864,7 @@ __global__ void gershgorin_kernel(const int64_t *__restrict__ rp, const int32_t 
             if (col[p] == i) dg += val[p];
             else off += fabs(val[p]);
         }
-        m = fmin(m, dg - off);
+        m = fmin(m, sign * dg - off);
     }
     __shared__ double red[256];
     red[threadIdx.x] = m;
@@ -979,7 +980,7 @@ void launch_gershgorin(arr_ctx *c, double *partial, int *nblk_out) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     gershgorin_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.val, c->A.n,
-                                                              partial);
+                                                              (double)c->sign, partial);
     c->launches++;
     *nblk_out = (int)blocks;
 }

@@ -407,3 +407,43 @@ def test_solve_with_interp_filter(arr, kind):
     assert info.converged == 1 and np.all(res <= spec.tol)
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
     assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "zipf"])
+def test_smallest_mode_solve(arr, kind):
+    """k algebraically smallest eigenpairs (eig_set_mode 'smallest': the method on
+    -A, the paper's second mode, Table 6 P:2161): eigenvalues of A ascending, equal to
+    the dense spectrum; the oracle's solve on -A gives the same values; residual
+    certificates recomputed by the oracle with A itself."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    ctx.eig_set_mode("smallest")
+    Xd = dev_block(X0)
+    ev, res, info = ctx.eig_solve(Xd, tol=spec.tol)
+    assert info.converged == 1 and np.all(res <= spec.tol)
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[:spec.k]
+    assert np.all(np.diff(ev) >= 0)
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+    negA = synth.CSR(A.n, A.row_ptr, A.col_idx, -A.val, name="negA")
+    orc = oracle.solve(negA, spec.k, spec.d, spec.p, X0, tol=spec.tol)
+    assert np.max(np.abs(ev + orc.mu) / np.maximum(1, np.abs(ev))) < 1e-10
+    cert = oracle.residuals(A, host(Xd)[:, :spec.k], ev)
+    assert np.all(cert <= 1.01 * spec.tol)
+
+
+def test_smallest_mode_bipartite_symmetry(arr):
+    """2-D Dirichlet Laplacian (diagonal 4, bipartite): the spectrum is symmetric about
+    4, so the k smallest are 8 - (the k largest) (SURVEY.md §8c-4 #5)."""
+    spec = configs.SMALL_ANALOGS["lap2d"]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    out = {}
+    for mode in ("largest", "smallest"):
+        ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+        ctx.eig_set_mode(mode)
+        ev, _, info = ctx.eig_solve(dev_block(X0), tol=spec.tol)
+        assert info.converged == 1
+        out[mode] = ev
+    np.testing.assert_allclose(out["smallest"], 8.0 - out["largest"], rtol=0, atol=1e-10 * 8)

@@ -68,3 +68,16 @@ def test_solve_small_zipf_dense():
     r = oracle.solve(A, spec.k, spec.d, spec.p, synth.starting_block(spec))
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1]
     _check(r, lam, spec.k)
+
+
+def test_solve_smallest_via_negated_matrix_1d_closed_form():
+    """The paper's second mode (k smallest, Table 6 P:2161) = the k largest of -A;
+    1-D Laplacian closed form lambda_j = 2 - 2 cos(j pi / (n+1)), j = 1..k."""
+    n, k = 300, 8
+    A = synth.laplacian_1d(n)
+    negA = synth.CSR(A.n, A.row_ptr, A.col_idx, -A.val, name="negA")
+    X0 = synth.gaussian_block(n, k + 1, 3)
+    r = oracle.solve(negA, k, 10, 1, X0, tol=1e-10, w=k + 1)
+    lam = 2 - 2 * np.cos(np.arange(1, k + 1) * np.pi / (n + 1))
+    assert r.converged
+    np.testing.assert_allclose(-r.mu, lam, rtol=1e-10)
