@@ -115,6 +115,10 @@ typedef struct {
     double tol;      /* outer stop: max_i res_i <= tol (Eq. out-stop)   */
     int32_t maxit;   /* maximum outer iterations                        */
     int32_t s_max;   /* cap of the sweeps-per-ARR rule (R6)                 */
+    int32_t exits;   /* the paper's extra stop rules, a bit mask, 0 = off
+                        (R10): 1 = (ii) max res not reduced over three
+                        consecutive outer iterations; 2 = (iii) max res < (1 + 9h/k) tol,
+                        h = #{res_i < 0.1 tol}                                       */
 } arr_solve_opts;
 
 typedef struct {
@@ -125,6 +129,8 @@ typedef struct {
     double maxres;       /* final max_i res_i                                     */
     double a, b;         /* final filter interval                                 */
     int64_t spmm_blocks; /* block SpMMs issued (filter degrees + ARR + residuals) */
+    int32_t exit_rule;   /* why the outer loop ended: 1 max res <= tol, 2 rule (ii),
+                            3 rule (iii), 0 maxit                                   */
 } arr_solve_info;
 
 /* ---------------------------------------------------------------- lifecycle

@@ -981,6 +981,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
     if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
     const int64_t spmm0 = c->spmm_blocks;
     bool done = false, mono = false;
+    std::vector<double> best_hist;
     double prev_maxres = 0.0;
     int32_t rank = 0;
     for (int outer = 1; outer <= opts->maxit; ++outer) {
@@ -1007,7 +1008,22 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         inf.maxres = maxres;
         inf.last_rank = rank;
         inf.a = a; inf.b = b;
-        if (maxres <= opts->tol) { done = true; break; }  // Eq. out-stop
+        if (maxres <= opts->tol) { done = true; inf.exit_rule = 1; break; }  // Eq. out-stop
+        // the paper's extra stop rules, opt-in (R10)
+        if (opts->exits & 1) {
+            best_hist.push_back(maxres);
+            const size_t h = best_hist.size();
+            if (h >= 4 && !(best_hist[h - 1] < best_hist[h - 4] || best_hist[h - 2] < best_hist[h - 4] ||
+                            best_hist[h - 3] < best_hist[h - 4])) {
+                inf.exit_rule = 2;  // (ii): not reduced over three consecutive outer iterations
+                break;
+            }
+        }
+        if (opts->exits & 2) {
+            int hsmall = 0;
+            for (int i = 0; i < k; ++i) hsmall += res[i] < 0.1 * opts->tol;
+            if (maxres < (1.0 + 9.0 * hsmall / k) * opts->tol) { inf.exit_rule = 3; break; }  // (iii)
+        }
         // b = mu_{w+1}, an under-estimate of lambda_{k+q} (interlacing); once
         // the max residual has grown tenfold between two outer iterations, b only increases (R3)
         mono = mono || (outer > 1 && maxres > 10.0 * prev_maxres);

@@ -447,3 +447,20 @@ def test_smallest_mode_bipartite_symmetry(arr):
         assert info.converged == 1
         out[mode] = ev
     np.testing.assert_allclose(out["smallest"], 8.0 - out["largest"], rtol=0, atol=1e-10 * 8)
+
+
+def test_paper_exit_rules(arr):
+    """The paper's extra stop rules, opt-in: (ii) stops a solve whose
+    tolerance is out of reach once max res stalls for three outer iterations; (iii),
+    when it fires, leaves max res < 10 tol."""
+    spec = configs.SMALL_ANALOGS["lap2d"]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    ev, res, info = ctx.eig_solve(dev_block(X0), tol=1e-18, maxit=200, exits=1)
+    assert info.exit_rule == 2 and info.outer < 200 and info.converged == 0
+    ev2, res2, info2 = ctx.eig_solve(dev_block(X0), tol=1e-10, maxit=200, exits=2)
+    assert info2.exit_rule in (1, 3)
+    assert res2.max() < 10 * 1e-10
+    ev3, res3, info3 = ctx.eig_solve(dev_block(X0), tol=1e-10, maxit=200, exits=0)
+    assert info3.exit_rule == 1 and info3.outer >= info2.outer
