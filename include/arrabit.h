@@ -119,6 +119,9 @@ typedef struct {
                         (R10): 1 = (ii) max res not reduced over three
                         consecutive outer iterations; 2 = (iii) max res < (1 + 9h/k) tol,
                         h = #{res_i < 0.1 tol}                                       */
+    int32_t inner;   /* sweeps between ARR steps: 0 = the dynamic-range rule (R6),
+                        1 = the paper's rcond rule (check rcond(X^T X) every 5
+                        sweeps, at most 10 times; stop at rc <= tol or rc/rc_prev > 0.99) */
 } arr_solve_opts;
 
 typedef struct {

@@ -606,6 +606,22 @@ arr_status residuals_core(arr_ctx *c, const double *Y, int64_t ldy, const double
     return ARR_OK;
 }
 
+// rc = lambda_min(X^T X) / lambda_max(X^T X) (2-norm reciprocal condition of the Gram;
+// the paper uses LAPACK's 1-norm estimate).  Synchronises.
+arr_status gram_rcond(arr_ctx *c, const double *X, int64_t ldx, double *rc) {
+    const int w = c->w;
+    double *G = G_buf(c), *V = V_buf(c);
+    ST_TRY(gram_x(c, X, ldx, w, X, ldx, w, G, w));
+    CUDA_TRY(cudaMemcpyAsync(V, G, sizeof(double) * (size_t)w * w, cudaMemcpyDeviceToDevice, c->stream));
+    SOLVER_TRY(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, w, V, w, c->evals,
+                                c->solver_work, c->solver_lwork, c->dinfo + INFO_SYEVD));
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage, c->evals, sizeof(double) * w, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const double lmin = c->h_stage[0], lmax = c->h_stage[w - 1];
+    *rc = (lmax > 0.0) ? std::max(lmin, 0.0) / lmax : 0.0;
+    return ARR_OK;
+}
+
 bool block_ok(const double *p, int64_t ld, int ncols) { return p != nullptr && ld >= ncols && ncols >= 1; }
 
 }  // namespace
@@ -995,8 +1011,25 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
             else s = (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
         }
         CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
-        for (int q = 0; q < s; ++q)
-            if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;  // MPM sweep
+        if (opts->inner == 1) {
+            // the paper's inner stop: every maxit_2 = 5 sweeps, at most maxit_1 = 10
+            // times, rc = rcond(X^T X); stop when rc <= tol or rc / rc_prev > 0.99 (rcond taken in the
+            // 2-norm, lambda_min / lambda_max of the Gram: DESIGN.md R6)
+            double rcp = -1.0;
+            s = 0;
+            for (int chk = 0; chk < 10; ++chk) {
+                for (int q = 0; q < 5; ++q)
+                    if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;
+                s += 5;
+                double rc = 0.0;
+                if ((st = gram_rcond(c, X, ldx, &rc)) != ARR_OK) return st;
+                if (rc <= opts->tol || (rcp > 0.0 && rc / rcp > 0.99)) break;
+                rcp = rc;
+            }
+        } else {
+            for (int q = 0; q < s; ++q)
+                if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;  // MPM sweep
+        }
         inf.sweeps += s;
         if ((st = arr_core(c, c->p, X, ldx, X, ldx, ritz.data(), &rank)) != ARR_OK) return st;  // ARR
         CUDA_TRY(cudaMemcpyAsync(c->h_istage + 32, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

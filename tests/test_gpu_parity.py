@@ -464,3 +464,17 @@ def test_paper_exit_rules(arr):
     assert res2.max() < 10 * 1e-10
     ev3, res3, info3 = ctx.eig_solve(dev_block(X0), tol=1e-10, maxit=200, exits=0)
     assert info3.exit_rule == 1 and info3.outer >= info2.outer
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "lap3dV"])
+def test_solve_with_paper_rcond_inner_rule(arr, kind):
+    """The paper's inner stop rule (rcond(X^T X) every 5 sweeps) instead of
+    the dynamic-range rule: the solve still reaches the dense eigenvalues."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    ev, res, info = ctx.eig_solve(dev_block(X0), tol=spec.tol, maxit=100, inner="rcond")
+    assert info.converged == 1 and info.sweeps % 5 == 0
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
