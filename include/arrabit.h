@@ -122,6 +122,10 @@ typedef struct {
     int32_t inner;   /* sweeps between ARR steps: 0 = the dynamic-range rule (R6),
                         1 = the paper's rcond rule (check rcond(X^T X) every 5
                         sweeps, at most 10 times; stop at rc <= tol or rc/rc_prev > 0.99) */
+    int32_t adapt;   /* the paper's adaptive parameters, a bit mask, 0 = fixed p and d:
+                        1 = p starts at 1 and grows by Eq. block up to the
+                        context's p; 2 = d starts at 3 and is re-chosen after every ARR by
+                        Eqs. hat-d / degree, the context's d as d_max      */
 } arr_solve_opts;
 
 typedef struct {
@@ -134,6 +138,8 @@ typedef struct {
     int64_t spmm_blocks; /* block SpMMs issued (filter degrees + ARR + residuals) */
     int32_t exit_rule;   /* why the outer loop ended: 1 max res <= tol, 2 rule (ii),
                             3 rule (iii), 0 maxit                                   */
+    int32_t p_final;     /* augmentation depth of the last ARR                      */
+    int32_t d_final;     /* filter degree of the last sweeps                        */
 } arr_solve_info;
 
 /* ---------------------------------------------------------------- lifecycle

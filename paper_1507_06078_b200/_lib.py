@@ -38,13 +38,14 @@ class arr_dist(ctypes.Structure):
 
 class arr_solve_opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("s_max", ctypes.c_int32),
-                ("exits", ctypes.c_int32), ("inner", ctypes.c_int32)]
+                ("exits", ctypes.c_int32), ("inner", ctypes.c_int32), ("adapt", ctypes.c_int32)]
 
 
 class arr_solve_info(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int32), ("outer", ctypes.c_int32), ("sweeps", ctypes.c_int32),
                 ("last_rank", ctypes.c_int32), ("maxres", ctypes.c_double), ("a", ctypes.c_double),
-                ("b", ctypes.c_double), ("spmm_blocks", ctypes.c_int64), ("exit_rule", ctypes.c_int32)]
+                ("b", ctypes.c_double), ("spmm_blocks", ctypes.c_int64), ("exit_rule", ctypes.c_int32),
+                ("p_final", ctypes.c_int32), ("d_final", ctypes.c_int32)]
 
 
 _lib = None

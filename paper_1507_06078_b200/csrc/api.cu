@@ -998,6 +998,13 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
     const int64_t spmm0 = c->spmm_blocks;
     bool done = false, mono = false;
     std::vector<double> best_hist;
+    // adaptive augmentation depth and degree (Alg. Arrabit2, Eqs. block / hat-d / degree,
+    // P:1418-1456), opt-in: p grows from 1 up to the context's p; d starts at 3 and is
+    // re-chosen after every ARR, capped by the context's d (the paper's d_max)
+    const int p_max = c->p, d_max = c->d;
+    int p_cur = (opts->adapt & 1) ? std::min(1, p_max) : p_max;
+    if ((opts->adapt & 2) && d_max > 3 && (st = eig_set_degree(c, 3)) != ARR_OK) return st;
+    double best_res = INFINITY, best_muk = 0.0, best_muw = 0.0, maxresp = INFINITY;
     double prev_maxres = 0.0;
     int32_t rank = 0;
     for (int outer = 1; outer <= opts->maxit; ++outer) {
@@ -1031,7 +1038,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                 if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;  // MPM sweep
         }
         inf.sweeps += s;
-        if ((st = arr_core(c, c->p, X, ldx, X, ldx, ritz.data(), &rank)) != ARR_OK) return st;  // ARR
+        if ((st = arr_core(c, p_cur, X, ldx, X, ldx, ritz.data(), &rank)) != ARR_OK) return st;  // ARR
         CUDA_TRY(cudaMemcpyAsync(c->h_istage + 32, c->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         if ((st = residuals_core(c, X, ldx, ritz.data(), k, res.data())) != ARR_OK) return st;  // Eq. resi
         if (c->h_istage[32]) return fail(c, ARR_ENUMERIC, "zero or non-finite column norm after filtering");
@@ -1061,11 +1068,37 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         // the max residual has grown tenfold between two outer iterations, b only increases (R3)
         mono = mono || (outer > 1 && maxres > 10.0 * prev_maxres);
         prev_maxres = maxres;
-        const double bn = ritz[std::min(w, m - 1)];
+        const double bn = ritz[std::min(w, m_of(c, p_cur) - 1)];
         b = mono ? std::max(b, bn) : bn;
         mu1 = ritz[0];
         if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+        if (maxres < best_res) { best_res = maxres; best_muk = ritz[k - 1]; best_muw = ritz[w - 1]; }
+        if ((opts->adapt & 1) && p_cur < p_max) {  // Eq. block: small decay and unimpressive progress
+            const double decay = (ritz[w - 1] - a) / (ritz[k - 1] - a);
+            if (decay > 0.95 && maxres / maxresp > 0.1) ++p_cur;
+        }
+        maxresp = maxres;
+        if ((opts->adapt & 2) && d_max > 3) {  // Eqs. hat-d, degree: smallest d >= 3 separating mu*_{k+q} from mu*_k
+            const double cc2 = 0.5 * (a + b), e2 = 0.5 * (b - a);
+            int dn = d_max;
+            for (int dd = 3; dd <= d_max; ++dd) {
+                double rk, rw;
+                if (c->filter_kind == 1) {
+                    const std::vector<double> cf = interp_coef(dd);
+                    rk = psi_eval(cf, (best_muk - cc2) / e2);
+                    rw = psi_eval(cf, (best_muw - cc2) / e2);
+                } else {
+                    rk = chebT(dd, (best_muk - cc2) / e2);
+                    rw = chebT(dd, (best_muw - cc2) / e2);
+                }
+                if (fabs(rw) < 0.9 * fabs(rk)) { dn = dd; break; }
+            }
+            if (dn != c->d && (st = eig_set_degree(c, dn)) != ARR_OK) return st;
+        }
     }
+    inf.p_final = p_cur;
+    inf.d_final = c->d;
+    if ((opts->adapt & 2) && c->d != d_max && (st = eig_set_degree(c, d_max)) != ARR_OK) return st;
     inf.converged = done ? 1 : 0;
     inf.spmm_blocks = c->spmm_blocks - spmm0;
     for (int i = 0; i < k; ++i) { eigval_host[i] = c->sign * ritz[i]; res_host[i] = res[i]; }

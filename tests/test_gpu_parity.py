@@ -478,3 +478,26 @@ def test_solve_with_paper_rcond_inner_rule(arr, kind):
     assert info.converged == 1 and info.sweeps % 5 == 0
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
     assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+
+
+@pytest.mark.parametrize("kind,adapt", [("lap2d", 1), ("lap2d", 2), ("lap3dV", 3), ("zipf", 3)])
+def test_solve_with_adaptive_p_and_d(arr, kind, adapt):
+    """The paper's adaptive augmentation depth (Eq. block) and degree (Eqs. hat-d,
+    degree): the solve reaches the dense eigenvalues; p stays within
+    [1, p_max] and d within [3, d_max]; the context's degree is restored."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    ev, res, info = ctx.eig_solve(dev_block(X0), tol=spec.tol, maxit=200, adapt=adapt)
+    assert info.converged == 1
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+    if adapt & 1:
+        assert 1 <= info.p_final <= spec.p
+    else:
+        assert info.p_final == spec.p
+    if adapt & 2:
+        assert 3 <= info.d_final <= spec.d
+    ev2, _, info2 = ctx.eig_solve(dev_block(X0), tol=spec.tol)  # fixed parameters afterwards
+    assert info2.d_final == spec.d and info2.p_final == spec.p
