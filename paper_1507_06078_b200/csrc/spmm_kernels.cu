@@ -527,7 +527,10 @@ struct WsInfo {
 // stages while the consumer warps compute the other: the CSR round trips of the
 // next tile are hidden behind the current one.
 template <int VEC, int NV, int K, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
-__global__ void __launch_bounds__(kMaxThreads + 32, 2) spmm_ws_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
+#ifndef ARR_SPMM_WS_MINB
+#define ARR_SPMM_WS_MINB 2
+#endif
+__global__ void __launch_bounds__(kMaxThreads + 32, ARR_SPMM_WS_MINB) spmm_ws_kernel(SpmmArgs a, int TX, int R, int RT, int wv,
                                                                       int64_t ntiles, int nnz_cap, int ncons) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const size_t stage_bytes = ((sizeof(Ent) * (size_t)nnz_cap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
