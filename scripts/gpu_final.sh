@@ -1,10 +1,10 @@
 #!/bin/bash
+# Round 1 final validation of the committed tree: all GPU tests, smoke, the default bench line.
 set -x
-O=gpurun_out/final4
+O=gpurun_out/final5
 mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "adaptive" > $O/pytest_adapt.log 2>&1; echo "exit $?" >> $O/pytest_adapt.log
-for lib in build/libarrabit_*.so; do
-  echo "== $lib" >> $O/ws3.log
-  ARRABIT_LIB=$PWD/$lib timeout 400 python scripts/profile_step.py --config 2 --filter-only --reps 5 --tiles 16 32 64 2>&1 | grep "filter degree" >> $O/ws3.log
-done
+timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
 echo done
