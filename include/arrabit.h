@@ -125,7 +125,9 @@ typedef struct {
     int32_t adapt;   /* the paper's adaptive parameters, a bit mask, 0 = fixed p and d:
                         1 = p starts at 1 and grows by Eq. block up to the
                         context's p; 2 = d starts at 3 and is re-chosen after every ARR by
-                        Eqs. hat-d / degree, the context's d as d_max      */
+                        Eqs. hat-d / degree, the context's d as d_max;
+                        4 = continuation + deflation (locking) of converged pairs, the
+                        paper's b update at continuation (R19)   */
 } arr_solve_opts;
 
 typedef struct {
@@ -140,6 +142,7 @@ typedef struct {
                             3 rule (iii), 0 maxit                                   */
     int32_t p_final;     /* augmentation depth of the last ARR                      */
     int32_t d_final;     /* filter degree of the last sweeps                        */
+    int32_t locked;      /* pairs locked by deflation (adapt bit 4)                 */
 } arr_solve_info;
 
 /* ---------------------------------------------------------------- lifecycle

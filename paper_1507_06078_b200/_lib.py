@@ -45,7 +45,7 @@ class arr_solve_info(ctypes.Structure):
     _fields_ = [("converged", ctypes.c_int32), ("outer", ctypes.c_int32), ("sweeps", ctypes.c_int32),
                 ("last_rank", ctypes.c_int32), ("maxres", ctypes.c_double), ("a", ctypes.c_double),
                 ("b", ctypes.c_double), ("spmm_blocks", ctypes.c_int64), ("exit_rule", ctypes.c_int32),
-                ("p_final", ctypes.c_int32), ("d_final", ctypes.c_int32)]
+                ("p_final", ctypes.c_int32), ("d_final", ctypes.c_int32), ("locked", ctypes.c_int32)]
 
 
 _lib = None

@@ -626,6 +626,97 @@ bool block_ok(const double *p, int64_t ld, int ncols) { return p != nullptr && l
 
 }  // namespace
 
+// Alg. Arrabit2 with continuation and deflation, MPM inner
+// solver, the dynamic-range sweeps rule (R6), fixed p and d (R19):
+//   tol_1 = sqrt(tol) (so that every locked pair meets tol), tol_{t+1} = max(1e-2 tol_t, tol)
+//   once max res <= tol_t, and then b = mu_{k+q}; after every ARR the leading
+//   Ritz pairs with res <= max(1e-14, tol_t^2) (Eq. defl) are locked: they stay in the
+//   leading columns of X (Q_c) and leave the iteration; the remaining w - n_c columns are
+//   filtered, projected against Q_c (X = X - Q_c Q_c^T X, twice) and augmented-RR'ed on
+//   their own (the context runs at width w - n_c); a final Rayleigh-Ritz on all w
+//   columns orders the pairs and recomputes every residual.
+arr_status solve_deflate(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts, double *eigval_host,
+                         double *res_host, arr_solve_info *info) {
+    const int w = c->w, k = c->k, p = c->p;
+    arr_solve_info inf{};
+    double a = 0.0;
+    arr_status st = eig_gershgorin_lower(c, &a);
+    if (st != ARR_OK) return st;
+    std::vector<double> r0(w), ritz((size_t)(p + 1) * w), res(k, 0.0), locked_res;
+    if ((st = arr_core(c, 0, X, ldx, nullptr, 0, r0.data(), nullptr)) != ARR_OK) return st;
+    double b = r0[w - 1], mu1 = r0[0];
+    if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    double tol_t = std::max(opts->tol, sqrt(opts->tol));
+    int nc = 0;  // locked columns X[:, :nc]
+    int32_t rank = 0;
+    const int64_t spmm0 = c->spmm_blocks;
+    bool done = false;
+    auto restore = [&]() { c->w = w; };
+    for (int outer = 1; outer <= opts->maxit; ++outer) {
+        const int wa = w - nc;
+        double *Xa = X + nc;
+        c->w = wa;  // the active block (buffers are sized for w; every ld derived from c->w fits)
+        if ((st = eig_set_interval(c, a, b)) != ARR_OK) { restore(); return st; }
+        const double cc = 0.5 * (a + b), e = 0.5 * (b - a);
+        const double amp = fabs(c->filter_kind == 1 ? psi_eval(c->coef, (mu1 - cc) / e) : chebT(c->d, (mu1 - cc) / e));
+        int s = opts->s_max;
+        if (amp > 1.0) s = !isfinite(amp) ? 1 : (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
+        CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
+        for (int q = 0; q < s; ++q)
+            if ((st = filter_core(c, Xa, ldx, 1, nullptr)) != ARR_OK) { restore(); return st; }
+        inf.sweeps += s;
+        if (nc > 0) {  // X = X - Q_c (Q_c^T X), twice
+            for (int pass = 0; pass < 2; ++pass) {
+                if ((st = gram_x(c, X, ldx, nc, Xa, ldx, wa, G_buf(c), wa)) != ARR_OK) { restore(); return st; }
+                launch_gemm(c, -1.0, X, ldx, nc, G_buf(c), wa, wa, 1.0, Xa, ldx, Xa, ldx, c->A.n);
+            }
+            CUDA_TRY(cudaGetLastError());
+        }
+        if ((st = arr_core(c, p, Xa, ldx, Xa, ldx, ritz.data(), &rank)) != ARR_OK) { restore(); return st; }
+        const int ka = k - nc;
+        std::vector<double> ra(ka);
+        if ((st = residuals_core(c, Xa, ldx, ritz.data(), ka, ra.data())) != ARR_OK) { restore(); return st; }
+        double maxres = 0.0;
+        for (int i = 0; i < ka; ++i) { res[nc + i] = ra[i]; maxres = std::max(maxres, ra[i]); }
+        for (int i = 0; i < nc; ++i) maxres = std::max(maxres, locked_res[i]);
+        inf.outer = outer;
+        inf.maxres = maxres;
+        inf.last_rank = rank;
+        inf.a = a; inf.b = b;
+        restore();
+        if (maxres <= opts->tol) { done = true; inf.exit_rule = 1; break; }
+        if (maxres <= tol_t) {  // continuation (Eq. contin; b update P:1516)
+            tol_t = std::max(1e-2 * tol_t, opts->tol);
+            b = ritz[wa - 1];
+        }
+        // deflation: lock the leading converged pairs (Eq. defl); keep >= 1 active
+        const double defl = std::max(1e-14, tol_t * tol_t);
+        int add = 0;
+        while (add < ka - 1 && ra[add] <= defl) ++add;
+        for (int i = 0; i < add; ++i) locked_res.push_back(ra[i]);
+        nc += add;
+        mu1 = ritz[add];
+        if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    }
+    restore();
+    // final Rayleigh-Ritz on the whole block: ordered pairs, fresh residuals
+    std::vector<double> rf(w), resf(k);
+    if ((st = arr_core(c, 0, X, ldx, X, ldx, rf.data(), nullptr)) != ARR_OK) return st;
+    if ((st = residuals_core(c, X, ldx, rf.data(), k, resf.data())) != ARR_OK) return st;
+    double maxres = 0.0;
+    for (int i = 0; i < k; ++i) maxres = std::max(maxres, resf[i]);
+    inf.maxres = maxres;
+    inf.converged = (done && maxres <= opts->tol) ? 1 : 0;
+    if (done && !inf.converged) inf.exit_rule = 0;
+    inf.spmm_blocks = c->spmm_blocks - spmm0;
+    inf.p_final = p;
+    inf.d_final = c->d;
+    inf.locked = nc;
+    for (int i = 0; i < k; ++i) { eigval_host[i] = c->sign * rf[i]; res_host[i] = resf[i]; }
+    if (info) *info = inf;
+    return ARR_OK;
+}
+
 // ====================================================================== C-ABI
 extern "C" {
 
@@ -983,6 +1074,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                      double *res_host, arr_solve_info *info) {
     GUARD(c);
     if (!block_ok(X, ldx, c->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
+    if (opts->adapt & 4) return solve_deflate(c, X, ldx, opts, eigval_host, res_host, info);
     const int w = c->w, k = c->k;
     const int m = m_of(c, c->p);
     std::vector<double> ritz(m), res(k);

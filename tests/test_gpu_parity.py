@@ -501,3 +501,22 @@ def test_solve_with_adaptive_p_and_d(arr, kind, adapt):
         assert 3 <= info.d_final <= spec.d
     ev2, _, info2 = ctx.eig_solve(dev_block(X0), tol=spec.tol)  # fixed parameters afterwards
     assert info2.d_final == spec.d and info2.p_final == spec.p
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "lap3dV", "st27", "zipf"])
+def test_solve_with_continuation_and_deflation(arr, kind):
+    """Alg. Arrabit2's continuation and deflation (locking), adapt bit 4:
+    the solve reaches the dense eigenvalues, every returned pair (locked or not) meets
+    tol by the oracle's own residual recomputation, and the pairs come out ordered."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    Xd = dev_block(X0)
+    ev, res, info = ctx.eig_solve(Xd, tol=spec.tol, maxit=200, adapt=4)
+    assert info.converged == 1 and 0 <= info.locked < spec.k
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+    assert np.all(np.diff(ev) <= 1e-12 * np.abs(ev).max())
+    cert = oracle.residuals(A, host(Xd)[:, :spec.k], ev)
+    assert np.all(cert <= 1.01 * spec.tol)
