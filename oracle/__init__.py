@@ -29,6 +29,7 @@ from .core import (  # noqa: F401
     psi,
     poly_filter,
     poly_sweep,
+    gn_step,
     orthonormalize,
     rayleigh_ritz,
     arr,

@@ -201,6 +201,16 @@ def poly_sweep(A, a: float, b: float, coef: np.ndarray, X: np.ndarray) -> np.nda
     return Y / nrm
 
 
+def gn_step(A, a: float, b: float, d: int, X: np.ndarray, coef=None) -> np.ndarray:
+    """One Gauss-Newton inner step of Alg. Arrabit2 (Alg. GN) with
+    the accelerator rho_d in place of A: Y = X (X^T X)^{-1}; Z = rho_d(A) Y;
+    X = Z - X (Y^T Z - I) / 2.  rho_d = T_d of the mapped matrix (coef None) or psi_d."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    Y = X @ np.linalg.inv(X.T @ X)
+    Z = cheb_filter(A, a, b, d, Y) if coef is None else poly_filter(A, a, b, coef, Y)
+    return Z - X @ (Y.T @ Z - np.eye(X.shape[1])) / 2.0
+
+
 # --------------------------------------------------------------------------- dense
 def orthonormalize(Z: np.ndarray):
     """U in orth(Z) (Alg. RR step 1): equilibrate columns (span unchanged),
@@ -292,7 +302,8 @@ class SolveResult:
 
 
 def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
-          s_max: int = 5, w: int | None = None, max_outer: int | None = None, filter: str = "cheb") -> SolveResult:
+          s_max: int = 5, w: int | None = None, max_outer: int | None = None, filter: str = "cheb",
+          inner_solver: str = "mpm") -> SolveResult:
     """Fixed-parameter ARRABIT-MPM (Alg. Arrabit2, with the
     adaptive lines disabled; DESIGN.md §4 R3/R6/R10):
 
@@ -322,7 +333,10 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     for outer in range(1, limit + 1):
         s = sweeps_rule(mu1, a, b, d, s_max, gamma)
         for _ in range(s):
-            X = mpm_sweep(A, a, b, d, X) if gamma is None else poly_sweep(A, a, b, gamma, X)
+            if inner_solver == "gn":  # Alg. Arrabit2's GN branch
+                X = gn_step(A, a, b, d, X, gamma)
+            else:
+                X = mpm_sweep(A, a, b, d, X) if gamma is None else poly_sweep(A, a, b, gamma, X)
         sweeps += s
         mu, Y, r = arr(A, X, p, keep=w)
         res = residuals(A, Y[:, :k], mu[:k])

@@ -81,3 +81,24 @@ def test_solve_smallest_via_negated_matrix_1d_closed_form():
     lam = 2 - 2 * np.cos(np.arange(1, k + 1) * np.pi / (n + 1))
     assert r.converged
     np.testing.assert_allclose(-r.mu, lam, rtol=1e-10)
+
+
+def test_gn_step_fixed_point_and_solve():
+    """Alg. GN: at X = V diag(sqrt(theta)) with V eigenvectors of the
+    (filtered) operator, theta its eigenvalues > 0, X is a fixed point of
+    X+ = Z - X (Y^T Z - I)/2 with Z = op(Y), Y = X (X^T X)^{-1}; and the GN inner
+    solver inside the fixed-parameter driver converges to the closed-form spectrum."""
+    n, k = 120, 6
+    A = synth.laplacian_1d(n)
+    lam = 2 - 2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
+    V = np.sqrt(2.0 / (n + 1)) * np.sin(np.outer(np.arange(1, n + 1), np.arange(1, n + 1)) * np.pi / (n + 1))
+    a, b, d = 0.0, 3.2, 4
+    theta = oracle.chebyshev_T(d, (lam - 1.6) / 1.6)  # rho_d on the spectrum
+    top = np.argsort(theta)[::-1][:k]
+    X = V[:, top] * np.sqrt(theta[top])
+    Xp = oracle.gn_step(A, a, b, d, X)
+    assert np.linalg.norm(Xp - X) <= 1e-10 * np.linalg.norm(X)
+    X0 = synth.gaussian_block(300, k + 1, 2)
+    r = oracle.solve(synth.laplacian_1d(300), k, 8, 1, X0, tol=1e-10, w=k + 1, inner_solver="gn")
+    ref = (2 - 2 * np.cos(np.arange(1, 301) * np.pi / 301))[::-1][:k]
+    assert r.converged and np.max(np.abs(r.mu - ref) / ref) < 1e-10
