@@ -128,6 +128,9 @@ typedef struct {
                         Eqs. hat-d / degree, the context's d as d_max;
                         4 = continuation + deflation (locking) of converged pairs, the
                         paper's b update at continuation (R19)   */
+    int32_t gn;      /* inner solver: 0 = MPM (filter + column normalisation),
+                        1 = Gauss-Newton (Alg. Arrabit2: Y = X (X^T X)^{-1},
+                        Z = rho_d(A) Y, X = Z - X (Y^T Z - I)/2); needs p >= 1          */
 } arr_solve_opts;
 
 typedef struct {

@@ -38,7 +38,8 @@ class arr_dist(ctypes.Structure):
 
 class arr_solve_opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("s_max", ctypes.c_int32),
-                ("exits", ctypes.c_int32), ("inner", ctypes.c_int32), ("adapt", ctypes.c_int32)]
+                ("exits", ctypes.c_int32), ("inner", ctypes.c_int32), ("adapt", ctypes.c_int32),
+                ("gn", ctypes.c_int32)]
 
 
 class arr_solve_info(ctypes.Structure):

@@ -295,12 +295,14 @@ class EigContext:
 
     # -- driver
     def eig_solve(self, X: torch.Tensor, tol: float = 1e-10, maxit: int = 300, s_max: int = 5, exits: int = 0,
-                  inner: str = "range", adapt: int = 0):
+                  inner: str = "range", adapt: int = 0, inner_solver: str = "mpm"):
         """exits: the paper's extra stop rules as a bit mask: 1 = (ii), 2 = (iii).
         inner: 'range' (dynamic-range rule, R6) or 'rcond' (the paper's).
-        adapt: the paper's adaptive p (bit 1) and degree (bit 2), see include/arrabit.h."""
+        adapt: the paper's adaptive p (bit 1), degree (bit 2), continuation + deflation (bit 4).
+        inner_solver: 'mpm' (default) or 'gn' (Gauss-Newton, Alg. Arrabit2)."""
         px, ld, _ = _blk(X, "X")
-        opts = arr_solve_opts(tol, maxit, s_max, exits, 1 if inner == "rcond" else 0, adapt)
+        opts = arr_solve_opts(tol, maxit, s_max, exits, 1 if inner == "rcond" else 0, adapt,
+                              1 if inner_solver == "gn" else 0)
         ev = np.empty(self.k)
         res = np.empty(self.k)
         info = arr_solve_info()
@@ -336,7 +338,7 @@ def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, 
     ev = np.empty(k)
     res = np.empty(k)
     info = arr_solve_info()
-    opts = arr_solve_opts(tol, maxit, s_max, 0, 0, 0)
+    opts = arr_solve_opts(tol, maxit, s_max, 0, 0, 0, 0)
     hs, _ = _stream_handle(stream)
     st = lib.eig_solve_host(int(n), nnz, ptr(row_ptr), ptr(col_idx), ptr(val), k, w, p, d, ptr(X0),
                             ctypes.byref(opts), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

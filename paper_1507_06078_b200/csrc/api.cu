@@ -622,6 +622,33 @@ arr_status gram_rcond(arr_ctx *c, const double *X, int64_t ldx, double *rc) {
     return ARR_OK;
 }
 
+// One Gauss-Newton inner step (Alg. Arrabit2's GN branch P:1490-1493, Alg. GN)
+// with the accelerator: Y = X (X^T X)^{-1}; Z = rho_d(A) Y; X = Z - X (Y^T Z - I)/2.
+// Y / Z live in the last basis block (free during the inner loop); Y^T Z is formed as
+// (X^T X)^{-1} (X^T Z); every n-row product is a DMMA Gram / GEMM.
+arr_status gn_step(arr_ctx *c, double *X, int64_t ldx) {
+    const int w = c->w;
+    const int64_t lq = ldQ(c);
+    double *Yb = c->Q + (int64_t)c->p * w;
+    double *G = G_buf(c), *Gi = V_buf(c), *C = B_buf(c);
+    ST_TRY(gram_x(c, X, ldx, w, X, ldx, w, G, w));
+    CUDA_TRY(cudaMemcpyAsync(Gi, G, sizeof(double) * (size_t)w * w, cudaMemcpyDeviceToDevice, c->stream));
+    int *inf = c->dinfo + INFO_CHOL;
+    SOLVER_TRY(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, w, Gi, w, c->solver_work, c->solver_lwork, inf));
+    SOLVER_TRY(cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, w, Gi, w, c->solver_work, c->solver_lwork, inf + 1));
+    launch_mirror_upper(c, Gi, w);  // column-major lower = row-major upper -> full symmetric inverse
+    ST_TRY(comm_bcast(c, Gi, (size_t)w * w, 0));
+    launch_gemm(c, 1.0, X, ldx, w, Gi, w, w, 0.0, nullptr, 0, Yb, lq, c->A.n);  // Y
+    ST_TRY(filter_core(c, Yb, lq, 0, nullptr));                                   // Z = rho_d(A) Y
+    ST_TRY(gram_x(c, X, ldx, w, Yb, lq, w, G, w));                                // X^T Z
+    launch_gemm(c, 1.0, Gi, w, w, G, w, w, 0.0, nullptr, 0, C, w, w);             // Y^T Z
+    launch_add_diag(c, C, w, w, -1.0);                                            // - I
+    launch_gemm(c, -0.5, X, ldx, w, C, w, w, 1.0, Yb, lq, Yb, lq, c->A.n);        // Z - X (Y^T Z - I)/2
+    launch_copy_rows(c, Yb, lq, X, ldx, c->A.n, w);
+    CHECK_LAUNCH();
+    return ARR_OK;
+}
+
 bool block_ok(const double *p, int64_t ld, int ncols) { return p != nullptr && ld >= ncols && ncols >= 1; }
 
 }  // namespace
@@ -795,7 +822,9 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
                                 c->evals, &lwork_w);
     int lwork_p = 0;
     cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_UPPER, (int)w, c->small, (int)w, &lwork_p);
-    c->solver_lwork = std::max(std::max(lwork, lwork_w), lwork_p);
+    int lwork_i = 0;
+    cusolverDnDpotri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, (int)w, c->small, (int)w, &lwork_i);
+    c->solver_lwork = std::max(std::max(std::max(lwork, lwork_w), lwork_p), lwork_i);
     size_t tdb = 0, thb = 0;
     if (cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, w, CUDA_R_64F, c->small, w,
                                     &tdb, &thb) != CUSOLVER_STATUS_SUCCESS) {
@@ -1074,6 +1103,8 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                      double *res_host, arr_solve_info *info) {
     GUARD(c);
     if (!block_ok(X, ldx, c->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
+    if (opts->gn && (c->p < 1 || (c->filter_kind == 1 && (c->T ? c->p < 1 : c->p < 2))))
+        return fail(c, ARR_EINVAL, "GN inner solver: needs a spare basis block (p >= 1; p >= 2 with psi_d in a lean context)");
     if (opts->adapt & 4) return solve_deflate(c, X, ldx, opts, eigval_host, res_host, info);
     const int w = c->w, k = c->k;
     const int m = m_of(c, c->p);
@@ -1117,8 +1148,10 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
             double rcp = -1.0;
             s = 0;
             for (int chk = 0; chk < 10; ++chk) {
-                for (int q = 0; q < 5; ++q)
-                    if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;
+                for (int q = 0; q < 5; ++q) {
+                    st = opts->gn ? gn_step(c, X, ldx) : filter_core(c, X, ldx, 1, nullptr);
+                    if (st != ARR_OK) return st;
+                }
                 s += 5;
                 double rc = 0.0;
                 if ((st = gram_rcond(c, X, ldx, &rc)) != ARR_OK) return st;
@@ -1126,8 +1159,11 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                 rcp = rc;
             }
         } else {
-            for (int q = 0; q < s; ++q)
-                if ((st = filter_core(c, X, ldx, 1, nullptr)) != ARR_OK) return st;  // MPM sweep
+            for (int q = 0; q < s; ++q) {
+                if (opts->gn) st = gn_step(c, X, ldx);             // GN inner solver
+                else st = filter_core(c, X, ldx, 1, nullptr);      // MPM sweep
+                if (st != ARR_OK) return st;
+            }
         }
         inf.sweeps += s;
         if ((st = arr_core(c, p_cur, X, ldx, X, ldx, ritz.data(), &rank)) != ARR_OK) return st;  // ARR

@@ -613,6 +613,30 @@ __global__ void maxabs_kernel(const double *__restrict__ x, int64_t count, doubl
 }
 }  // namespace
 
+namespace {
+// M (row-major w x w): M[j][i] = M[i][j] for i < j, then M[i][i] += add_diag
+__global__ void mirror_upper_kernel(double *M, int w, double add_diag) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    if (i < j) M[(int64_t)j * w + i] = M[(int64_t)i * w + j];
+    else if (i == j) M[t] += add_diag;
+}
+__global__ void add_diag_kernel(double *M, int w, int64_t ld, double v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < w) M[(int64_t)i * ld + i] += v;
+}
+}  // namespace
+
+void launch_mirror_upper(arr_ctx *c, double *M, int32_t w) {
+    mirror_upper_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(M, w, 0.0);
+    c->launches++;
+}
+void launch_add_diag(arr_ctx *c, double *M, int32_t w, int64_t ld, double v) {
+    add_diag_kernel<<<(w + 255) / 256, 256, 0, c->stream>>>(M, w, ld, v);
+    c->launches++;
+}
+
 void launch_maxabs(arr_ctx *c, const double *x, int64_t count, double *out) {
     cudaMemsetAsync(out, 0, sizeof(double), c->stream);
     int64_t blocks = (count + 255) / 256;

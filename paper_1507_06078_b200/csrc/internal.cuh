@@ -173,3 +173,5 @@ void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d);
 
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out);
 void launch_maxabs(arr_ctx *c, const double *x, int64_t count, double *out);
+void launch_mirror_upper(arr_ctx *c, double *M, int32_t w);  // row-major upper -> lower
+void launch_add_diag(arr_ctx *c, double *M, int32_t w, int64_t ld, double v);

@@ -520,3 +520,20 @@ def test_solve_with_continuation_and_deflation(arr, kind):
     assert np.all(np.diff(ev) <= 1e-12 * np.abs(ev).max())
     cert = oracle.residuals(A, host(Xd)[:, :spec.k], ev)
     assert np.all(cert <= 1.01 * spec.tol)
+
+
+@pytest.mark.parametrize("kind", ["lap2d", "lap3dV", "zipf"])
+def test_solve_with_gn_inner_solver(arr, kind):
+    """Alg. Arrabit2 with the Gauss-Newton inner solver: the solve
+    reaches the dense eigenvalues; residual certificates by the oracle."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = synth.starting_block(spec)
+    ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+    Xd = dev_block(X0)
+    ev, res, info = ctx.eig_solve(Xd, tol=spec.tol, maxit=200, inner_solver="gn")
+    assert info.converged == 1
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
+    cert = oracle.residuals(A, host(Xd)[:, :spec.k], ev)
+    assert np.all(cert <= 1.01 * spec.tol)
