@@ -52,6 +52,8 @@ def parse():
                     help="cheb: T_d (default); interp: the paper's interpolant psi_d (Section 5)")
     ap.add_argument("--adapt", type=int, default=0,
                     help="the paper's adaptive options (bit mask: 1 p, 2 d, 4 continuation + deflation)")
+    ap.add_argument("--inner-solver", default="mpm", choices=["mpm", "gn"],
+                    help="inner solver of Alg. Arrabit2: mpm (default) or gn (Gauss-Newton)")
     ap.add_argument("--partition", action="store_true",
                     help="N>1: row-partition the config over the ranks even for configs 1-2")
     return ap.parse_args()
@@ -277,7 +279,8 @@ def run_ours(args):
         X.copy_(X0, non_blocking=True)
 
     def one_solve():
-        return ctx.eig_solve(X, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max, adapt=args.adapt)
+        return ctx.eig_solve(X, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max, adapt=args.adapt,
+                             inner_solver=args.inner_solver)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -387,7 +390,7 @@ def run_ours(args):
     # eigenpairs inside the timed region (one GPU: the eig_solve_host C-ABI call;
     # partitioned: each rank uploads its local CSR + X0 rows, eig_init_dist, eig_solve)
     e2e = None
-    if not args.no_e2e and (args.filter != "cheb" or args.adapt):
+    if not args.no_e2e and (args.filter != "cheb" or args.adapt or args.inner_solver != "mpm"):
         e2e = {"value": None, "unit": UNIT, "error": "the host-buffer entry eig_solve_host runs the fixed-parameter T_d solve only"}
     elif not args.no_e2e:
         try:
@@ -459,7 +462,7 @@ def run_ours(args):
                 "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "w": spec.w, "d": spec.d,
                            "p": spec.p, "tol": spec.tol, "step": "one full eig_solve from X0",
                            "filter": {"cheb": "T_d (Eq. cheby-poly)", "interp": "psi_d (paper Section 5)"}[args.filter],
-                           "adapt": args.adapt,
+                           "adapt": args.adapt, "inner_solver": args.inner_solver,
                            "l2": "flushed between timed steps (256 MiB write), outside the events",
                            "parallelism": par, "row_order": sched or "natural",
                            "context": "lean (no scratch block)" if ctx_lean else "standard",
