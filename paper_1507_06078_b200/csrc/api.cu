@@ -712,10 +712,12 @@ arr_status solve_deflate(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opt
         inf.a = a; inf.b = b;
         restore();
         if (maxres <= opts->tol) { done = true; inf.exit_rule = 1; break; }
-        if (maxres <= tol_t) {  // continuation (Eq. contin; b update P:1516)
-            tol_t = std::max(1e-2 * tol_t, opts->tol);
-            b = ritz[wa - 1];
-        }
+        if (maxres <= tol_t) tol_t = std::max(1e-2 * tol_t, opts->tol);  // continuation (Eq. contin)
+        // b: the R3 rule (mu_{w+1} after every ARR, here the first active Ritz value outside
+        // the block); the paper's update only at continuation (b = mu_{k+q}) leaves the
+        // RR(X0) estimate in place until max res <= tol_1, which with few sweeps per ARR never
+        // happens (cfg2: max res stays at 0.2 for 300 outer iterations)
+        b = ritz[std::min(wa, (p + 1) * wa - 1)];
         // deflation: lock the leading converged pairs (Eq. defl); keep >= 1 active
         const double defl = std::max(1e-14, tol_t * tol_t);
         int add = 0;
