@@ -306,7 +306,7 @@ def run_ours(args):
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            infos.append((info.converged, info.outer, info.sweeps, info.maxres))
+            infos.append((info.converged, info.outer, info.sweeps, info.maxres, info.locked, info.p_final, info.d_final))
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -451,7 +451,7 @@ def run_ours(args):
                                f"({'oracle full-solve counts, tests/golden' if cnt else 'GPU solve counts'})"}
 
     if rank == 0:
-        conv, outer, sweeps, maxres = infos[-1]
+        conv, outer, sweeps, maxres, locked, p_fin, d_fin = infos[-1]
         par = ("1 GPU" if world == 1 else
                (f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
                 if partitioned else f"{world} independent replicas (no collective)"))
@@ -466,7 +466,8 @@ def run_ours(args):
                            "l2": "flushed between timed steps (256 MiB write), outside the events",
                            "parallelism": par, "row_order": sched or "natural",
                            "context": "lean (no scratch block)" if ctx_lean else "standard",
-                           "converged": bool(conv), "outer": outer, "sweeps": sweeps, "maxres": maxres},
+                           "converged": bool(conv), "outer": outer, "sweeps": sweeps, "maxres": maxres,
+                           "locked": locked, "p_final": p_fin, "d_final": d_fin},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

@@ -476,6 +476,12 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
             const int g = spmm_x(c, s, &st2);
             if (st2 != ARR_OK) return st2;
             if (g < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
+            if (c->defl_n > 0) {  // ARR in the orthogonal complement of the locked vectors
+                for (int pass = 0; pass < 2; ++pass) {
+                    ST_TRY(gram_x(c, c->defl_Q, c->defl_ld, c->defl_n, T, lt, w, G_buf(c), w));
+                    launch_gemm(c, -1.0, c->defl_Q, c->defl_ld, c->defl_n, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
+                }
+            }
             for (int pass = 0; pass < 2; ++pass) {
                 ST_TRY(gram_x(c, Q, lq, jw, T, lt, w, G_buf(c), w));
                 // The first pass's coefficients Q[:, :jw]^T (A U_{j-1}) ARE rows [0, jw) of
@@ -699,7 +705,10 @@ arr_status solve_deflate(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opt
             }
             CUDA_TRY(cudaGetLastError());
         }
-        if ((st = arr_core(c, p, Xa, ldx, Xa, ldx, ritz.data(), &rank)) != ARR_OK) { restore(); return st; }
+        c->defl_Q = X; c->defl_ld = ldx; c->defl_n = nc;
+        st = arr_core(c, p, Xa, ldx, Xa, ldx, ritz.data(), &rank);
+        c->defl_n = 0;
+        if (st != ARR_OK) { restore(); return st; }
         const int ka = k - nc;
         std::vector<double> ra(ka);
         if ((st = residuals_core(c, Xa, ldx, ritz.data(), ka, ra.data())) != ARR_OK) { restore(); return st; }

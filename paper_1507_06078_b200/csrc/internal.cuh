@@ -40,6 +40,10 @@ struct arr_ctx {
     int max_row_nnz;  // longest CSR row (selects the SpMM chunk size)
     int tile_rows;    // SpMM rows per tile in natural order (1..64; env ARRABIT_TILE)
     int col_split;    // column vectors per SpMM thread (1 default; env ARRABIT_SPLIT, tuning)
+    // deflation (solve_deflate): locked vectors the augmentation blocks are projected against
+    const double *defl_Q;
+    int64_t defl_ld;
+    int defl_n;
     // eig_set_mode: +1 = k largest eigenpairs of A, -1 = k smallest (the solver runs on -A)
     int sign;
     // polynomial filter (eig_set_filter): 0 = T_d, 1 = psi_d (Chebyshev coefficients coef[0..d])

@@ -1,10 +1,11 @@
 #!/bin/bash
 # Round 1 final validation of the committed tree: all GPU tests, smoke, the default bench line.
 set -x
-O=gpurun_out/final5
+O=gpurun_out/final6
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
 timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
+timeout 900 python bench.py --adapt 4 --no-e2e --no-cpu-baseline > $O/bench_cfg2_adapt4.json 2> $O/bench_cfg2_adapt4.err
 echo done

@@ -514,7 +514,8 @@ def test_solve_with_continuation_and_deflation(arr, kind):
     ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
     Xd = dev_block(X0)
     ev, res, info = ctx.eig_solve(Xd, tol=spec.tol, maxit=200, adapt=4)
-    assert info.converged == 1 and 0 <= info.locked < spec.k
+    assert info.converged == 1 and 0 <= info.locked < spec.k, (
+        info.outer, info.maxres, info.locked, info.exit_rule, info.a, info.b)
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
     assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
     assert np.all(np.diff(ev) <= 1e-12 * np.abs(ev).max())
