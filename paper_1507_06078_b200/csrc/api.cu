@@ -895,6 +895,10 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         }
         c->max_row_nnz = (int)c->h_stage[0];
     }
+    if (!multi) {  // union-staged SpMM plan (spmm_union.cu); optional, off when it does not pay
+        union_prepare(c);
+        cudaGetLastError();
+    }
     *out = c;
     return ARR_OK;
 }
@@ -907,6 +911,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    union_release(c);
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
                     c->trtri_dwork};
     for (void *p : ptrs)
@@ -950,6 +955,8 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
     if (is_dist(c)) return fail(c, ARR_EINVAL, "schedule: not supported on a distributed context");
     if (!tile_row0) {
         c->tile_row0 = nullptr; c->tile_len = nullptr; c->ntiles = 0;
+        union_prepare(c);
+        cudaGetLastError();
         return ARR_OK;
     }
     if (!tile_len || ntiles < 1) return fail(c, ARR_EINVAL, "schedule: null lengths or no tiles");
@@ -960,6 +967,8 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->h_istage[0]) return fail(c, ARR_EINVAL, "schedule does not cover every row exactly once with tiles of 1..64 rows");
     c->tile_row0 = tile_row0; c->tile_len = tile_len; c->ntiles = ntiles;
+    union_prepare(c);  // the union tiles follow the new order
+    cudaGetLastError();
     return ARR_OK;
 }
 
