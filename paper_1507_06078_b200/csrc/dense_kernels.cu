@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const doubl
                                                        int m1, const double *__restrict__ B, int64_t ldb, int m2,
                                                        double beta, const double *Cin, int64_t ldc, double *Out,
                                                        int64_t ldo, int64_t n, int upper) {
-    const int64_t r0 = (int64_t)blockIdx.x * TILE;
-    const int c0 = blockIdx.y * TILE;
+    // column tile fastest: the column tiles of one row tile run together and share its
+    // X rows through L2 (one DRAM read of X instead of one per column tile)
+    const int nct = (m2 + TILE - 1) / TILE;
+    const int64_t r0 = (int64_t)(blockIdx.x / nct) * TILE;
+    const int c0 = (int)(blockIdx.x % nct) * TILE;
     if (upper && c0 + TILE < m1) m1 = c0 + TILE;
     __shared__ double Xs[2][TILE][KS + PAD];
     __shared__ double Bs[2][KS][TILE + PAD];
@@ -309,8 +312,11 @@ __global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gemm_kernel_ca(double 
                                                           int m1, const double *__restrict__ B, int64_t ldb, int m2,
                                                           double beta, const double *Cin, int64_t ldc, double *Out,
                                                           int64_t ldo, int64_t n, int upper) {
-    const int64_t r0 = (int64_t)blockIdx.x * TILE;
-    const int c0 = blockIdx.y * TILE;
+    // column tile fastest: the column tiles of one row tile run together and share its
+    // X rows through L2 (one DRAM read of X instead of one per column tile)
+    const int nct = (m2 + TILE - 1) / TILE;
+    const int64_t r0 = (int64_t)(blockIdx.x / nct) * TILE;
+    const int c0 = (int)(blockIdx.x % nct) * TILE;
     if (upper && c0 + TILE < m1) m1 = c0 + TILE;
     extern __shared__ __align__(16) double dsm[];
     double (*Xs)[TILE][KS + PAD] = reinterpret_cast<double (*)[TILE][KS + PAD]>(dsm);
@@ -494,7 +500,7 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
 void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
                  int64_t n, int upper) {
-    dim3 grid((unsigned)((n + TILE - 1) / TILE), (m2 + TILE - 1) / TILE);
+    const unsigned grid = (unsigned)(((n + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE));
 #if ARR_DMMA_CA
     if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
         const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));

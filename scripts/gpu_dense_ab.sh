@@ -1,5 +1,5 @@
 #!/bin/bash
-O=gpurun_out/ksplit
+O=gpurun_out/gemmgrid
 mkdir -p $O
 python scripts/micro_gram_shapes.py > $O/shapes.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist.py -q -x > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
