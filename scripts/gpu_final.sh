@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round 1 final validation of the committed tree: all GPU tests, smoke, the default bench line.
 set -x
-O=gpurun_out/final6
+O=gpurun_out/final7
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
