@@ -4,6 +4,8 @@
 // order reduction of the partial tiles (deterministic, no atomics).
 #include <math.h>
 
+#include <cmath>
+
 #include "internal.cuh"
 
 #ifndef ARR_DMMA_CA
@@ -465,12 +467,23 @@ int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     }
     const int64_t slots = (int64_t)num_sms * per_sm;
     int64_t ns = slots / tiles;
-    if (ns < 1) ns = (tiles > slots) ? 1 : 1;
-    const int64_t maxns = n / 512;
-    if (ns > maxns) ns = maxns;
     if (ns < 1) ns = 1;
-    if (ns > 64) ns = 64;
-    return (int)ns;
+    int64_t maxns = n / 512;
+    if (maxns > 64) maxns = 64;
+    if (maxns < 1) maxns = 1;
+    if (ns > maxns) ns = maxns;
+    // wave quantisation: tiles*ns CTAs fill ceil(tiles*ns/slots) waves; take the smallest
+    // split count from ns up whose last wave is >= 95% full (else the best fill seen)
+    auto fill = [&](int64_t q) {
+        const double w = (double)(tiles * q) / (double)slots;
+        return w / std::ceil(w);
+    };
+    int64_t best = ns;
+    for (int64_t q = ns; q <= maxns; ++q) {
+        if (fill(q) > fill(best) + 1e-9) best = q;
+        if (fill(best) >= 0.95) break;
+    }
+    return (int)best;
 }
 
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
