@@ -469,7 +469,7 @@ int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     int64_t ns = slots / tiles;
     if (ns < 1) ns = 1;
     int64_t maxns = n / 512;
-    if (maxns > 64) maxns = 64;
+    if (maxns > 128) maxns = 128;
     if (maxns < 1) maxns = 1;
     if (ns > maxns) ns = maxns;
     // wave quantisation: tiles*ns CTAs fill ceil(tiles*ns/slots) waves; take the smallest
