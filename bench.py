@@ -428,6 +428,7 @@ def run_ours(args):
             e2e = {"value": spec.k * len(e2e_s) * jobs / tot, "unit": UNIT,
                    "h2d_bytes_per_step": int(8 * (r1 - r0 + 1) + 12 * nnz_loc + 8 * nrows * spec.w),
                    "d2h_bytes_per_step": int(16 * spec.k + 8 * (r1 - r0) * spec.k),
+                   "step_ms": [round(1e3 * x, 3) for x in e2e_s],
                    "api": ("eig_solve_host (C-ABI, pinned host buffers, device alloc + copies inside)" if not partitioned
                            else "per rank: H2D of local CSR + X0 rows, eig_init_dist + eig_solve, D2H of the local "
                                 "eigenvector rows (bytes of rank 0)")}
