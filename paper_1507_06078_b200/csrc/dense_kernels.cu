@@ -453,18 +453,16 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     const int64_t ta = (m1 + TILE - 1) / TILE, tb = (m2 + TILE - 1) / TILE;
     const int64_t tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        int o = 0;
 #if ARR_DMMA_CA
-        cudaFuncSetAttribute(gram_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * 2 * S_CA * KS * (TILE + PAD)));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
+    static LaunchCache cache;
+    const int per_sm = cached_occupancy(cache, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
 #else
+    static const int per_sm = [] {
+        int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gram_kernel, THREADS, 0);
+        return o > 0 ? o : 1;
+    }();
 #endif
-        per_sm = o > 0 ? o : 1;
-    }
     const int64_t slots = (int64_t)num_sms * per_sm;
     int64_t ns = slots / tiles;
     if (ns < 1) ns = 1;
@@ -497,11 +495,8 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
 #if ARR_DMMA_CA
     if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
         const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(gram_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        static LaunchCache cache;
+        cached_occupancy(cache, gram_kernel_ca, THREADS, smem);  // sets the smem attribute once
         gram_kernel_ca<<<grid, THREADS, smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
     } else
 #endif
@@ -517,11 +512,8 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
 #if ARR_DMMA_CA
     if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
         const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(gemm_kernel_ca, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        static LaunchCache cache;
+        cached_occupancy(cache, gemm_kernel_ca, THREADS, smem);  // sets the smem attribute once
         gemm_kernel_ca<<<grid, THREADS, smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n,
                                                            upper);
     } else

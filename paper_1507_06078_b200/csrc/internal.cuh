@@ -4,6 +4,7 @@
 #include <cusolverDn.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -137,6 +138,27 @@ struct SpmmArgs {
     const int32_t *tile_len;
     int64_t ntiles;
 };
+
+// Per-kernel-instantiation cache of the dynamic shared-memory attribute and the
+// occupancy at that size; the mutex makes it safe for the host threads of an
+// in-process rank group (comm_init_local_group) that launch concurrently.
+struct LaunchCache {
+    std::mutex mu;
+    int occ = -1;
+    size_t smem = 0;
+};
+template <class Kern>
+int cached_occupancy(LaunchCache &lc, Kern kern, int threads, size_t smem) {
+    std::lock_guard<std::mutex> lk(lc.mu);
+    if (lc.occ < 0 || lc.smem != smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+        lc.occ = o > 0 ? o : 1;
+        lc.smem = smem;
+    }
+    return lc.occ;
+}
 
 // Launch the fused SpMM: Yout = alpha*(A Yin - shift*Yin) + beta*Yprev.
 // Returns the grid size used (number of partial rows written if partials != nullptr).

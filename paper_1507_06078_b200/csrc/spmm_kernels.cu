@@ -718,15 +718,8 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
         size_t smem = 2 * stage;
         const size_t red = 8 * (size_t)ncons * VEC;
         if (smem < red) smem = red;
-        static int occ = -1;
-        static size_t occ_smem = 0;
-        if (occ < 0 || occ_smem != smem) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int o = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, ncons + 32, smem);
-            occ = o > 0 ? o : 1;
-            occ_smem = smem;
-        }
+        static LaunchCache cache;  // per instantiation (one device per process)
+        const int occ = cached_occupancy(cache, kern, ncons + 32, smem);
         const int64_t ntiles = a.tile_row0 ? a.ntiles : (a.n + RT - 1) / RT;
         int64_t G = (int64_t)c->num_sms * occ;
         if (G > ntiles) G = ntiles;
@@ -743,15 +736,8 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     size_t smem = ((sizeof(Ent) * (size_t)kNnzCap + 4 * (size_t)(kTile + 2) + 15) & ~size_t(15));
     const size_t red = 8 * (size_t)nthr * VEC;
     if (smem < red) smem = red;
-    static int occ = -1;  // per instantiation (one device per process)
-    static size_t occ_smem = 0;
-    if (occ < 0 || occ_smem != smem) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, nthr, smem);
-        occ = o > 0 ? o : 1;
-        occ_smem = smem;
-    }
+    static LaunchCache cache;  // per instantiation (one device per process)
+    const int occ = cached_occupancy(cache, kern, nthr, smem);
     const int64_t ntiles = a.tile_row0 ? a.ntiles : (a.n + RT - 1) / RT;
     int64_t G = (int64_t)c->num_sms * occ;
     if (G > ntiles) G = ntiles;

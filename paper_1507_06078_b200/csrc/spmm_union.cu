@@ -343,14 +343,8 @@ static int launch_union_t(arr_ctx *c, const SpmmArgs &a) {
     const UnionPlan &u = c->uplan;
     const size_t smem = union_smem_bytes(u.umax, u.rtmax, u.nzmax, u.pw);
     auto kern = spmm_union_kernel<HAS_PREV, STORE, SUMSQ, COLSHIFT, HAS_X>;
-    static size_t smem_set = 0;
-    static int per_sm = 0;
-    if (smem != smem_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUThreads, smem);
-        if (per_sm < 1) per_sm = 1;
-        smem_set = smem;
-    }
+    static LaunchCache cache;
+    const int per_sm = cached_occupancy(cache, kern, kUThreads, smem);
     int64_t grid = (int64_t)c->num_sms * per_sm;
     if (grid > u.ntiles) grid = u.ntiles;
     if (grid < 1) grid = 1;
