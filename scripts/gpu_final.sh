@@ -2,7 +2,7 @@
 # Round 1 final validation of the committed tree: all GPU tests, smoke, the default bench
 # line, the reference arm, and the ncu launch list of the same bench command.
 set -x
-O=gpurun_out/final8
+O=gpurun_out/final9
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
