@@ -127,10 +127,13 @@ typedef struct {
                         context's p; 2 = d starts at 3 and is re-chosen after every ARR by
                         Eqs. hat-d / degree, the context's d as d_max;
                         4 = continuation + deflation (locking) of converged pairs, the
-                        paper's b update at continuation (R19)   */
+                        paper's b update at continuation (R19);
+                        bit 4 runs fixed p / d MPM sweeps with the dynamic-range rule and
+                        returns ARR_EINVAL combined with bits 1/2, gn, inner or exits   */
     int32_t gn;      /* inner solver: 0 = MPM (filter + column normalisation),
                         1 = Gauss-Newton (Alg. Arrabit2: Y = X (X^T X)^{-1},
-                        Z = rho_d(A) Y, X = Z - X (Y^T Z - I)/2); needs p >= 1          */
+                        Z = rho_d(A) Y, X = Z - X (Y^T Z - I)/2); needs p >= 1; a step
+                        whose X^T X is not positive definite returns ARR_ENUMERIC   */
 } arr_solve_opts;
 
 typedef struct {
@@ -151,7 +154,7 @@ typedef struct {
 /* ---------------------------------------------------------------- lifecycle
  * eig_init: create a context for A with k wanted pairs, block width w = k,
  * ARR augmentation depth p (Eq. S:ARR) and Chebyshev degree d
- * (Eq. cheby-poly).  Requires 1 <= k, 0 <= p, 1 <= d, (p+1)k < n
+ * (Eq. cheby-poly).  Requires 1 <= k, 0 <= p <= 16, 1 <= d, (p+1)k < n
  * (Alg. ARR input), n < 2^31.  stream: cudaStream_t or NULL.
  * Allocates the workspace described above (ARR_ENOMEM if it does not fit). */
 arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream);
@@ -172,8 +175,8 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A_local, int32_t k, int32
 arr_status eig_destroy(arr_ctx *c);
 const char *eig_last_error(const arr_ctx *c);
 size_t eig_workspace_bytes(const arr_ctx *c);
-/* Number of kernels this context has launched so far (CUDA-graph replays count
- * every node).  Library calls (cuSOLVER) are not counted. */
+/* Number of kernels this context has launched so far (a replayed CUDA graph
+ * counts every kernel node).  Library calls (cuSOLVER) are not counted. */
 uint64_t eig_launch_count(const arr_ctx *c);
 /* Phase timing (CUDA events on the context stream, resolved at the stream
  * syncs the calls already make).  on != 0 enables it and zeroes the totals.
@@ -237,14 +240,18 @@ arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, do
 
 /* ---------------------------------------------------------------- A3 (test hook)
  * Y = alpha (A - shift I) X for ncols columns (ncols <= 2048).  X, Y device,
- * row-major, must not alias. */
+ * row-major, must not alias.  Always A itself (also in eig_set_mode smallest).
+ * On a distributed context the call is collective: the ghost rows of X are
+ * exchanged first (they are overwritten), then the owned rows of Y computed. */
 arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t ldx,
                 double *Y, int64_t ldy, int32_t ncols);
 
 /* ---------------------------------------------------------------- A4
  * Tall-skinny fp64 products on DMMA tensor cores (mma.sync m8n8k4.f64).
  * gram:  G = X^T Y, X n x m1, Y n x m2, G device row-major m1 x m2 (ldg).
- *        Split over rows, fixed-order reduction (deterministic).
+ *        Split over rows, fixed-order reduction (deterministic).  m1 * m2 must
+ *        fit the context's partial-sum buffer (>= max(16 m w, 4096 max(m, 2048))
+ *        doubles, m = (p+1)w), else ARR_EINVAL.
  * gemm:  Out = beta*Cin + alpha * X B, X n x m1, B device row-major m1 x m2 (ldb),
  *        Cin/Out n x m2.  Cin may equal Out; X must not alias Out.       */
 arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
@@ -253,11 +260,15 @@ arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t 
                 int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out,
                 int64_t ldo);
 
-/* Orthonormalise the ncols (<= w) columns of X in place: two passes of SVQB
- * (X^T X Gram, column equilibration, eig, X <- X D V L^{-1/2}).  The span is
- * that of X plus, if X is rank deficient, directions from its rounding noise
- * (Alg. RR step 1, "orthonormalize Z").  *rank = number of Gram
- * eigenvalues above 1e-14 * max in the first pass (host, synchronises). */
+/* Orthonormalise the ncols (<= w) columns of X in place: shifted CholeskyQR3
+ * (Gram X^T X on DMMA, column equilibration, shift 11(n c + c(c+1)) u c, potrf,
+ * trtri, X <- X D R^{-1}; two unshifted passes follow, the third skipped when the
+ * second factor is within 1e-6 of I), falling back to two SVQB passes
+ * (X <- X D V L^{-1/2}) if a Cholesky factorisation fails.  The span is that of X
+ * plus, if X is rank deficient, directions from its rounding noise (Alg. RR
+ * step 1, "orthonormalize Z").  *rank = number of R_ii^2 above
+ * 100 x shift in the first pass (SVQB: Gram eigenvalues above 1e-14 * max;
+ * host, synchronises). */
 arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank);
 
 /* Augmented Rayleigh-Ritz (Alg. ARR P:531-541 with Alg. RR) on

@@ -14,9 +14,17 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 namespace {
+
+// NVTX range around one public call (visible in nsys / ncu --nvtx timelines).
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 // Process-wide pool of cuSOLVER handles (creating one costs tens of ms; the
 // host-buffer entry creates a context per call).  A handle is bound to the
@@ -68,7 +76,8 @@ void dev_free(void *p, cudaStream_t s) {
 }
 
 constexpr double kSvqbTau = 1e-14;  // eigenvalue floor of the SVQB Gram (relative)
-enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2, INFO_CHOL = 40 };  // dinfo slots (INFO_RANK0.. per block;
+enum { INFO_SYEVD = 0, INFO_BAD = 1, INFO_RANK0 = 2, INFO_CHOL = 40 };
+static_assert(INFO_RANK0 + ARR_MAX_P + 1 <= INFO_CHOL, "per-block rank slots overlap the Cholesky info words");  // dinfo slots (INFO_RANK0.. per block;
                                                                         // INFO_CHOL..+5: potrf/trtri of 3 passes)
 
 arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
@@ -199,9 +208,9 @@ inline bool is_dist(const arr_ctx *c) { return c->nranks > 1; }
 // rows.  Column sums of squares (if requested) of the two launches are written
 // to consecutive partial rows.  Returns the number of partial rows (< 0: width
 // not supported).
-int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st) {
+int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
     *st = ARR_OK;
-    if (c->sign < 0) {  // the solver's operator is -A: alpha (-A y - shift y) = (-alpha) (A y + shift y)
+    if (op && c->sign < 0) {  // the solver's operator is -A: alpha (-A y - shift y) = (-alpha) (A y + shift y)
         s.alpha = -s.alpha;
         s.shift = -s.shift;
     }
@@ -642,6 +651,13 @@ arr_status gn_step(arr_ctx *c, double *X, int64_t ldx) {
     int *inf = c->dinfo + INFO_CHOL;
     SOLVER_TRY(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, w, Gi, w, c->solver_work, c->solver_lwork, inf));
     SOLVER_TRY(cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, w, Gi, w, c->solver_work, c->solver_lwork, inf + 1));
+    // X^T X must be SPD for the inverse to exist: a singular or indefinite Gram (X lost
+    // rank) fails the solve instead of feeding a garbage inverse into Y and X
+    CUDA_TRY(cudaMemcpyAsync(c->h_istage + 56, inf, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->h_istage[56] != 0 || c->h_istage[57] != 0)
+        return fail(c, ARR_ENUMERIC, "GN step: X^T X is not positive definite (potrf/potri info " +
+                                         std::to_string(c->h_istage[56]) + "/" + std::to_string(c->h_istage[57]) + ")");
     launch_mirror_upper(c, Gi, w);  // column-major lower = row-major upper -> full symmetric inverse
     ST_TRY(comm_bcast(c, Gi, (size_t)w * w, 0));
     launch_gemm(c, 1.0, X, ldx, w, Gi, w, w, 0.0, nullptr, 0, Yb, lq, c->A.n);  // Y
@@ -776,7 +792,8 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     if (multi && (dist->n_ghost < 0 || A->n + dist->n_ghost >= (int64_t(1) << 31) || dist->row_begin < 0 ||
                   dist->row_begin + A->n > n_global))
         return ARR_EINVAL;
-    if (k < 1 || w_in < k || p < 0 || d < 1 || (int64_t)(p + 1) * w_in >= n_global || w_in > ARR_MAX_W) return ARR_EINVAL;
+    if (k < 1 || w_in < k || p < 0 || p > ARR_MAX_P || d < 1 || (int64_t)(p + 1) * w_in >= n_global || w_in > ARR_MAX_W)
+        return ARR_EINVAL;
     arr_ctx *c = new (std::nothrow) arr_ctx();
     if (!c) return ARR_ENOMEM;
     c->A = *A;
@@ -895,10 +912,6 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         }
         c->max_row_nnz = (int)c->h_stage[0];
     }
-    if (!multi) {  // union-staged SpMM plan (spmm_union.cu); optional, off when it does not pay
-        union_prepare(c);
-        cudaGetLastError();
-    }
     *out = c;
     return ARR_OK;
 }
@@ -911,7 +924,6 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    union_release(c);
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
                     c->trtri_dwork};
     for (void *p : ptrs)
@@ -955,8 +967,6 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
     if (is_dist(c)) return fail(c, ARR_EINVAL, "schedule: not supported on a distributed context");
     if (!tile_row0) {
         c->tile_row0 = nullptr; c->tile_len = nullptr; c->ntiles = 0;
-        union_prepare(c);
-        cudaGetLastError();
         return ARR_OK;
     }
     if (!tile_len || ntiles < 1) return fail(c, ARR_EINVAL, "schedule: null lengths or no tiles");
@@ -967,8 +977,6 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->h_istage[0]) return fail(c, ARR_EINVAL, "schedule does not cover every row exactly once with tiles of 1..64 rows");
     c->tile_row0 = tile_row0; c->tile_len = tile_len; c->ntiles = ntiles;
-    union_prepare(c);  // the union tiles follow the new order
-    cudaGetLastError();
     return ARR_OK;
 }
 
@@ -999,6 +1007,7 @@ arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
 
 arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev) {
     GUARD(c);
+    Nvtx nvtx_("arrabit::filter_step");
     if (!c->have_interval) return fail(c, ARR_EINVAL, "eig_set_interval not called");
     if (!block_ok(X, ldx, c->w)) return fail(c, ARR_EINVAL, "bad block X / ldx");
     CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
@@ -1043,7 +1052,10 @@ arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t
     s.Yin = X; s.ld_in = ldx;
     s.alpha = alpha; s.shift = shift;
     s.Yout = Y; s.ld_out = ldy;
-    if (launch_spmm(c, s) < 0) return fail(c, ARR_EINVAL, "unsupported width");
+    arr_status st;
+    const int g = spmm_x(c, s, &st, /*op=*/false);  // A itself (not the solver's operator sign*A)
+    if (st != ARR_OK) return st;
+    if (g < 0) return fail(c, ARR_EINVAL, "unsupported width");
     CHECK_LAUNCH();
     return ARR_OK;
 }
@@ -1052,6 +1064,9 @@ arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const doub
                 double *G, int64_t ldg) {
     GUARD(c);
     if (!block_ok(X, ldx, m1) || !block_ok(Y, ldy, m2) || !G || ldg < m2) return fail(c, ARR_EINVAL, "bad gram args");
+    if ((size_t)m1 * (size_t)m2 > c->part_elems)
+        return fail(c, ARR_EINVAL, "gram: m1 * m2 exceeds the context's partial-sum buffer (m1 * m2 <= " +
+                                       std::to_string(c->part_elems) + ")");
     ST_TRY(gram_x(c, X, ldx, m1, Y, ldy, m2, G, ldg));
     CHECK_LAUNCH();
     return ARR_OK;
@@ -1070,6 +1085,7 @@ arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t 
 
 arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank) {
     GUARD(c);
+    Nvtx nvtx_("arrabit::orthonormalize");
     if (!block_ok(X, ldx, ncols) || ncols > c->w) return fail(c, ARR_EINVAL, "bad block / ncols > w");
     // keep the input in the basis buffer: CholeskyQR3 X_copy -> X, SVQB fallback from the copy
     launch_copy_rows(c, X, ldx, c->Q, ldQ(c), c->A.n, ncols);
@@ -1091,6 +1107,7 @@ arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int
 arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx, double *Y, int64_t ldy,
                          double *ritz_host, int32_t *rank) {
     GUARD(c);
+    Nvtx nvtx_("arrabit::arr_project");
     if (p_use < 0 || p_use > c->p) return fail(c, ARR_EINVAL, "p_use out of range");
     if (!block_ok(X, ldx, c->w) || (Y && !block_ok(Y, ldy, c->w)) || !ritz_host)
         return fail(c, ARR_EINVAL, "bad arr_project args");
@@ -1111,6 +1128,7 @@ arr_status arr_project(arr_ctx *c, const double *X, int64_t ldx, double *Y, int6
 arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_host, int32_t ncols,
                      double *res_host) {
     GUARD(c);
+    Nvtx nvtx_("arrabit::residuals");
     if (!block_ok(Y, ldy, ncols) || ncols > std::max(m_of(c, c->p), ARR_MAX_W) || !mu_host || !res_host)
         return fail(c, ARR_EINVAL, "bad residual args");
     if (c->sign > 0) return residuals_core(c, Y, ldy, mu_host, ncols, res_host);
@@ -1122,10 +1140,17 @@ arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_
 arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts, double *eigval_host,
                      double *res_host, arr_solve_info *info) {
     GUARD(c);
+    Nvtx nvtx_("arrabit::eig_solve");
     if (!block_ok(X, ldx, c->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
     if (opts->gn && (c->p < 1 || (c->filter_kind == 1 && (c->T ? c->p < 1 : c->p < 2))))
         return fail(c, ARR_EINVAL, "GN inner solver: needs a spare basis block (p >= 1; p >= 2 with psi_d in a lean context)");
-    if (opts->adapt & 4) return solve_deflate(c, X, ldx, opts, eigval_host, res_host, info);
+    if (opts->adapt & 4) {
+        // continuation + deflation runs the fixed-p/d MPM sweeps of solve_deflate only
+        if ((opts->adapt & 3) || opts->gn || opts->inner != 0 || opts->exits != 0)
+            return fail(c, ARR_EINVAL, "adapt bit 4 (continuation + deflation) cannot be combined with adaptive p/d, "
+                                       "GN, the rcond inner rule or the extra exit rules");
+        return solve_deflate(c, X, ldx, opts, eigval_host, res_host, info);
+    }
     const int w = c->w, k = c->k;
     const int m = m_of(c, c->p);
     std::vector<double> ritz(m), res(k);

@@ -11,6 +11,7 @@
 #include "../../include/arrabit.h"
 
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
+#define ARR_MAX_P 16    // deepest ARR augmentation (the paper uses p <= 3)
 constexpr int kPhases = 6;  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
 
 // Row-partition plan of one rank (comm.cu; arr_dist in include/arrabit.h).
@@ -30,20 +31,6 @@ struct DistPlan {
     bool cur_direct = true;                // state of the exchange in flight
     int cur_ncols = 0;
     int64_t cur_ld = 0;
-};
-
-// Union-staged SpMM plan (spmm_union.cu): contiguous row tiles, the sorted distinct
-// columns of each tile and a 16-bit local index per non-zero.
-struct UnionPlan {
-    int64_t *r0 = nullptr;   // [ntiles] first row
-    int32_t *len = nullptr;  // [ntiles] rows
-    int32_t *cnt = nullptr;  // [ntiles] distinct columns U
-    int32_t *ucol = nullptr; // [nnz] tile t's columns at [row_ptr[r0[t]], + U)
-    uint16_t *loc = nullptr; // [nnz] index of each non-zero's column in its tile's list
-    int64_t ntiles = 0;
-    int umax = 0, rtmax = 0, nzmax = 0, pw = 0;
-    double ratio = 0.0;      // nnz / sum U (reuse of a staged row)
-    bool on = false;
 };
 
 struct arr_ctx {
@@ -104,7 +91,6 @@ struct arr_ctx {
     // multi-GPU (eig_init_dist): communicator, partition plan, allreduce staging
     arr_comm *comm;
     int nranks;  // size of comm (1 without one)
-    UnionPlan uplan;
     DistPlan plan;
     double *stage;
     size_t stage_elems;
@@ -163,10 +149,6 @@ int cached_occupancy(LaunchCache &lc, Kern kern, int threads, size_t smem) {
 // Launch the fused SpMM: Yout = alpha*(A Yin - shift*Yin) + beta*Yprev.
 // Returns the grid size used (number of partial rows written if partials != nullptr).
 int launch_spmm(arr_ctx *c, const SpmmArgs &a);
-// union-staged variant (spmm_union.cu): -1 when it does not apply to this launch
-int launch_spmm_union(arr_ctx *c, const SpmmArgs &a);
-bool union_prepare(arr_ctx *c);
-void union_release(arr_ctx *c);
 // out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)
 void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,
                              const double *mu_div);

@@ -922,10 +922,6 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
     if (a.Xa) v2 = v2 && vec2_ok(a.Xa, a.ld_xa);
     c->spmm_blocks++;
-    if (c->uplan.on) {
-        const int g = launch_spmm_union(c, a);
-        if (g >= 0) return g;
-    }
 #if ARR_SPMM_V4
     bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
     if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);
