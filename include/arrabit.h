@@ -206,6 +206,20 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b);
  * arrays, borrowed (must outlive the context or the next call).
  * tile_row0 == NULL restores natural order. */
 arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles);
+/* Declare A a stencil operator on an nx x ny x nz grid (row i = x + nx (y + ny z),
+ * x fastest): every row's columns sorted ascending and within the 3x3x3
+ * neighbourhood of its grid point (the finite-difference operators of the paper's
+ * test set; cfg 1-3, 5).  The pattern is verified on the device
+ * (ARR_EINVAL if it does not hold or nx*ny*nz != n); then A is stored once more as K
+ * diagonals (DIA, K = number of neighbour offsets present, 8 K n bytes allocated
+ * here: the one allocation after eig_init; ARR_ENOMEM if it does not fit) and every
+ * fused SpMM of the context without a per-column shift runs the stencil-aware
+ * 2.5-D blocked kernel: same per-row FMA order, so outputs are
+ * bitwise those of the CSR kernels.  nx = ny = nz = 0 switches back to CSR and
+ * frees the copy.  Single-GPU contexts only; synchronises the stream. */
+arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
+/* K of the active stencil path (0 = the CSR kernels). */
+int32_t eig_stencil_active(const arr_ctx *c);
 /* Change the degree d used by filter_step (1 <= d). */
 arr_status eig_set_degree(arr_ctx *c, int32_t d);
 /* Which end of the spectrum: smallest = 0 (default): the k algebraically largest

@@ -10,8 +10,9 @@ from arXiv 1507.06078 (PAPER.md = P):
 
 * sparse part in plain C (``csr_oracle.c``: SpMM, Chebyshev filter, column
   norms), loaded with ctypes;
-* dense part with numpy/scipy library primitives (pivoted Householder QR,
-  symmetric eig) used as single steps of the paper's algorithms.
+* dense part in ``dense.py``: the oracle's own pivoted / blocked Householder QR,
+  cyclic Jacobi eig, Cholesky and Gaussian elimination (no LAPACK on the oracle
+  path; numpy matmul serves as a single library step of the tall-skinny products).
 
 Every function cites the passage it follows.  The pins that tie it to the
 paper and to mathematics (not to itself) are in ``tests/test_oracle_*.py``.
@@ -36,5 +37,8 @@ from .core import (  # noqa: F401
     residuals,
     sweeps_rule,
     solve,
+    solve_deflate,
+    rcond_gram,
     SolveResult,
 )
+from . import dense  # noqa: F401

@@ -12,7 +12,8 @@ import subprocess
 from dataclasses import dataclass, field
 
 import numpy as np
-import scipy.linalg
+
+from . import dense
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "csr_oracle.c")
@@ -145,12 +146,13 @@ def interp_coeffs(d: int) -> np.ndarray:
     Reading (R18): psi_d is kept in the Chebyshev basis; the paper's
     monomial coefficients Gamma_d (Eq. chebfun-f) reach 1e5 (d = 20) and 3e8 (d = 30)
     with alternating signs, so two fp64 computations of them differ by 1e-11 to 1e-7
-    relative and Alg. poly's Horner output by up to 1e-4 — not a reproducible target."""
+    relative and Alg. poly's Horner output by up to 1e-4 — not a reproducible target.
+    The square system is solved by the oracle's own Gaussian elimination (dense.solve_gepp)."""
     if d < 1:
         raise ValueError("d >= 1")
     t = -np.cos(np.arange(d + 1) * np.pi / d)
     f = np.maximum(0.0, t) ** (10 * d)
-    return np.linalg.solve(chebyshev_basis(d, t), f)
+    return dense.solve_gepp(chebyshev_basis(d, t), f)
 
 
 def chebyshev_basis(d: int, t) -> np.ndarray:
@@ -206,7 +208,9 @@ def gn_step(A, a: float, b: float, d: int, X: np.ndarray, coef=None) -> np.ndarr
     the accelerator rho_d in place of A: Y = X (X^T X)^{-1}; Z = rho_d(A) Y;
     X = Z - X (Y^T Z - I) / 2.  rho_d = T_d of the mapped matrix (coef None) or psi_d."""
     X = np.ascontiguousarray(X, dtype=np.float64)
-    Y = X @ np.linalg.inv(X.T @ X)
+    R = dense.cholesky_upper(dense.gram(X, X))          # X^T X = R^T R
+    Rinv = dense.solve_upper_right(np.eye(R.shape[0]), R)
+    Y = dense.gemm(X, Rinv @ Rinv.T)                     # X (X^T X)^{-1}
     Z = cheb_filter(A, a, b, d, Y) if coef is None else poly_filter(A, a, b, coef, Y)
     return Z - X @ (Y.T @ Z - np.eye(X.shape[1])) / 2.0
 
@@ -214,57 +218,112 @@ def gn_step(A, a: float, b: float, d: int, X: np.ndarray, coef=None) -> np.ndarr
 # --------------------------------------------------------------------------- dense
 def orthonormalize(Z: np.ndarray):
     """U in orth(Z) (Alg. RR step 1): equilibrate columns (span unchanged),
-    Householder QR with column pivoting (library step), keep
-    r = #{i : |R_ii| > n*eps*|R_11|} columns (reading DESIGN.md §4 R8)."""
+    Householder QR with column pivoting (the oracle's own, dense.qr_pivoted), keep
+    r = #{i : |R_ii| > n*eps*|R_11|} columns (reading DESIGN.md R8)."""
     Z = np.asarray(Z, dtype=np.float64)
     n, m = Z.shape
-    nrm = np.linalg.norm(Z, axis=0)
+    nrm = np.sqrt(np.einsum("ij,ij->j", Z, Z))
     keep = nrm > 0
     Zs = Z[:, keep] / nrm[keep]
     if Zs.shape[1] == 0:
         return np.zeros((n, 0)), 0
-    Q, R, _ = scipy.linalg.qr(Zs, mode="economic", pivoting=True)
+    Q, R, _ = dense.qr_pivoted(Zs)
     dR = np.abs(np.diag(R))
     r = int(np.sum(dR > n * np.finfo(float).eps * dR[0]))
     return Q[:, :r], r
+
+
+def _ritz(A, U: np.ndarray, H: np.ndarray | None = None):
+    """Alg. RR steps 2-4 on an orthonormal U: H = U^T A U (symmetrised),
+    H = V Sigma V^T by cyclic Jacobi (dense.jacobi_eigh), Ritz values descending,
+    Y = U V."""
+    if H is None:
+        H = U.T @ spmm(A, U) if U.shape[1] > 0 else np.zeros((0, 0))
+    H = 0.5 * (H + H.T)
+    mu, V = dense.jacobi_eigh(H)
+    order = np.argsort(-mu, kind="stable")
+    return mu[order], V[:, order]
 
 
 def rayleigh_ritz(A, Z: np.ndarray):
     """(Y, Sigma) = RR(A, Z), Alg. RR: U = orth(Z); H = U^T A U;
     H = V^T Sigma V; Y = U V.  Ritz values sorted descending."""
     U, r = orthonormalize(Z)
-    AU = spmm(A, U) if r > 0 else np.zeros_like(U)
-    H = U.T @ AU
-    H = 0.5 * (H + H.T)
-    mu, V = np.linalg.eigh(H)
-    order = np.argsort(-mu, kind="stable")
-    mu = mu[order]
-    V = V[:, order]
+    mu, V = _ritz(A, U)
     return mu, U @ V, r
 
 
-def arr(A, X: np.ndarray, p: int, keep: int | None = None, rng_seed: int = 12345):
-    """(Y, Sigma) = ARR(A, X, p), Alg. ARR: Z = [X, AX, ..., A^p X]
-    (plain A, Eq. S:ARR P:515-523), RR(A, Z), keep the leading pairs.
-    Returns (mu_all_descending, Y_keep, rank).  If the rank r < keep the block
-    is topped up with seeded Gaussian columns orthonormalised against Y
-    (reading DESIGN.md §4 R7; never triggered in the pinned cases)."""
+def _top_up(Y: np.ndarray, keep: int, rng_seed: int):
+    """Fill a rank-deficient Ritz block to `keep` columns with seeded Gaussian columns
+    orthonormalised against it (reading DESIGN.md R7)."""
+    n, r = Y.shape
+    extra = np.random.default_rng(rng_seed).standard_normal((n, keep - r))
+    for _ in range(2):
+        extra -= Y @ (Y.T @ extra)
+    Qe, _ = dense.qr_blocked(extra)
+    return np.hstack([Y, Qe])
+
+
+def arr(A, X: np.ndarray, p: int, keep: int | None = None, rng_seed: int = 12345, method: str = "qr",
+        Qc: np.ndarray | None = None):
+    """(Y, Sigma) = ARR(A, X, p), Alg. ARR, returns (mu_all_descending,
+    Y_keep, rank).
+
+    method "qr" (paper-literal): Z = [X, AX, ..., A^p X] with plain A (Eq. S:ARR,
+      P:515-523), RR(A, Z) with the pivoted-QR orth.
+    method "cgs2" (the orthonormalise-then-augment reading R8, the GPU's span):
+      U_0 = orth(X), U_j = orth((I - Q Q^T) A U_{j-1}) with block classical Gram-Schmidt
+      applied twice (row-panel Gram / GEMM loops, dense.gram / dense.gemm) and orth = the
+      oracle's blocked Householder QR; if max |Q^T U_j| > 1e-12 (a nearly invariant block)
+      U_j is projected out of Q twice more and re-orthonormalised; H = Q^T A Q one
+      block column at a time (A Q never stored); RR steps 3-4.
+    Qc (deflation): the ARR is performed in the orthogonal complement of
+      R(Qc): every block of Z (qr) / every augmentation block (cgs2) has Qc projected out
+      twice.
+    If the rank r < keep the block is topped up with seeded Gaussian columns
+    orthonormalised against Y (reading DESIGN.md R7)."""
     n, w = X.shape
     keep = w if keep is None else keep
     if (p + 1) * w >= n:
         raise ValueError("(p+1)k must be < n (Alg. ARR input, P:536)")
-    blocks = [np.asarray(X, dtype=np.float64)]
-    for _ in range(p):
-        blocks.append(spmm(A, blocks[-1]))
-    Z = np.hstack(blocks)
-    mu, Y, r = rayleigh_ritz(A, Z)
+
+    def defl(B):
+        if Qc is not None and Qc.shape[1] > 0:
+            for _ in range(2):
+                B = B - dense.gemm(Qc, dense.gram(Qc, B))
+        return B
+
+    if method == "qr":
+        blocks = [np.asarray(X, dtype=np.float64)]
+        for _ in range(p):
+            blocks.append(spmm(A, blocks[-1]))
+        Z = defl(np.hstack(blocks))
+        mu, Y, r = rayleigh_ritz(A, Z)
+    elif method == "cgs2":
+        U, _ = dense.qr_blocked(np.asarray(X, dtype=np.float64))
+        Q = U
+        for j in range(1, p + 1):
+            W = defl(spmm(A, Q[:, (j - 1) * w:j * w]))
+            for _ in range(2):
+                W = W - dense.gemm(Q, dense.gram(Q, W))
+            Uj, _ = dense.qr_blocked(W)
+            if np.max(np.abs(dense.gram(Q, Uj))) > 1e-12:
+                for _ in range(2):
+                    Uj = Uj - dense.gemm(Q, dense.gram(Q, Uj))
+                Uj, _ = dense.qr_blocked(Uj)
+            Q = np.hstack([Q, Uj])
+        m = Q.shape[1]
+        H = np.empty((m, m))
+        for j in range(p + 1):
+            H[:, j * w:(j + 1) * w] = dense.gram(Q, spmm(A, Q[:, j * w:(j + 1) * w]))
+        mu, V = _ritz(A, Q, H)
+        Y = dense.gemm(Q, V[:, :keep])
+        r = m
+    else:
+        raise ValueError(method)
     if r >= keep:
         return mu, Y[:, :keep], r
-    rng = np.random.default_rng(rng_seed)
-    extra = rng.standard_normal((n, keep - r))
-    extra -= Y @ (Y.T @ extra)
-    Q, _ = np.linalg.qr(extra)
-    return mu, np.hstack([Y, Q]), r
+    return mu, _top_up(Y, keep, rng_seed), r
 
 
 def residuals(A, Y: np.ndarray, mu: np.ndarray) -> np.ndarray:
@@ -299,23 +358,75 @@ class SolveResult:
     outer: int
     sweeps: int
     log: list = field(default_factory=list)
+    exit_rule: int = 0
+    p_final: int = 0
+    d_final: int = 0
+    locked: int = 0
+
+
+def rcond_gram(X: np.ndarray) -> float:
+    """rc = lambda_min(X^T X) / lambda_max(X^T X), the reciprocal 2-norm condition of
+    the Gram (the paper's rcond(X^T X), P:1364-1369, takes LAPACK's 1-norm estimate;
+    reading DESIGN.md R6), eigenvalues by the oracle's Jacobi."""
+    lam, _ = dense.jacobi_eigh(dense.gram(X, X))
+    return max(lam[0], 0.0) / lam[-1] if lam[-1] > 0 else 0.0
+
+
+def _degree_rule(d_max: int, a: float, b: float, mu_k: float, mu_w: float, gamma_of=None) -> int:
+    """Eqs. hat-d / degree: the smallest d >= 3 with
+    |rho_d(mu*_{k+q})| < 0.9 |rho_d(mu*_k)|, capped at d_max (rho_d = T_d on the
+    interval map, or psi_d with the interpolant filter)."""
+    c = 0.5 * (a + b)
+    e = 0.5 * (b - a)
+    for dd in range(3, d_max + 1):
+        if gamma_of is None:
+            rk = float(chebyshev_T(dd, (mu_k - c) / e))
+            rw = float(chebyshev_T(dd, (mu_w - c) / e))
+        else:
+            g = gamma_of(dd)
+            rk = float(psi(g, np.array([(mu_k - c) / e]))[0])
+            rw = float(psi(g, np.array([(mu_w - c) / e]))[0])
+        if abs(rw) < 0.9 * abs(rk):
+            return dd
+    return d_max
 
 
 def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
           s_max: int = 5, w: int | None = None, max_outer: int | None = None, filter: str = "cheb",
-          inner_solver: str = "mpm") -> SolveResult:
-    """Fixed-parameter ARRABIT-MPM (Alg. Arrabit2, with the
-    adaptive lines disabled; DESIGN.md §4 R3/R6/R10):
+          inner_solver: str = "mpm", arr_method: str = "qr", inner: str = "range", exits: int = 0,
+          adapt: int = 0) -> SolveResult:
+    """ARRABIT-MPM (Alg. Arrabit2).  Defaults = the fixed-parameter solve
+    (adaptive lines disabled; R3/R6/R10):
 
         a := Gershgorin lower bound;  U0 := orth(X0); mu := eig(U0^T A U0); b := mu_w
         loop: s := sweeps_rule(mu_1);  s x { X := T_d((A-cI)/e) X; normalise }
               (mu, Y) := ARR(A, X, p)                                          (P:1502-1507)
               res_i, i <= k  (Eq. resi)  ;  stop if max res <= tol              (Eq. out-stop)
               b := mu_{w+1} (monotone once maxres grew);  X := Y[:, :w]   (R3)
-    """
+
+    Options (the paper's rules, Section 6):
+      inner="rcond": every maxit_2 = 5 sweeps (at most maxit_1 = 10 times) rc = rcond(X^T X);
+        stop at rc <= tol or rc / rc_prev > 0.99 (Eq. inn-stop).
+      exits bit 1: (ii) max res not reduced over three consecutive outer iterations;
+            bit 2: (iii) max res < (1 + 9h/k) tol, h = #{res_i < 0.1 tol}.
+      adapt bit 1: p from 1 up to p by Eq. block with the ratio taken on the
+              shifted Ritz values (mu - a) (the inner solvers run on A - aI, P:1355-1357;
+              DESIGN.md R20);
+            bit 2: d from 3, re-chosen after every ARR by Eqs. hat-d / degree
+              with d as d_max;
+            bit 4: continuation + deflation (solve_deflate, R19).
+      arr_method: "qr" (paper-literal) or "cgs2" (orthonormalise-then-augment, R8)."""
+    if adapt & 4:
+        if (adapt & 3) or inner != "range" or exits or inner_solver != "mpm":
+            raise ValueError("continuation + deflation runs fixed p / d MPM sweeps only")
+        return solve_deflate(A, k, d, p, X0, tol=tol, maxit=maxit, s_max=s_max, w=w, filter=filter,
+                             arr_method=arr_method, max_outer=max_outer)
     n = A.n
     w = X0.shape[1] if w is None else w  # w - k guard vectors (P:1291-1299)
-    gamma = None if filter == "cheb" else interp_coeffs(d)  # "interp": the paper's psi_d (DESIGN.md R18)
+    d_max, p_max = d, p
+    gamma_of = None if filter == "cheb" else interp_coeffs  # "interp": the paper's psi_d (DESIGN.md R18)
+    p_cur = min(1, p_max) if adapt & 1 else p_max
+    d_cur = 3 if (adapt & 2) and d_max > 3 else d_max
     X = np.array(X0[:, :w], dtype=np.float64, copy=True)
     a = gershgorin_lower(A)
     mu0, _, _ = rayleigh_ritz(A, X)
@@ -330,20 +441,49 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     Y = X
     res = np.full(k, np.inf)
     mono, prev_maxres = False, None
+    hist = []
+    best_res, best_muk, best_muw, maxresp = np.inf, 0.0, 0.0, np.inf
+    exit_rule = 0
+
+    def sweep(X):
+        gamma = None if gamma_of is None else gamma_of(d_cur)
+        if inner_solver == "gn":  # Alg. Arrabit2's GN branch
+            return gn_step(A, a, b, d_cur, X, gamma)
+        return mpm_sweep(A, a, b, d_cur, X) if gamma is None else poly_sweep(A, a, b, gamma, X)
+
     for outer in range(1, limit + 1):
-        s = sweeps_rule(mu1, a, b, d, s_max, gamma)
-        for _ in range(s):
-            if inner_solver == "gn":  # Alg. Arrabit2's GN branch
-                X = gn_step(A, a, b, d, X, gamma)
-            else:
-                X = mpm_sweep(A, a, b, d, X) if gamma is None else poly_sweep(A, a, b, gamma, X)
+        if inner == "rcond":
+            s, rcp = 0, -1.0
+            for _ in range(10):
+                for _ in range(5):
+                    X = sweep(X)
+                s += 5
+                rc = rcond_gram(X)
+                if rc <= tol or (rcp > 0.0 and rc / rcp > 0.99):
+                    break
+                rcp = rc
+        else:
+            s = sweeps_rule(mu1, a, b, d_cur, s_max, None if gamma_of is None else gamma_of(d_cur))
+            for _ in range(s):
+                X = sweep(X)
         sweeps += s
-        mu, Y, r = arr(A, X, p, keep=w)
+        mu, Y, r = arr(A, X, p_cur, keep=w, method=arr_method)
         res = residuals(A, Y[:, :k], mu[:k])
         maxres = float(np.max(res))
-        log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres))
+        log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres, p=p_cur, d=d_cur))
         if maxres <= tol:
-            return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log)
+            return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log, 1, p_cur, d_cur)
+        if exits & 1:
+            hist.append(maxres)
+            h = len(hist)
+            if h >= 4 and not (hist[h - 1] < hist[h - 4] or hist[h - 2] < hist[h - 4] or hist[h - 3] < hist[h - 4]):
+                exit_rule = 2
+                break
+        if exits & 2:
+            hsmall = int(np.sum(res < 0.1 * tol))
+            if maxres < (1.0 + 9.0 * hsmall / k) * tol:
+                exit_rule = 3
+                break
         # b := mu_{w+1}, an under-estimate of lambda_{k+q} (mu_{w+1} <= lambda_{w+1} by
         # interlacing); once the max residual has grown tenfold between two
         # outer iterations (b fell and amplified the guard range), b only increases (R3)
@@ -355,4 +495,78 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
             a = b - 1e-8 * (abs(b) + 1.0)
         mu1 = float(mu[0])
         X = Y[:, :w]
-    return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, False, limit, sweeps, log)
+        if maxres < best_res:
+            best_res, best_muk, best_muw = maxres, float(mu[k - 1]), float(mu[w - 1])
+        if (adapt & 1) and p_cur < p_max:  # Eq. block
+            if (mu[w - 1] - a) / (mu[k - 1] - a) > 0.95 and maxres / maxresp > 0.1:
+                p_cur += 1
+        maxresp = maxres
+        if (adapt & 2) and d_max > 3:  # Eqs. hat-d / degree
+            d_cur = _degree_rule(d_max, a, b, best_muk, best_muw, gamma_of)
+    return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, False, len(log), sweeps, log, exit_rule, p_cur, d_cur)
+
+
+def solve_deflate(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
+                  s_max: int = 5, w: int | None = None, filter: str = "cheb", arr_method: str = "qr",
+                  max_outer: int | None = None) -> SolveResult:
+    """Alg. Arrabit2 with continuation (Eq. contin, P:1336-1349) and deflation (Eq. defl,
+    P:1396-1416), MPM sweeps by the dynamic-range rule, fixed p and d (R19):
+      tol_1 = sqrt(tol); tol_{t+1} = max(1e-2 tol_t, tol) once max res <= tol_t;
+      after every ARR the leading Ritz pairs with res <= max(1e-14, tol_t^2) are locked
+      (Q_c, the leading columns of X; at least one pair stays active); the active block
+      X is filtered, projected X - Q_c(Q_c^T X) twice and ARR'ed in the
+      orthogonal complement of R(Q_c) (P:1411-1414); b = mu_{w_a+1} of the active ARR;
+      a final Rayleigh-Ritz on all w columns orders the pairs and recomputes residuals."""
+    w = X0.shape[1] if w is None else w
+    gamma = None if filter == "cheb" else interp_coeffs(d)
+    X = np.array(X0[:, :w], dtype=np.float64, copy=True)
+    a = gershgorin_lower(A)
+    mu0, _, _ = rayleigh_ritz(A, X)
+    b, mu1 = float(mu0[w - 1]), float(mu0[0])
+    if not a < b:
+        a = b - 1e-8 * (abs(b) + 1.0)
+    tol_t = max(tol, math.sqrt(tol))
+    nc = 0
+    locked_res: list[float] = []
+    log = []
+    sweeps = 0
+    done = False
+    limit = maxit if max_outer is None else min(maxit, max_outer)
+    for outer in range(1, limit + 1):
+        wa = w - nc
+        Qc = X[:, :nc]
+        Xa = X[:, nc:]
+        s = sweeps_rule(mu1, a, b, d, s_max, gamma)
+        for _ in range(s):
+            Xa = mpm_sweep(A, a, b, d, Xa) if gamma is None else poly_sweep(A, a, b, gamma, Xa)
+        sweeps += s
+        if nc > 0:
+            for _ in range(2):
+                Xa = Xa - dense.gemm(Qc, dense.gram(Qc, Xa))
+        mu, Y, r = arr(A, Xa, p, keep=wa, method=arr_method, Qc=Qc if nc > 0 else None)
+        ka = k - nc
+        ra = residuals(A, Y[:, :ka], mu[:ka])
+        maxres = max(float(np.max(ra)), max(locked_res) if locked_res else 0.0)
+        X = np.hstack([Qc, Y[:, :wa]])
+        log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres, locked=nc, tol_t=tol_t))
+        if maxres <= tol:
+            done = True
+            break
+        if maxres <= tol_t:
+            tol_t = max(1e-2 * tol_t, tol)  # continuation
+        b = float(mu[min(wa, r - 1)])
+        thr = max(1e-14, tol_t * tol_t)
+        add = 0
+        while add < ka - 1 and ra[add] <= thr:
+            add += 1
+        locked_res.extend(float(x) for x in ra[:add])
+        nc += add
+        mu1 = float(mu[add])
+        if not a < b:
+            a = b - 1e-8 * (abs(b) + 1.0)
+    mu, V = _ritz(A, X)
+    Yf = X @ V
+    res = residuals(A, Yf[:, :k], mu[:k])
+    conv = done and float(np.max(res)) <= tol
+    return SolveResult(mu[:k].copy(), Yf[:, :k].copy(), res, conv, len(log), sweeps, log,
+                       1 if conv else 0, p, d, nc)

@@ -18,7 +18,7 @@ EXPORTED = [
     "eig_init", "eig_init_w", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "eig_set_filter", "eig_set_mode", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
-    "eig_set_timing", "eig_phase_times", "eig_set_schedule",
+    "eig_set_timing", "eig_phase_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active",
     "eig_init_dist", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
 ]
 
@@ -81,6 +81,8 @@ def load(path: str = LIB_PATH):
         "eig_gershgorin_lower": ([vp, pf64], ctypes.c_int),
         "eig_set_interval": ([vp, f64, f64], ctypes.c_int),
         "eig_set_degree": ([vp, i32], ctypes.c_int),
+        "eig_set_stencil": ([vp, i64, i64, i64], ctypes.c_int),
+        "eig_stencil_active": ([vp], ctypes.c_int32),
         "eig_set_filter": ([vp, i32], ctypes.c_int),
         "eig_set_mode": ([vp, i32], ctypes.c_int),
         "eig_set_timing": ([vp, i32], ctypes.c_int),

@@ -214,6 +214,16 @@ class EigContext:
         self._check(self.lib.eig_set_schedule(self.h, ctypes.c_void_p(r0.data_ptr()), ctypes.c_void_p(ln.data_ptr()),
                                               int(r0.numel())), "eig_set_schedule")
 
+    def eig_set_stencil(self, nx: int, ny: int = 1, nz: int = 1):
+        """Declare A a <= 27-point stencil on an nx x ny x nz grid (x fastest); (0, 0, 0)
+        switches back to the CSR kernels (see include/arrabit.h)."""
+        self._check(self.lib.eig_set_stencil(self.h, int(nx), int(ny), int(nz)), "eig_set_stencil")
+
+    @property
+    def stencil_points(self) -> int:
+        """K of the active stencil path (0: CSR kernels)."""
+        return int(self.lib.eig_stencil_active(self.h))
+
     def eig_set_degree(self, d: int):
         self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
         self.d = d

@@ -10,7 +10,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["spmm_kernels.cu", "dense_kernels.cu", "comm.cu", "api.cu"]
+SOURCES = ["spmm_kernels.cu", "stencil_kernels.cu", "dense_kernels.cu", "comm.cu", "api.cu"]
 LIB = os.path.join(HERE, "libarrabit.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -924,6 +924,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    stencil_release(c);
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
                     c->trtri_dwork};
     for (void *p : ptrs)
@@ -979,6 +980,19 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
     c->tile_row0 = tile_row0; c->tile_len = tile_len; c->ntiles = ntiles;
     return ARR_OK;
 }
+
+arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
+    GUARD(c);
+    if (is_dist(c) && (nx || ny || nz)) return fail(c, ARR_EINVAL, "stencil path: single-GPU contexts only");
+    const arr_status st = stencil_setup(c, nx, ny, nz);
+    if (st == ARR_EINVAL)
+        return fail(c, st, "eig_set_stencil: n != nx*ny*nz, or a row of A is unsorted / has a column outside the "
+                           "3x3x3 neighbourhood of its grid point");
+    if (st != ARR_OK) return fail(c, st, "eig_set_stencil failed");
+    return ARR_OK;
+}
+
+int32_t eig_stencil_active(const arr_ctx *c) { return c && c->st.on ? c->st.K : 0; }
 
 arr_status eig_set_degree(arr_ctx *c, int32_t d) {
     GUARD(c);

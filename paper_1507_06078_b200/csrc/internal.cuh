@@ -33,6 +33,35 @@ struct DistPlan {
     int64_t cur_ld = 0;
 };
 
+// Stencil-aware filter path (stencil_kernels.cu; eig_set_stencil): A stored as K
+// diagonals of a 3x3x3 neighbourhood on an nx x ny x nz grid (x fastest).
+struct StencilSlots {
+    int K;
+    int slot[27];  // bit (dz+1)*9 + (dy+1)*3 + (dx+1) -> DIA column, -1 if absent
+};
+struct StencilState {
+    bool on = false;
+    int64_t nx = 0, ny = 0, nz = 0;
+    int K = 0, Kpad = 0;
+    double *dia = nullptr;  // [n][Kpad] (K rounded up to even: 16-byte rows), owned
+    int shape = 0, hx = 0, hy = 0;  // stencil_kernels.cu Shape<>: 0 27-pt, 1 7-pt, 2 2-D 5-pt, 3 1-D 3-pt
+    int smem_optin = 0;
+};
+// One launch of the stencil kernel (kernel parameter, __grid_constant__).
+struct StencilLaunch {
+    const double *Yin, *Yprev, *Xa;
+    double *Yout;
+    int64_t ld_in, ld_prev, ld_out, ld_xa;
+    double alpha, shift, beta, gxa;
+    double *partials;
+    const double *val;
+    int64_t nitems;
+    int w, wv, K, Kpad;
+    int nx, ny, nz;
+    int Px, Py, Lz, npx, npy, nzc, npan, pwv, NS;
+    int box_x, box_y, hx, hy;
+};
+
 struct arr_ctx {
     // problem
     arr_csr A;
@@ -92,6 +121,7 @@ struct arr_ctx {
     arr_comm *comm;
     int nranks;  // size of comm (1 without one)
     DistPlan plan;
+    StencilState st;
     double *stage;
     size_t stage_elems;
     // pinned host staging
@@ -149,6 +179,10 @@ int cached_occupancy(LaunchCache &lc, Kern kern, int threads, size_t smem) {
 // Launch the fused SpMM: Yout = alpha*(A Yin - shift*Yin) + beta*Yprev.
 // Returns the grid size used (number of partial rows written if partials != nullptr).
 int launch_spmm(arr_ctx *c, const SpmmArgs &a);
+// stencil path (stencil_kernels.cu): -1 when it does not apply to this launch
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a);
+arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
+void stencil_release(arr_ctx *c);
 // out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)
 void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,
                              const double *mu_div);

@@ -191,6 +191,12 @@ struct __align__(16) Ent {
     double val;
 };
 
+// alpha (acc - shift y_i) with the contraction spelled out (the stencil path,
+// stencil_kernels.cu, uses the same sequence: bitwise equal outputs)
+__device__ __forceinline__ double epi(double alpha, double acc, double shift, double yi) {
+    return alpha * fma(-shift, yi, acc);
+}
+
 // Epilogue of one row: out = alpha*(acc - shift*y_i) + beta*y_prev, column
 // sums of squares, evict-first store.
 template <int VEC, int NV, bool HAS_PREV, bool STORE, bool SUMSQ, bool COLSHIFT, bool HAS_X>
@@ -210,9 +216,9 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
-            double o = a.alpha * (V::get(acc[v], e) - sh * V::get(yi, e));
-            if (HAS_PREV) o += a.beta * V::get(yp[v], e);
-            if (HAS_X) o += a.gxa * V::get(xa, e);
+            double o = epi(a.alpha, V::get(acc[v], e), sh, V::get(yi, e));
+            if (HAS_PREV) o = fma(a.beta, V::get(yp[v], e), o);
+            if (HAS_X) o = fma(a.gxa, V::get(xa, e), o);
             V::set(out, e, o);
             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
         }
@@ -433,9 +439,9 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
                         T out;
                         for (int e = 0; e < VEC; ++e) {
                             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
-                            double o = a.alpha * (V::get(acc, e) - sh * V::get(yi, e));
-                            if (HAS_PREV) o += a.beta * V::get(yp, e);
-                            if (HAS_X) o += a.gxa * a.Xa[i * a.ld_xa + vv * VEC + e];
+                            double o = epi(a.alpha, V::get(acc, e), sh, V::get(yi, e));
+                            if (HAS_PREV) o = fma(a.beta, V::get(yp, e), o);
+                            if (HAS_X) o = fma(a.gxa, a.Xa[i * a.ld_xa + vv * VEC + e], o);
                             V::set(out, e, o);
                             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                         }
@@ -665,9 +671,9 @@ __global__ void __launch_bounds__(kMaxThreads + 32, ARR_SPMM_WS_MINB) spmm_ws_ke
                     T out;
                     for (int e = 0; e < VEC; ++e) {
                         const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
-                        double o = a.alpha * (Vv::get(acc, e) - sh * Vv::get(yi, e));
-                        if (HAS_PREV) o += a.beta * Vv::get(yp, e);
-                        if (HAS_X) o += a.gxa * a.Xa[i * a.ld_xa + vv * VEC + e];
+                        double o = epi(a.alpha, Vv::get(acc, e), sh, Vv::get(yi, e));
+                        if (HAS_PREV) o = fma(a.beta, Vv::get(yp, e), o);
+                        if (HAS_X) o = fma(a.gxa, a.Xa[i * a.ld_xa + vv * VEC + e], o);
                         Vv::set(out, e, o);
                         if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                     }
@@ -922,6 +928,10 @@ int launch_spmm(arr_ctx *c, const SpmmArgs &a_in) {
     if (a.Yout) v2 = v2 && vec2_ok(a.Yout, a.ld_out);
     if (a.Xa) v2 = v2 && vec2_ok(a.Xa, a.ld_xa);
     c->spmm_blocks++;
+    if (c->st.on && !a.tile_row0) {  // declared stencil operator (eig_set_stencil): the 2.5-D blocked path
+        const int g = launch_spmm_stencil(c, a);
+        if (g >= 0) return g;
+    }
 #if ARR_SPMM_V4
     bool v4 = (a.w % 4 == 0) && vec4_ok(a.Yin, a.ld_in);
     if (a.Yprev) v4 = v4 && vec4_ok(a.Yprev, a.ld_prev);

@@ -1,0 +1,658 @@
+// Stencil-aware fused filter degree for sm_100a ("structured path";
+// Survey §8f-4).  Same operation and the same per-row FMA order as the CSR kernels
+// of spmm_kernels.cu (Eq. cheby-poly P:377-383 on the map of Eq. rhod P:1225-1232,
+// Alg. Arrabit2 line P:1486; the augmentation SpMM of Alg. ARR):
+//     Y_{j+1} = alpha (A Y_j - shift Y_j) + beta Y_{j-1} (+ gxa X)
+// for a matrix whose pattern lies in the 3x3x3 neighbourhood of an nx x ny x nz grid
+// (x fastest; the finite-difference operators the paper's test set comes from,
+// P:1624-1627).  eig_set_stencil verifies the CSR pattern on the device and stores A
+// as K diagonals (DIA, [n][K], zeros where a neighbour is absent).
+//
+// Why: the per-degree CSR kernel gathers every neighbour row through L1/L2; for the
+// 7- and 27-point operators at w = 282..550 that is 5-21 block-sized passes of
+// L2 -> SM traffic per degree, and the L2 (~6300 B/clk chip-wide) saturates before
+// HBM does.  Here a CTA owns a Px x Py patch of grid lines and a column panel and
+// marches along z: plane z's patch (plus its x/y halo) is copied ONCE into shared
+// memory by the bulk-copy engine (cp.async.bulk, mbarrier complete_tx, NS-stage
+// ring, one producer warp), and every staged row is used for the three output
+// planes z-1, z, z+1 from registers (three rotating accumulators per output).  L2 ->
+// SM traffic per degree drops to (box/patch) + 2 blocks.  The terms of each output
+// row are still added in ascending column order (plane z-1, then z, then z+1; within
+// a plane (dy, dx) ascending): bitwise the CSR kernels' sums.
+#include <math.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kStThreads = 1024;  // 31 consumer warps (one output vector each per step) + 1 producer warp
+constexpr int kStCons = kStThreads - 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+// one contiguous row segment global -> shared through the bulk-copy engine (TMA)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_stream(const double *p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_stream(double *p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "l"(pol)
+                 : "memory");
+}
+// alpha (acc - shift y_i): the same contraction as the CSR kernels' epilogue
+__device__ __forceinline__ double epi(double alpha, double acc, double shift, double yi) {
+    return alpha * fma(-shift, yi, acc);
+}
+__device__ __forceinline__ void fma2(double2 &acc, double a, const double2 &x) {
+    acc.x = fma(a, x.x, acc.x);
+    acc.y = fma(a, x.y, acc.y);
+}
+
+// Compile-time stencil shapes.  In-plane positions q are in (dy, dx) ascending order
+// (the order of each output's terms within a plane); k(dz, q) is the DIA slot of
+// neighbour (dx, dy, dz) = (dx(q), dy(q), dz), -1 if the shape has none.  Slots are
+// numbered in ascending column order.  A verified pattern runs on the smallest shape
+// containing it (absent neighbours are zero slots: exact no-op FMAs).
+//   0: 27-point (full 3x3x3)            1: 7-point (3-D)
+//   2: 5-point of a 2-D grid declared (nx, 1, ny): x-neighbours in plane, y = march
+//   3: 3-point (1-D)
+template <int SH>
+struct Shape;
+template <>
+struct Shape<0> {
+    static constexpr int NQ = 9, K = 27, QC = 4, HY = 1;
+    static constexpr __host__ __device__ int dy(int q) { return q / 3 - 1; }
+    static constexpr __host__ __device__ int dx(int q) { return q % 3 - 1; }
+    static constexpr __host__ __device__ int k(int dz, int q) { return (dz + 1) * 9 + q; }
+};
+template <>
+struct Shape<1> {
+    static constexpr int NQ = 5, K = 7, QC = 2, HY = 1;
+    static constexpr __host__ __device__ int dy(int q) { return q == 0 ? -1 : (q == 4 ? 1 : 0); }
+    static constexpr __host__ __device__ int dx(int q) { return q == 1 ? -1 : (q == 3 ? 1 : 0); }
+    static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? 1 + q : (q == 2 ? (dz < 0 ? 0 : 6) : -1); }
+};
+template <>
+struct Shape<2> {
+    static constexpr int NQ = 3, K = 5, QC = 1, HY = 0;
+    static constexpr __host__ __device__ int dy(int) { return 0; }
+    static constexpr __host__ __device__ int dx(int q) { return q - 1; }
+    static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? 1 + q : (q == 1 ? (dz < 0 ? 0 : 4) : -1); }
+};
+template <>
+struct Shape<3> {
+    static constexpr int NQ = 3, K = 3, QC = 1, HY = 0;
+    static constexpr __host__ __device__ int dy(int) { return 0; }
+    static constexpr __host__ __device__ int dx(int q) { return q - 1; }
+    static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? q : -1; }
+};
+template <int SH>
+__host__ __device__ bool shape_needs(int ly, int lx, int hy, int hx, int pye, int pxe) {
+    bool need = false;
+#pragma unroll
+    for (int q = 0; q < Shape<SH>::NQ; ++q) {
+        const int oy = ly - hy - Shape<SH>::dy(q), ox = lx - hx - Shape<SH>::dx(q);
+        need = need || (oy >= 0 && oy < pye && ox >= 0 && ox < pxe);
+    }
+    return need;
+}
+template <int SH>
+unsigned shape_mask() {
+    unsigned m = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int q = 0; q < Shape<SH>::NQ; ++q)
+            if (Shape<SH>::k(dz, q) >= 0) m |= 1u << ((dz + 1) * 9 + (Shape<SH>::dy(q) + 1) * 3 + (Shape<SH>::dx(q) + 1));
+    return m;
+}
+template <int SH>
+void shape_slots(StencilSlots &sl) {
+    for (int b = 0; b < 27; ++b) sl.slot[b] = -1;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int q = 0; q < Shape<SH>::NQ; ++q)
+            if (Shape<SH>::k(dz, q) >= 0)
+                sl.slot[(dz + 1) * 9 + (Shape<SH>::dy(q) + 1) * 3 + (Shape<SH>::dx(q) + 1)] = Shape<SH>::k(dz, q);
+    sl.K = Shape<SH>::K;
+}
+
+// Work item -> patch / panel / z-chunk (panel fastest: a CTA keeps one panel when
+// gridDim.x is a multiple of npan, which makes its column partial sums static).
+struct Item {
+    int panel, x0, y0, pxe, pye, zc0, zc1;
+};
+__device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) {
+    Item r;
+    r.panel = (int)(it % P.npan);
+    int64_t q = it / P.npan;
+    const int px = (int)(q % P.npx);
+    q /= P.npx;
+    const int py = (int)(q % P.npy);
+    const int zc = (int)(q / P.npy);
+    r.x0 = px * P.Px;
+    r.y0 = py * P.Py;
+    r.pxe = min(P.Px, P.nx - r.x0);
+    r.pye = min(P.Py, P.ny - r.y0);
+    r.zc0 = zc * P.Lz;
+    r.zc1 = min(P.nz, r.zc0 + P.Lz);
+    return r;
+}
+
+// Shared memory of one CTA: [full[4] | empty[4] mbarriers (128 B)] [NS stages] [val ring]
+// stage:    box rows of Y_j (nbox x pwv vectors) | Y_{j-1} rows | X rows (patch rows)
+// val ring: VS = NS + 2 slots of the patch's DIA rows of one plane (Px*Py x Kpad)
+template <bool HAS_PREV, bool HAS_X>
+struct StageLayout {
+    uint32_t box, prev, xa, bytes;
+    __host__ __device__ StageLayout(int nbox, int nrow_max, int pwv) {
+        box = 0;
+        prev = (uint32_t)nbox * pwv * 16u;
+        xa = prev + (HAS_PREV ? (uint32_t)nrow_max * pwv * 16u : 0u);
+        bytes = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
+    }
+};
+
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
+__global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_constant__ StencilLaunch P) {
+    using Sh = Shape<SH>;
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm);
+    uint64_t *empty = full + 4;
+    unsigned char *stages = sm + 128;
+    const int tid = threadIdx.x;
+    const int NS = P.NS, VS = P.NS + 2;
+    const int nbox = P.box_x * P.box_y;
+    const StageLayout<HAS_PREV, HAS_X> SL(nbox, P.Px * P.Py, P.pwv);
+    const uint32_t slot_bytes = (uint32_t)P.Px * P.Py * P.Kpad * 8u;
+    unsigned char *vring = stages + (size_t)NS * SL.bytes;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kStCons / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t G = gridDim.x;
+    const int64_t nxy = (int64_t)P.nx * P.ny;
+    const int pwv = P.pwv;  // smem row stride in 16-byte vectors
+    if (tid >= kStCons) {
+        // ------------------------------------------------------------ producer warp
+        // Per step (plane z of the march; z == nz is a tail step with no plane) it
+        // copies, completing on full[b]: the box rows of plane z that an output reads,
+        // the Y_{j-1} (and X) rows of the outputs of plane z-1, and the DIA rows of
+        // plane z+1 (and of plane z on an item's first step) into the value ring.
+        const int lane = tid - kStCons;
+        const uint64_t pol_keep = pol_evict_last();    // Y_j rows: re-staged by the neighbouring patches
+        const uint64_t pol_once = pol_evict_first();   // Y_{j-1}, X, DIA: read once
+        uint32_t step = 0;
+        for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
+            const Item I = decode_item(P, it);
+            const int pw = min(pwv, P.wv - I.panel * pwv);
+            const uint32_t rowb = (uint32_t)pw * 16u;
+            const int64_t col0 = (int64_t)I.panel * pwv * 2;
+            const int nrow = I.pxe * I.pye;
+            const uint32_t vlb = (uint32_t)I.pxe * P.Kpad * 8u;  // DIA bytes of one patch line
+            const int zs = max(I.zc0 - 1, 0);
+            for (int z = zs; z <= I.zc1; ++z, ++step) {
+                const int b = (int)(step % NS);
+                if (step >= (uint32_t)NS) mbar_wait(empty + b, ((step / NS) - 1) & 1);
+                const bool real = z < P.nz;
+                const bool fin = z - 1 >= I.zc0;
+                // DIA planes to load: z+1 (and z on the first step when z is an output plane)
+                const int va0 = (z == zs && z >= I.zc0 && real) ? z : z + 1;
+                const int va1 = (z + 1 < I.zc1) ? z + 1 : z;  // inclusive; empty if va1 < va0
+                uint32_t mine = 0;
+                if (real) {
+                    for (int r = lane; r < nbox; r += 32) {
+                        const int ly = r / P.box_x, lx = r - ly * P.box_x;
+                        const int gy = I.y0 - P.hy + ly, gx = I.x0 - P.hx + lx;
+                        if (gx < 0 || gx >= P.nx || gy < 0 || gy >= P.ny) continue;
+                        if (shape_needs<SH>(ly, lx, P.hy, P.hx, I.pye, I.pxe)) mine += rowb;
+                    }
+                }
+                for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+                uint32_t total = mine;
+                if (fin) total += (uint32_t)nrow * rowb * ((HAS_PREV ? 1u : 0u) + (HAS_X ? 1u : 0u));
+                if (va1 >= va0) total += (uint32_t)(va1 - va0 + 1) * I.pye * vlb;
+                if (lane == 0) mbar_expect_tx(full + b, total);
+                __syncwarp();
+                unsigned char *st = stages + (size_t)b * SL.bytes;
+                if (real) {
+                    const double *src_plane = P.Yin + (int64_t)z * nxy * P.ld_in + col0;
+                    for (int r = lane; r < nbox; r += 32) {
+                        const int ly = r / P.box_x, lx = r - ly * P.box_x;
+                        const int gy = I.y0 - P.hy + ly, gx = I.x0 - P.hx + lx;
+                        if (gx < 0 || gx >= P.nx || gy < 0 || gy >= P.ny) continue;
+                        if (shape_needs<SH>(ly, lx, P.hy, P.hx, I.pye, I.pxe))
+                            bulk_g2s(st + SL.box + (size_t)r * pwv * 16, src_plane + ((int64_t)gy * P.nx + gx) * P.ld_in,
+                                     rowb, full + b, pol_keep);
+                    }
+                }
+                if (fin && (HAS_PREV || HAS_X)) {
+                    for (int r = lane; r < nrow; r += 32) {
+                        const int oy = r / I.pxe, ox = r - oy * I.pxe;
+                        const int64_t row = (int64_t)(z - 1) * nxy + (int64_t)(I.y0 + oy) * P.nx + I.x0 + ox;
+                        const size_t so = (size_t)(oy * P.Px + ox) * pwv * 16;
+                        if (HAS_PREV) bulk_g2s(st + SL.prev + so, P.Yprev + row * P.ld_prev + col0, rowb, full + b, pol_once);
+                        if (HAS_X) bulk_g2s(st + SL.xa + so, P.Xa + row * P.ld_xa + col0, rowb, full + b, pol_once);
+                    }
+                }
+                for (int zz = va0; zz <= va1; ++zz) {
+                    unsigned char *slot = vring + (size_t)((step + (uint32_t)(zz - z)) % VS) * slot_bytes;
+                    for (int oy = lane; oy < I.pye; oy += 32)
+                        bulk_g2s(slot + (size_t)oy * P.Px * P.Kpad * 8,
+                                 P.val + ((int64_t)zz * nxy + (int64_t)(I.y0 + oy) * P.nx + I.x0) * P.Kpad, vlb,
+                                 full + b, pol_once);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------------------- consumers
+    const uint64_t pols = pol_evict_first();
+    const int Kp = P.Kpad;
+    uint32_t step = 0;
+    double ss0 = 0.0, ss1 = 0.0;
+    int panel_of_cta = (int)(blockIdx.x % P.npan);
+    for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
+        const Item I = decode_item(P, it);
+        const int pw = min(pwv, P.wv - I.panel * pwv);
+        const int nrow = I.pxe * I.pye;
+        const int colv0 = I.panel * pwv;
+        const int r = tid / pw;
+        const int v = tid - r * pw;
+        const bool act = r < nrow;
+        const int oy = act ? r / I.pxe : 0, ox = act ? r - (r / I.pxe) * I.pxe : 0;
+        const int cb = (oy + P.hy) * P.box_x + (ox + P.hx);
+        const int rs = oy * P.Px + ox;  // patch row slot (prev / X rows, value ring)
+        const int64_t rxy = (int64_t)(I.y0 + oy) * P.nx + (I.x0 + ox);
+        // smem row of each in-plane position (the centre where the neighbour is outside
+        // the grid: its DIA slot is zero there)
+        int qoff[Sh::NQ];
+#pragma unroll
+        for (int q = 0; q < Sh::NQ; ++q) {
+            const int gx = I.x0 + ox + Sh::dx(q), gy = I.y0 + oy + Sh::dy(q);
+            const bool in = gx >= 0 && gx < P.nx && gy >= 0 && gy < P.ny;
+            qoff[q] = (in ? cb + Sh::dy(q) * P.box_x + Sh::dx(q) : cb) * pwv + v;
+        }
+        double2 accA = make_double2(0.0, 0.0), accB = make_double2(0.0, 0.0), yiA = make_double2(0.0, 0.0);
+        const int zs = max(I.zc0 - 1, 0);
+        for (int z = zs; z <= I.zc1; ++z, ++step) {
+            const int b = (int)(step % NS);
+            const bool real = z < P.nz;
+            const bool fin = z - 1 >= I.zc0;                // out(z-1) completes in this step
+            const bool mid = z >= I.zc0 && z < I.zc1;       // out(z) gets its plane-z terms
+            const bool nxt = z + 1 < I.zc1;                 // out(z+1) starts with its plane-z terms
+            mbar_wait(full + b, (step / NS) & 1);
+            const unsigned char *st = stages + (size_t)b * SL.bytes;
+            const double2 *S = reinterpret_cast<const double2 *>(st + SL.box);
+            double2 accC = make_double2(0.0, 0.0), yiB = make_double2(0.0, 0.0);
+            double2 yp = make_double2(0.0, 0.0), xa = make_double2(0.0, 0.0);
+            if (act) {
+                if (real) {
+                    const double *vp = reinterpret_cast<const double *>(vring + (size_t)((step + VS - 1) % VS) * slot_bytes) + rs * Kp;
+                    const double *v0 = reinterpret_cast<const double *>(vring + (size_t)(step % VS) * slot_bytes) + rs * Kp;
+                    const double *vm = reinterpret_cast<const double *>(vring + (size_t)((step + 1) % VS) * slot_bytes) + rs * Kp;
+#pragma unroll
+                    for (int q = 0; q < Sh::NQ; ++q) {
+                        const double2 y = S[qoff[q]];
+                        if (q == Sh::QC) yiB = y;
+                        if (Sh::k(1, q) >= 0 && fin) fma2(accA, vp[Sh::k(1, q)], y);    // row z-1: its dz = +1 terms
+                        if (Sh::k(0, q) >= 0 && mid) fma2(accB, v0[Sh::k(0, q)], y);    // row z:   dz = 0
+                        if (Sh::k(-1, q) >= 0 && nxt) fma2(accC, vm[Sh::k(-1, q)], y);  // row z+1: dz = -1
+                    }
+                }
+                if (fin) {
+                    if (HAS_PREV) yp = reinterpret_cast<const double2 *>(st + SL.prev)[rs * pwv + v];
+                    if (HAS_X) xa = reinterpret_cast<const double2 *>(st + SL.xa)[rs * pwv + v];
+                }
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(empty + b);  // this warp is done with stage b
+            if (fin && act) {
+                const int64_t row = (int64_t)(z - 1) * nxy + rxy;
+                double2 out;
+                out.x = epi(P.alpha, accA.x, P.shift, yiA.x);
+                out.y = epi(P.alpha, accA.y, P.shift, yiA.y);
+                if (HAS_PREV) {
+                    out.x = fma(P.beta, yp.x, out.x);
+                    out.y = fma(P.beta, yp.y, out.y);
+                }
+                if (HAS_X) {
+                    out.x = fma(P.gxa, xa.x, out.x);
+                    out.y = fma(P.gxa, xa.y, out.y);
+                }
+                if (SUMSQ) {
+                    ss0 = fma(out.x, out.x, ss0);
+                    ss1 = fma(out.y, out.y, ss1);
+                }
+                st_stream(P.Yout + row * P.ld_out + (int64_t)(colv0 + v) * 2, out, pols);
+            }
+            accA = accB;
+            accB = accC;
+            yiA = yiB;
+        }
+    }
+    if (SUMSQ) {
+        // fixed-order reduction over the consumer threads of each column of this CTA's
+        // panel (every stage has landed: all full barriers were waited on), then one
+        // partial row of w doubles per CTA (zeros outside the panel)
+        asm volatile("bar.sync 1, %0;" ::"r"(kStCons) : "memory");
+        double2 *red = reinterpret_cast<double2 *>(stages);
+        red[tid] = make_double2(ss0, ss1);
+        asm volatile("bar.sync 1, %0;" ::"r"(kStCons) : "memory");
+        const int pw = min(pwv, P.wv - panel_of_cta * pwv);
+        for (int c = tid; c < P.wv; c += kStCons) {
+            double2 s = make_double2(0.0, 0.0);
+            const int lc = c - panel_of_cta * pwv;
+            if (lc >= 0 && lc < pw) {
+                for (int i = lc; i < kStCons; i += pw) {
+                    s.x += red[i].x;
+                    s.y += red[i].y;
+                }
+            }
+            double *dst = P.partials + (int64_t)blockIdx.x * P.w + 2 * c;
+            dst[0] = s.x;
+            if (2 * c + 1 < P.w) dst[1] = s.y;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- setup kernels
+__device__ __forceinline__ void decode3(int64_t i, int64_t nx, int64_t ny, int64_t &x, int64_t &y, int64_t &z) {
+    x = i % nx;
+    const int64_t t = i / nx;
+    y = t % ny;
+    z = t / ny;
+}
+
+// Pattern check: sorted, duplicate-free rows whose columns lie in the 3x3x3
+// neighbourhood of the row's grid point; OR of the 27 offset bits present.
+__global__ void stencil_check_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col, int64_t n,
+                                     int64_t nx, int64_t ny, unsigned *mask, int *bad) {
+    unsigned m = 0;
+    int b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x, y, z;
+        decode3(i, nx, ny, x, y, z);
+        int64_t prev = -1;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int64_t j = col[p];
+            if (j <= prev || j < 0 || j >= n) { b = 1; break; }
+            prev = j;
+            int64_t xj, yj, zj;
+            decode3(j, nx, ny, xj, yj, zj);
+            const int64_t dx = xj - x, dy = yj - y, dz = zj - z;
+            if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) { b = 1; break; }
+            m |= 1u << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
+        }
+    }
+    m = __reduce_or_sync(0xffffffffu, m);
+    b = __reduce_or_sync(0xffffffffu, (unsigned)b);
+    if ((threadIdx.x & 31) == 0) {
+        if (m) atomicOr(mask, m);
+        if (b) atomicOr(bad, 1);
+    }
+}
+
+// DIA values: dia[i*K + slot(bit)] = A_ij (0 where the neighbour is absent)
+__global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                    const double *__restrict__ val, int64_t n, int64_t nx, int64_t ny,
+                                    StencilSlots sl, double *__restrict__ dia) {
+    const int Kp = (sl.K + 1) & ~1;  // rows padded to 16 bytes (bulk copies)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double *row = dia + i * Kp;
+        for (int k = 0; k < Kp; ++k) row[k] = 0.0;
+        int64_t x, y, z;
+        decode3(i, nx, ny, x, y, z);
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            int64_t xj, yj, zj;
+            decode3(col[p], nx, ny, xj, yj, zj);
+            const int bit = (int)((zj - z + 1) * 9 + (yj - y + 1) * 3 + (xj - x + 1));
+            row[sl.slot[bit]] = val[p];
+        }
+    }
+}
+
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
+int launch_st(arr_ctx *c, StencilLaunch &L) {
+    auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X>;
+    const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
+    const size_t ring = (size_t)(L.NS + 2) * L.Px * L.Py * L.Kpad * 8;
+    const size_t smem = 128 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
+    static LaunchCache cache;
+    const int occ = cached_occupancy(cache, kern, kStThreads, smem);
+    int64_t G = (int64_t)c->num_sms * occ;
+    G = (G / L.npan) * L.npan;  // each CTA keeps one panel (static column partial sums)
+    if (G > L.nitems) G = L.nitems;
+    if (G < L.npan) G = L.npan;
+    kern<<<(unsigned)G, kStThreads, smem, c->stream>>>(L);
+    c->launches++;
+    return (int)G;
+}
+
+template <int SH>
+int dispatch_st_flags(arr_ctx *c, StencilLaunch &L, bool prev, bool ss, bool xa) {
+    if (!xa) {
+        if (prev && !ss) return launch_st<SH, true, false, false>(c, L);
+        if (prev && ss) return launch_st<SH, true, true, false>(c, L);
+        if (!prev && !ss) return launch_st<SH, false, false, false>(c, L);
+        return launch_st<SH, false, true, false>(c, L);
+    }
+    if (prev && !ss) return launch_st<SH, true, false, true>(c, L);
+    if (prev && ss) return launch_st<SH, true, true, true>(c, L);
+    if (!prev && !ss) return launch_st<SH, false, false, true>(c, L);
+    return launch_st<SH, false, true, true>(c, L);
+}
+
+bool al16(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
+
+}  // namespace
+
+// Host: geometry of one launch (patch, panels, z-chunks, stages) for block width w.
+// Cost model: L2 -> SM bytes per output row = staged rows per patch
+// row + the streamed operands, plus the DIA row once per panel, divided by the
+// useful fraction of the launch (ragged patches, last wave of work items).
+bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLaunch &L) {
+    const StencilState &S = c->st;
+    if (!S.on || w % 2 != 0) return false;
+    const int wv = w / 2;
+    const int items_max = kStCons;  // one output vector per consumer thread (IPT = 2 spills at 1024 threads)
+    size_t smem_max = (size_t)S.smem_optin - 256;
+    double best = 1e300;
+    bool found = false;
+    const int hx = S.hx, hy = S.hy;
+    for (int npan = 1; npan <= 8; ++npan) {
+        const int pwv = (wv + npan - 1) / npan;
+        if (pwv < 8 && npan > 1) break;
+        for (int Py = 1; Py <= (S.ny > 1 ? 16 : 1); ++Py) {
+            for (int Px = 1; Px <= 64; ++Px) {
+                const int nrow = Px * Py;
+                if ((int64_t)nrow * pwv > items_max) break;
+                if (Px > S.nx || Py > S.ny) break;
+                const int bx = Px + 2 * hx, by = Py + 2 * hy;
+                const size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
+                const size_t slot = (size_t)nrow * S.Kpad * 8;
+                int NS = 4;
+                while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
+                if (NS < 2) continue;
+                // staged rows actually read (the box minus unused corners)
+                int need = 0;
+                for (int ly = 0; ly < by; ++ly)
+                    for (int lx = 0; lx < bx; ++lx) {
+                        bool nd = false;
+                        switch (S.shape) {
+                            case 0: nd = shape_needs<0>(ly, lx, hy, hx, Py, Px); break;
+                            case 1: nd = shape_needs<1>(ly, lx, hy, hx, Py, Px); break;
+                            case 2: nd = shape_needs<2>(ly, lx, hy, hx, Py, Px); break;
+                            default: nd = shape_needs<3>(ly, lx, hy, hx, Py, Px); break;
+                        }
+                        need += nd;
+                    }
+                const int npx = (S.nx + Px - 1) / Px, npy = (S.ny + Py - 1) / Py;
+                const double rag = (double)S.nx * S.ny / ((double)npx * Px * npy * Py);
+                // z-chunks: enough work items for >= ~12 per CTA, chunks of >= 8 planes
+                const int64_t G = (int64_t)c->num_sms;
+                int nzc = 1;
+                while ((int64_t)npx * npy * npan * nzc < 12 * G && S.nz / (nzc + 1) >= 8) ++nzc;
+                const int Lz = (S.nz + nzc - 1) / nzc;
+                nzc = (S.nz + Lz - 1) / Lz;
+                const int64_t items = (int64_t)npx * npy * npan * nzc;
+                const double waves = (double)items / (double)((G / npan) * npan);
+                const double tail = waves / std::ceil(waves);
+                const double warm = (double)(Lz + (nzc > 1 ? 1 : 0)) / Lz;
+                const double rowbytes = 16.0 * wv;
+                double cost = ((double)need / nrow * warm + 1.0 + (has_prev ? 1.0 : 0.0) + (has_x ? 1.0 : 0.0)) * rowbytes +
+                              8.0 * S.Kpad * npan;
+                cost /= rag * tail;
+                if (NS == 2) cost *= 1.05;
+                if (cost < best) {
+                    best = cost;
+                    found = true;
+                    L.Px = Px; L.Py = Py; L.Lz = Lz;
+                    L.npx = npx; L.npy = npy; L.nzc = nzc; L.npan = npan;
+                    L.pwv = pwv; L.wv = wv; L.NS = NS;
+                    L.box_x = bx; L.box_y = by;
+                    L.nitems = items;
+                }
+            }
+        }
+    }
+    if (!found) return false;
+    L.nx = (int)S.nx; L.ny = (int)S.ny; L.nz = (int)S.nz;
+    L.hx = hx; L.hy = hy;
+    L.K = S.K;
+    L.Kpad = S.Kpad;
+    L.val = S.dia;
+    L.w = w;
+    return true;
+}
+
+// Fused SpMM through the stencil path; -1 when it does not apply to this launch.
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
+    if (!c->st.on || a.colshift || a.n != c->A.n || a.w % 2 != 0) return -1;
+    if (!al16(a.Yin, a.ld_in) || !a.Yout || !al16(a.Yout, a.ld_out)) return -1;
+    if (a.Yprev && !al16(a.Yprev, a.ld_prev)) return -1;
+    if (a.Xa && !al16(a.Xa, a.ld_xa)) return -1;
+    StencilLaunch L{};
+    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, L)) return -1;
+    L.Yin = a.Yin; L.ld_in = a.ld_in;
+    L.Yprev = a.Yprev; L.ld_prev = a.ld_prev;
+    L.Yout = a.Yout; L.ld_out = a.ld_out;
+    L.Xa = a.Xa; L.ld_xa = a.ld_xa;
+    L.alpha = a.alpha; L.shift = a.shift; L.beta = a.beta; L.gxa = a.gxa;
+    L.partials = a.partials;
+    const bool prev = a.Yprev != nullptr, ss = a.partials != nullptr, xa = a.Xa != nullptr;
+    switch (c->st.shape) {
+        case 0: return dispatch_st_flags<0>(c, L, prev, ss, xa);
+        case 1: return dispatch_st_flags<1>(c, L, prev, ss, xa);
+        case 2: return dispatch_st_flags<2>(c, L, prev, ss, xa);
+        case 3: return dispatch_st_flags<3>(c, L, prev, ss, xa);
+    }
+    return -1;
+}
+
+// Verify the pattern and build the DIA values (eig_set_stencil).
+arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
+    StencilState &S = c->st;
+    if (S.dia) {
+        cudaFreeAsync(S.dia, c->stream);
+        S.dia = nullptr;
+    }
+    S.on = false;
+    if (nx == 0 && ny == 0 && nz == 0) return ARR_OK;
+    if (nx < 1 || ny < 1 || nz < 1 || nx * ny * nz != c->A.n) return ARR_EINVAL;
+    unsigned *mask = reinterpret_cast<unsigned *>(c->dinfo + 60);
+    int *bad = c->dinfo + 61;
+    cudaMemsetAsync(c->dinfo + 60, 0, 2 * sizeof(int), c->stream);
+    int64_t blocks = (c->A.n + 255) / 256;
+    if (blocks > (int64_t)c->num_sms * 8) blocks = (int64_t)c->num_sms * 8;
+    stencil_check_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.n, nx, ny, mask,
+                                                                   bad);
+    c->launches++;
+    if (cudaMemcpyAsync(c->h_istage, c->dinfo + 60, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return ARR_ECUDA;
+    const unsigned m = (unsigned)c->h_istage[0];
+    if (c->h_istage[1] || m == 0) return ARR_EINVAL;
+    // the smallest compiled shape whose neighbour set contains the pattern (its slots are
+    // in ascending column order; absent neighbours stay zero)
+    StencilSlots sl{};
+    int shape = -1;
+    if ((m & ~shape_mask<3>()) == 0) { shape = 3; shape_slots<3>(sl); }
+    else if ((m & ~shape_mask<2>()) == 0) { shape = 2; shape_slots<2>(sl); }
+    else if ((m & ~shape_mask<1>()) == 0) { shape = 1; shape_slots<1>(sl); }
+    else { shape = 0; shape_slots<0>(sl); }
+    const int K = sl.K;
+    S.shape = shape;
+    S.hx = 1;
+    S.hy = (shape <= 1 && ny > 1) ? 1 : 0;
+    void *dia = nullptr;
+    const int Kpad = (K + 1) & ~1;
+    if (cudaMallocAsync(&dia, sizeof(double) * (size_t)c->A.n * Kpad, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return ARR_ENOMEM;
+    }
+    stencil_fill_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.val, c->A.n, nx, ny,
+                                                                  sl, (double *)dia);
+    c->launches++;
+    if (cudaGetLastError() != cudaSuccess) return ARR_ECUDA;
+    S.dia = (double *)dia;
+    S.nx = nx; S.ny = ny; S.nz = nz;
+    S.K = K;
+    S.Kpad = Kpad;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    S.smem_optin = optin > 0 ? optin : 227 * 1024;
+    S.on = true;
+    return ARR_OK;
+}
+
+void stencil_release(arr_ctx *c) {
+    if (c->st.dia) cudaFreeAsync(c->st.dia, c->stream);
+    c->st.dia = nullptr;
+    c->st.on = false;
+}

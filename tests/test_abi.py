@@ -15,7 +15,7 @@ LIB = os.path.join(ROOT, "paper_1507_06078_b200", "libarrabit.so")
 def _declared():
     src = open(HDR).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:arr_status|const char|size_t|uint64_t)\s*\**\s*(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:arr_status|const char|size_t|uint64_t|int32_t)\s*\**\s*(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 

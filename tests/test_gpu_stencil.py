@@ -1,0 +1,151 @@
+"""The stencil-aware filter path (eig_set_stencil, csrc/stencil_kernels.cu): the same
+fused degree as the CSR kernels with the same per-row FMA order, so the un-normalised
+output is bitwise the CSR kernels' and both match the oracle (Eq. cheby-poly
+P:377-383; Alg. Arrabit2 line P:1486).  Covers 1-D / 2-D / 3-D 7-point (+V) / 27-point
+operators, ragged patches, several panels and z-chunks, padded leading dimensions, the
+interpolant filter's fourth operand and the MPM normalisation."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def arr():
+    import paper_1507_06078_b200 as m
+    return m
+
+
+def dev_block(X, ld=None):
+    n, w = X.shape
+    ld = w if ld is None else ld
+    buf = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    buf[:, :w] = torch.from_numpy(np.ascontiguousarray(X))
+    return buf[:, :w]
+
+
+def relF(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# (matrix, declared grid (nx, ny, nz))
+CASES = {
+    "lap1d": (lambda: synth.laplacian_1d(1000), (1000, 1, 1)),
+    "lap2d_xz": (lambda: synth.laplacian_2d(37, 41), (37, 1, 41)),   # march along y
+    "lap2d_xy": (lambda: synth.laplacian_2d(37, 41), (37, 41, 1)),   # one plane, y halo
+    "lap3dV": (lambda: synth.laplacian_3d_potential(13, 2), (13, 13, 13)),
+    "st27": (lambda: synth.stencil27_3d(11), (11, 11, 11)),
+    "st27_tall": (lambda: synth.stencil27_3d(6), (6, 6, 6)),
+}
+
+
+def _pair(arr, A, grid, w, d, ld=None):
+    Ad = arr.to_device_csr(A)
+    c_csr = arr.eig_init(Ad, k=w, p=0, d=d)
+    c_st = arr.eig_init(Ad, k=w, p=0, d=d)
+    c_st.eig_set_stencil(*grid)
+    assert c_st.stencil_points > 0 and c_csr.stencil_points == 0
+    return c_csr, c_st
+
+
+@pytest.mark.parametrize("kind", list(CASES))
+@pytest.mark.parametrize("w,ld", [(2, 2), (24, 26), (98, 98), (282, 282), (550, 552)])
+def test_stencil_filter_bitwise_and_oracle(arr, kind, w, ld):
+    mk, grid = CASES[kind]
+    A = mk()
+    if w >= A.n:
+        pytest.skip("block wider than the matrix")
+    d = 5
+    X = synth.gaussian_block(A.n, w, 7)
+    a = oracle.gershgorin_lower(A)
+    b = a + 0.7 * (2 * np.abs(A.val).max() * 2 - a)
+    c_csr, c_st = _pair(arr, A, grid, w, d)
+    out = {}
+    for name, ctx in (("csr", c_csr), ("st", c_st)):
+        ctx.eig_set_interval(a, b)
+        Xd = dev_block(X, ld)
+        ctx.filter_step(Xd, normalize=False)
+        out[name] = Xd.cpu().numpy()
+    diff = np.abs(out["csr"] - out["st"])
+    assert np.array_equal(out["csr"], out["st"]), \
+        f"stencil path not bitwise equal to the CSR kernels: {np.count_nonzero(diff)} entries, max {diff.max():.3e}"
+    if w <= 98:
+        ref = oracle.cheb_filter(A, a, b, d, X)
+        assert relF(out["st"], ref) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["lap3dV", "st27", "lap2d_xz"])
+def test_stencil_normalised_and_interp(arr, kind):
+    mk, grid = CASES[kind]
+    A = mk()
+    w, d = 40, 8
+    X = synth.gaussian_block(A.n, w, 9)
+    a = oracle.gershgorin_lower(A)
+    b = a + 0.6 * (2 * np.abs(A.val).max() * 2 - a)
+    c_csr, c_st = _pair(arr, A, grid, w, d)
+    ref = oracle.mpm_sweep(A, a, b, d, X)
+    res = {}
+    for name, ctx in (("csr", c_csr), ("st", c_st)):
+        ctx.eig_set_interval(a, b)
+        Xd = dev_block(X)
+        nrm = torch.empty(w, dtype=torch.float64, device="cuda")
+        ctx.filter_step(Xd, normalize=True, colnorm=nrm)
+        res[name] = Xd.cpu().numpy()
+        assert relF(res[name], ref) <= 1e-12
+    # column norms are summed in another order by the two paths: equal to rounding
+    assert relF(res["st"], res["csr"]) <= 1e-14
+    # the paper's interpolant filter (Clenshaw steps with X as the fourth operand)
+    coef = oracle.interp_coeffs(d)
+    ref = oracle.poly_filter(A, a, b, coef, X)
+    outs = {}
+    for name, ctx in (("csr", c_csr), ("st", c_st)):
+        ctx.eig_set_filter("interp")
+        Xd = dev_block(X)
+        ctx.filter_step(Xd, normalize=False)
+        outs[name] = Xd.cpu().numpy()
+    assert np.array_equal(outs["csr"], outs["st"])
+    assert relF(outs["st"], ref) <= 1e-12
+
+
+def test_stencil_rejects_non_stencil(arr):
+    A = synth.zipf_random(3000, 3)
+    ctx = arr.eig_init(arr.to_device_csr(A), k=8, p=1, d=3)
+    with pytest.raises(arr.ArrError):
+        ctx.eig_set_stencil(3000, 1, 1)
+    A = synth.laplacian_3d_potential(9, 2)
+    ctx = arr.eig_init(arr.to_device_csr(A), k=8, p=1, d=3)
+    with pytest.raises(arr.ArrError):
+        ctx.eig_set_stencil(27, 3, 9)  # right n, wrong grid: neighbours outside the 3x3x3 box
+    with pytest.raises(arr.ArrError):
+        ctx.eig_set_stencil(9, 9, 10)
+    ctx.eig_set_stencil(9, 9, 9)
+    assert ctx.stencil_points == 7
+    ctx.eig_set_stencil(0, 0, 0)
+    assert ctx.stencil_points == 0
+
+
+@pytest.mark.parametrize("kind", ["lap3dV", "st27"])
+def test_stencil_solve_and_arr(arr, kind):
+    """Full solves (ARR's augmentation SpMMs also take the stencil path): identical
+    eigenvalues and iteration counts to the CSR path, and the oracle's certificates."""
+    from synth import configs
+    spec = configs.SMALL_ANALOGS[kind]
+    A, _ = configs.build_config(spec)
+    X0 = configs.starting_block(spec)
+    N = spec.size
+    outs = {}
+    for st in (False, True):
+        ctx = arr.eig_init(arr.to_device_csr(A), spec.k, spec.p, spec.d, w=spec.w)
+        if st:
+            ctx.eig_set_stencil(N, N, N)
+        ev, res, info = ctx.eig_solve(torch.from_numpy(X0).cuda(), tol=1e-10)
+        assert info.converged
+        outs[st] = (ev, info.outer, info.sweeps)
+    assert outs[True][1:] == outs[False][1:]
+    assert np.max(np.abs(outs[True][0] - outs[False][0]) / np.abs(outs[False][0])) <= 1e-13
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    assert np.max(np.abs(outs[True][0] - lam) / np.abs(lam)) <= 1e-10
