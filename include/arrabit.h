@@ -134,6 +134,8 @@ typedef struct {
                         1 = Gauss-Newton (Alg. Arrabit2: Y = X (X^T X)^{-1},
                         Z = rho_d(A) Y, X = Z - X (Y^T Z - I)/2); needs p >= 1; a step
                         whose X^T X is not positive definite returns ARR_ENUMERIC   */
+    int64_t grid[3]; /* eig_solve_host only: {nx, ny, nz} != 0 declares A a stencil operator
+                        (eig_set_stencil on the internal context); {0,0,0}: CSR kernels  */
 } arr_solve_opts;
 
 typedef struct {
@@ -220,6 +222,8 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
 arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
 /* K of the active stencil path (0 = the CSR kernels). */
 int32_t eig_stencil_active(const arr_ctx *c);
+/* Name of the kernel the context's last fused SpMM launched (static string; "" if none). */
+const char *eig_last_spmm_kernel(const arr_ctx *c);
 /* Change the degree d used by filter_step (1 <= d). */
 arr_status eig_set_degree(arr_ctx *c, int32_t d);
 /* Which end of the spectrum: smallest = 0 (default): the k algebraically largest

@@ -25,28 +25,58 @@ EPS = np.finfo(np.float64).eps
 
 
 # --------------------------------------------------------------------------- QR
+def _rank1_sub(B: np.ndarray, v: np.ndarray, w: np.ndarray, chunk: int = 8192):
+    """B -= v w^T, in row chunks (keeps the outer-product temporary small)."""
+    for r0 in range(0, B.shape[0], chunk):
+        B[r0:r0 + chunk] -= np.outer(v[r0:r0 + chunk], w)
+
+
+def _form_q(V: list, betas: list, n: int, t: int, nb: int = 32) -> np.ndarray:
+    """Q = H_0 H_1 ... H_{t-1} [I_t; 0] from reflectors v_k (v_k[0] = 1, length n - k),
+    applied in compact-WY groups of nb (I - V T V^T, Schreiber & Van Loan) in reverse."""
+    Q = np.zeros((n, t))
+    Q[np.arange(t), np.arange(t)] = 1.0
+    for k0 in range(((t - 1) // nb) * nb, -1, -nb):
+        k1 = min(t, k0 + nb)
+        b = k1 - k0
+        Vp = np.zeros((n - k0, b))
+        for j in range(b):
+            Vp[j:, j] = V[k0 + j]
+        T = np.zeros((b, b))
+        for j in range(b):
+            T[j, j] = betas[k0 + j]
+            if j:
+                T[:j, j] = -betas[k0 + j] * (T[:j, :j] @ (Vp[:, :j].T @ Vp[:, j]))
+        Q[k0:, k0:] -= Vp @ (T @ (Vp.T @ Q[k0:, k0:]))
+    return Q
+
+
 def qr_pivoted(Z: np.ndarray, want_q: bool = True):
     """Z[:, piv] = Q R, Q n x m with orthonormal columns, R upper triangular with
     |R_00| >= |R_11| >= ... (column pivoting on the largest remaining 2-norm).
 
     Returns (Q, R, piv).  Householder reflectors H_k = I - beta_k v_k v_k^T with
-    v_k[k] = 1 (Golub & Van Loan Alg. 5.1.1), applied to the trailing columns; Q is
-    accumulated by applying them in reverse order to the first m columns of I."""
+    v_k[k] = 1 (Golub & Van Loan Alg. 5.1.1), applied to the trailing columns; the
+    trailing column norms are downdated (nrm_j^2 -= R_kj^2) and recomputed when they
+    have lost more than 99% to cancellation (Golub & Van Loan §5.4.1); Q is
+    accumulated from the reflectors in reverse order (compact WY groups)."""
     A = np.array(Z, dtype=np.float64, copy=True)
     n, m = A.shape
     t = min(n, m)
     piv = np.arange(m)
     V = []       # reflector vectors (length n - k)
     betas = []
+    nrm2 = np.einsum("ij,ij->j", A, A)
+    ref2 = nrm2.copy()
     for k in range(t):
-        # pivot: the trailing column of largest 2-norm (recomputed, no downdating)
-        norms = np.einsum("ij,ij->j", A[k:, k:], A[k:, k:])
-        j = k + int(np.argmax(norms))
+        j = k + int(np.argmax(nrm2[k:]))
         if j != k:
             A[:, [k, j]] = A[:, [j, k]]
             piv[[k, j]] = piv[[j, k]]
+            nrm2[[k, j]] = nrm2[[j, k]]
+            ref2[[k, j]] = ref2[[j, k]]
         x = A[k:, k].copy()
-        alpha = np.linalg.norm(x)
+        alpha = np.sqrt(x @ x)
         if alpha == 0.0:
             V.append(np.zeros(n - k))
             betas.append(0.0)
@@ -58,21 +88,22 @@ def qr_pivoted(Z: np.ndarray, want_q: bool = True):
         v /= v[0]
         beta = 2.0 / float(v @ v)
         # H_k applied to the trailing columns: A <- A - beta v (v^T A)
-        A[k:, k:] -= beta * np.outer(v, v @ A[k:, k:])
+        wv = beta * (v @ A[k:, k:])
+        _rank1_sub(A[k:, k:], v, wv)
         A[k + 1:, k] = 0.0
         V.append(v)
         betas.append(beta)
+        # downdate the trailing norms by the new row of R
+        if k + 1 < m:
+            nrm2[k + 1:] -= A[k, k + 1:] ** 2
+            bad = np.nonzero(nrm2[k + 1:] <= 1e-2 * ref2[k + 1:])[0] + k + 1
+            for c in bad:
+                nrm2[c] = A[k + 1:, c] @ A[k + 1:, c]
+                ref2[c] = nrm2[c]
     R = np.triu(A[:t, :])
     if not want_q:
         return None, R, piv
-    Q = np.zeros((n, t))
-    Q[np.arange(t), np.arange(t)] = 1.0
-    for k in range(t - 1, -1, -1):
-        v, beta = V[k], betas[k]
-        if beta == 0.0:
-            continue
-        Q[k:, k:] -= beta * np.outer(v, v @ Q[k:, k:])
-    return Q, R, piv
+    return _form_q(V, betas, n, t), R, piv
 
 
 # --------------------------------------------------------------------------- eig

@@ -220,6 +220,11 @@ class EigContext:
         self._check(self.lib.eig_set_stencil(self.h, int(nx), int(ny), int(nz)), "eig_set_stencil")
 
     @property
+    def last_spmm_kernel(self) -> str:
+        """Name of the kernel the last fused SpMM of this context launched."""
+        return self.lib.eig_last_spmm_kernel(self.h).decode()
+
+    @property
     def stencil_points(self) -> int:
         """K of the active stencil path (0: CSR kernels)."""
         return int(self.lib.eig_stencil_active(self.h))
@@ -330,10 +335,11 @@ def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = 
 
 
 def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, s_max=5, evec=None,
-                   stream=None):
+                   stream=None, grid=None):
     """Public host-buffer entry (eig_solve_host): host arrays in, host results out.
     X0 is n x w (w >= k; w - k guard columns).  Arguments may be numpy arrays or
-    (pinned) CPU torch tensors."""
+    (pinned) CPU torch tensors.  grid = (nx, ny, nz) declares A a stencil operator
+    (eig_set_stencil on the internal context)."""
     lib = _lib.load()
     w = int(X0.shape[1])
 
@@ -349,6 +355,8 @@ def eig_solve_host(n, row_ptr, col_idx, val, k, p, d, X0, tol=1e-10, maxit=300, 
     res = np.empty(k)
     info = arr_solve_info()
     opts = arr_solve_opts(tol, maxit, s_max, 0, 0, 0, 0)
+    if grid is not None:
+        opts.grid[0], opts.grid[1], opts.grid[2] = (int(x) for x in grid)
     hs, _ = _stream_handle(stream)
     st = lib.eig_solve_host(int(n), nnz, ptr(row_ptr), ptr(col_idx), ptr(val), k, w, p, d, ptr(X0),
                             ctypes.byref(opts), ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

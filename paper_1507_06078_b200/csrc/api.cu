@@ -993,6 +993,7 @@ arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
 }
 
 int32_t eig_stencil_active(const arr_ctx *c) { return c && c->st.on ? c->st.K : 0; }
+const char *eig_last_spmm_kernel(const arr_ctx *c) { return c && c->last_kernel ? c->last_kernel : ""; }
 
 arr_status eig_set_degree(arr_ctx *c, int32_t d) {
     GUARD(c);
@@ -1327,6 +1328,8 @@ arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const 
     }
     arr_csr A{n, nnz, d_rp, d_ci, d_val};
     st = eig_init_w(&c, &A, k, w, p, d, stream);
+    if (st == ARR_OK && (opts->grid[0] || opts->grid[1] || opts->grid[2]))
+        st = eig_set_stencil(c, opts->grid[0], opts->grid[1], opts->grid[2]);
     if (st == ARR_OK) st = eig_solve(c, d_X, ldx, opts, eigval, res, info);
     if (st == ARR_OK && evec) {
         if (cudaMemcpy2DAsync(evec, sizeof(double) * k, d_X, sizeof(double) * ldx, sizeof(double) * k, n,

@@ -1,5 +1,6 @@
 // Internal declarations of libarrabit (not part of the C-ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 #include <stdint.h>
@@ -49,6 +50,7 @@ struct StencilState {
 };
 // One launch of the stencil kernel (kernel parameter, __grid_constant__).
 struct StencilLaunch {
+    CUtensorMap tm_in, tm_prev, tm_xa, tm_val;  // TMA descriptors (64-byte aligned)
     const double *Yin, *Yprev, *Xa;
     double *Yout;
     int64_t ld_in, ld_prev, ld_out, ld_xa;
@@ -105,6 +107,7 @@ struct arr_ctx {
     cusolverDnHandle_t solver;
     size_t ws_bytes;
     // bookkeeping
+    const char *last_kernel;  // name of the kernel the last fused SpMM launched (eig_last_spmm_kernel)
     uint64_t launches;
     int64_t spmm_blocks;
     arr_status poisoned;

@@ -732,6 +732,7 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
         if (G < 1) G = 1;
         kern<<<(unsigned)G, ncons + 32, smem, c->stream>>>(a, TX, R, RT, wv, ntiles, kWsCap, ncons);
         c->launches++;
+        c->last_kernel = "spmm_ws_kernel (CSR, warp-specialised)";
         return (int)G;
     }
 #endif
@@ -750,6 +751,7 @@ int launch_t(arr_ctx *c, const SpmmArgs &a, int TX, int R, int wv) {
     if (G < 1) G = 1;
     kern<<<(unsigned)G, nthr, smem, c->stream>>>(a, TX, R, RT, wv, ntiles, kNnzCap);
     c->launches++;
+    c->last_kernel = "spmm_tile_kernel (CSR)";
     return (int)G;
 }
 

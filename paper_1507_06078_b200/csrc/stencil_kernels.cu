@@ -19,6 +19,8 @@
 // SM traffic per degree drops to (box/patch) + 2 blocks.  The terms of each output
 // row are still added in ascending column order (plane z-1, then z, then z+1; within
 // a plane (dy, dx) ascending): bitwise the CSR kernels' sums.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 
 #include <algorithm>
@@ -51,12 +53,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
-// one contiguous row segment global -> shared through the bulk-copy engine (TMA)
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+// one 2-D box of a tensor map global -> shared (TMA; out-of-range rows are zero-filled)
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar,
+                                       uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ uint64_t pol_evict_last() {
@@ -68,13 +71,6 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
-}
-__device__ __forceinline__ double2 ld_stream(const double *p, uint64_t pol) {
-    double2 r;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(r.x), "=d"(r.y)
-                 : "l"(p), "l"(pol));
-    return r;
 }
 __device__ __forceinline__ void st_stream(double *p, double2 v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
@@ -102,28 +98,28 @@ template <int SH>
 struct Shape;
 template <>
 struct Shape<0> {
-    static constexpr int NQ = 9, K = 27, QC = 4, HY = 1;
+    static constexpr int NQ = 9, K = 27, QC = 4;
     static constexpr __host__ __device__ int dy(int q) { return q / 3 - 1; }
     static constexpr __host__ __device__ int dx(int q) { return q % 3 - 1; }
     static constexpr __host__ __device__ int k(int dz, int q) { return (dz + 1) * 9 + q; }
 };
 template <>
 struct Shape<1> {
-    static constexpr int NQ = 5, K = 7, QC = 2, HY = 1;
+    static constexpr int NQ = 5, K = 7, QC = 2;
     static constexpr __host__ __device__ int dy(int q) { return q == 0 ? -1 : (q == 4 ? 1 : 0); }
     static constexpr __host__ __device__ int dx(int q) { return q == 1 ? -1 : (q == 3 ? 1 : 0); }
     static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? 1 + q : (q == 2 ? (dz < 0 ? 0 : 6) : -1); }
 };
 template <>
 struct Shape<2> {
-    static constexpr int NQ = 3, K = 5, QC = 1, HY = 0;
+    static constexpr int NQ = 3, K = 5, QC = 1;
     static constexpr __host__ __device__ int dy(int) { return 0; }
     static constexpr __host__ __device__ int dx(int q) { return q - 1; }
     static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? 1 + q : (q == 1 ? (dz < 0 ? 0 : 4) : -1); }
 };
 template <>
 struct Shape<3> {
-    static constexpr int NQ = 3, K = 3, QC = 1, HY = 0;
+    static constexpr int NQ = 3, K = 3, QC = 1;
     static constexpr __host__ __device__ int dy(int) { return 0; }
     static constexpr __host__ __device__ int dx(int q) { return q - 1; }
     static constexpr __host__ __device__ int k(int dz, int q) { return dz == 0 ? q : -1; }
@@ -178,9 +174,11 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
     return r;
 }
 
-// Shared memory of one CTA: [full[4] | empty[4] mbarriers (128 B)] [NS stages] [val ring]
-// stage:    box rows of Y_j (nbox x pwv vectors) | Y_{j-1} rows | X rows (patch rows)
-// val ring: VS = NS + 2 slots of the patch's DIA rows of one plane (Px*Py x Kpad)
+// Shared memory of one CTA: [full[4] | empty[4] mbarriers (128 B)] [NS stages] [val ring],
+// every region 128-byte aligned (TMA destinations):
+// stage:    box lines of Y_j (box_y lines x box_x rows x 2 pwv doubles) | Y_{j-1} lines |
+//           X lines (Py lines x Px rows each)
+// val ring: VS = NS + 2 slots, one plane of the patch's DIA rows (Py lines x Px rows x Kpad)
 template <bool HAS_PREV, bool HAS_X>
 struct StageLayout {
     uint32_t box, prev, xa, bytes;
@@ -191,11 +189,13 @@ struct StageLayout {
         bytes = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
     }
 };
+__host__ __device__ inline uint32_t vline_bytes(int Px, int Kpad) { return ((uint32_t)Px * Kpad * 8u + 127u) & ~127u; }
 
 template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
 __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_constant__ StencilLaunch P) {
     using Sh = Shape<SH>;
-    extern __shared__ __align__(128) unsigned char sm[];
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    unsigned char *sm = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);  // 128-byte aligned base
     uint64_t *full = reinterpret_cast<uint64_t *>(sm);
     uint64_t *empty = full + 4;
     unsigned char *stages = sm + 128;
@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
     const int NS = P.NS, VS = P.NS + 2;
     const int nbox = P.box_x * P.box_y;
     const StageLayout<HAS_PREV, HAS_X> SL(nbox, P.Px * P.Py, P.pwv);
-    const uint32_t slot_bytes = (uint32_t)P.Px * P.Py * P.Kpad * 8u;
+    const uint32_t vlb = vline_bytes(P.Px, P.Kpad);
+    const uint32_t slot_bytes = (uint32_t)P.Py * vlb;
     unsigned char *vring = stages + (size_t)NS * SL.bytes;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -215,24 +216,25 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
     __syncthreads();
     const int64_t G = gridDim.x;
     const int64_t nxy = (int64_t)P.nx * P.ny;
-    const int pwv = P.pwv;  // smem row stride in 16-byte vectors
+    const int pwv = P.pwv;  // smem row stride in 16-byte vectors (a multiple of 8: 128-byte rows)
     if (tid >= kStCons) {
         // ------------------------------------------------------------ producer warp
-        // Per step (plane z of the march; z == nz is a tail step with no plane) it
-        // copies, completing on full[b]: the box rows of plane z that an output reads,
-        // the Y_{j-1} (and X) rows of the outputs of plane z-1, and the DIA rows of
-        // plane z+1 (and of plane z on an item's first step) into the value ring.
+        // Per step (plane z of the march; z == nz is a tail step with no plane), one TMA
+        // box per grid-line run, completing on full[b]: the box lines of plane z that exist
+        // (box_x rows with the x halo), the Y_{j-1} (and X) lines of the outputs of plane
+        // z-1, and the DIA lines of plane z+1 (and of plane z on an item's first step).
         const int lane = tid - kStCons;
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_in)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_val)) : "memory");
+        }
         const uint64_t pol_keep = pol_evict_last();    // Y_j rows: re-staged by the neighbouring patches
         const uint64_t pol_once = pol_evict_first();   // Y_{j-1}, X, DIA: read once
+        const uint32_t boxline = (uint32_t)P.box_x * pwv * 16u, pline = (uint32_t)P.Px * pwv * 16u;
         uint32_t step = 0;
         for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
             const Item I = decode_item(P, it);
-            const int pw = min(pwv, P.wv - I.panel * pwv);
-            const uint32_t rowb = (uint32_t)pw * 16u;
-            const int64_t col0 = (int64_t)I.panel * pwv * 2;
-            const int nrow = I.pxe * I.pye;
-            const uint32_t vlb = (uint32_t)I.pxe * P.Kpad * 8u;  // DIA bytes of one patch line
+            const int col0 = I.panel * pwv * 2;  // first column of the panel
             const int zs = max(I.zc0 - 1, 0);
             for (int z = zs; z <= I.zc1; ++z, ++step) {
                 const int b = (int)(step % NS);
@@ -242,48 +244,42 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                 // DIA planes to load: z+1 (and z on the first step when z is an output plane)
                 const int va0 = (z == zs && z >= I.zc0 && real) ? z : z + 1;
                 const int va1 = (z + 1 < I.zc1) ? z + 1 : z;  // inclusive; empty if va1 < va0
-                uint32_t mine = 0;
-                if (real) {
-                    for (int r = lane; r < nbox; r += 32) {
-                        const int ly = r / P.box_x, lx = r - ly * P.box_x;
-                        const int gy = I.y0 - P.hy + ly, gx = I.x0 - P.hx + lx;
-                        if (gx < 0 || gx >= P.nx || gy < 0 || gy >= P.ny) continue;
-                        if (shape_needs<SH>(ly, lx, P.hy, P.hx, I.pye, I.pxe)) mine += rowb;
-                    }
+                // job list: [0, box_y) box lines, [box_y, box_y + Py) prev lines,
+                // then X lines, then DIA lines (plane va0 .. va1, Py each)
+                const int nbl = real ? P.box_y : 0;
+                const int npl = (fin && HAS_PREV) ? I.pye : 0;
+                const int nxl = (fin && HAS_X) ? I.pye : 0;
+                const int nvl = va1 >= va0 ? (va1 - va0 + 1) * I.pye : 0;
+                uint32_t total = 0;
+                for (int ly = 0; ly < nbl; ++ly) {
+                    const int gy = I.y0 - P.hy + ly;
+                    if (gy >= 0 && gy < P.ny) total += boxline;
                 }
-                for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-                uint32_t total = mine;
-                if (fin) total += (uint32_t)nrow * rowb * ((HAS_PREV ? 1u : 0u) + (HAS_X ? 1u : 0u));
-                if (va1 >= va0) total += (uint32_t)(va1 - va0 + 1) * I.pye * vlb;
+                total += (uint32_t)(npl + nxl) * pline + (uint32_t)nvl * (uint32_t)P.Px * P.Kpad * 8u;
                 if (lane == 0) mbar_expect_tx(full + b, total);
                 __syncwarp();
                 unsigned char *st = stages + (size_t)b * SL.bytes;
-                if (real) {
-                    const double *src_plane = P.Yin + (int64_t)z * nxy * P.ld_in + col0;
-                    for (int r = lane; r < nbox; r += 32) {
-                        const int ly = r / P.box_x, lx = r - ly * P.box_x;
-                        const int gy = I.y0 - P.hy + ly, gx = I.x0 - P.hx + lx;
-                        if (gx < 0 || gx >= P.nx || gy < 0 || gy >= P.ny) continue;
-                        if (shape_needs<SH>(ly, lx, P.hy, P.hx, I.pye, I.pxe))
-                            bulk_g2s(st + SL.box + (size_t)r * pwv * 16, src_plane + ((int64_t)gy * P.nx + gx) * P.ld_in,
-                                     rowb, full + b, pol_keep);
+                const int njobs = nbl + npl + nxl + nvl;
+                for (int j = lane; j < njobs; j += 32) {
+                    if (j < nbl) {
+                        const int gy = I.y0 - P.hy + j;
+                        if (gy < 0 || gy >= P.ny) continue;
+                        const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + (I.x0 - P.hx);
+                        tma_2d(st + SL.box + (size_t)j * boxline, &P.tm_in, col0, (int)row, full + b, pol_keep);
+                    } else if (j < nbl + npl + nxl) {
+                        const int jj = j - nbl;
+                        const bool isx = jj >= npl;
+                        const int oy = isx ? jj - npl : jj;
+                        const int64_t row = ((int64_t)(z - 1) * P.ny + I.y0 + oy) * P.nx + I.x0;
+                        if (HAS_PREV && !isx) tma_2d(st + SL.prev + (size_t)oy * pline, &P.tm_prev, col0, (int)row, full + b, pol_once);
+                        if (HAS_X && isx) tma_2d(st + SL.xa + (size_t)oy * pline, &P.tm_xa, col0, (int)row, full + b, pol_once);
+                    } else {
+                        const int jj = j - nbl - npl - nxl;
+                        const int zz = va0 + jj / I.pye, oy = jj - (jj / I.pye) * I.pye;
+                        unsigned char *slot = vring + (size_t)((step + (uint32_t)(zz - z)) % VS) * slot_bytes;
+                        const int64_t row = ((int64_t)zz * P.ny + I.y0 + oy) * P.nx + I.x0;
+                        tma_2d(slot + (size_t)oy * vlb, &P.tm_val, 0, (int)row, full + b, pol_once);
                     }
-                }
-                if (fin && (HAS_PREV || HAS_X)) {
-                    for (int r = lane; r < nrow; r += 32) {
-                        const int oy = r / I.pxe, ox = r - oy * I.pxe;
-                        const int64_t row = (int64_t)(z - 1) * nxy + (int64_t)(I.y0 + oy) * P.nx + I.x0 + ox;
-                        const size_t so = (size_t)(oy * P.Px + ox) * pwv * 16;
-                        if (HAS_PREV) bulk_g2s(st + SL.prev + so, P.Yprev + row * P.ld_prev + col0, rowb, full + b, pol_once);
-                        if (HAS_X) bulk_g2s(st + SL.xa + so, P.Xa + row * P.ld_xa + col0, rowb, full + b, pol_once);
-                    }
-                }
-                for (int zz = va0; zz <= va1; ++zz) {
-                    unsigned char *slot = vring + (size_t)((step + (uint32_t)(zz - z)) % VS) * slot_bytes;
-                    for (int oy = lane; oy < I.pye; oy += 32)
-                        bulk_g2s(slot + (size_t)oy * P.Px * P.Kpad * 8,
-                                 P.val + ((int64_t)zz * nxy + (int64_t)(I.y0 + oy) * P.nx + I.x0) * P.Kpad, vlb,
-                                 full + b, pol_once);
                 }
             }
         }
@@ -302,10 +298,10 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
         const int colv0 = I.panel * pwv;
         const int r = tid / pw;
         const int v = tid - r * pw;
-        const bool act = r < nrow;
+        const bool act = r < nrow;  // (v < pw by construction; the smem rows are pwv wide)
         const int oy = act ? r / I.pxe : 0, ox = act ? r - (r / I.pxe) * I.pxe : 0;
         const int cb = (oy + P.hy) * P.box_x + (ox + P.hx);
-        const int rs = oy * P.Px + ox;  // patch row slot (prev / X rows, value ring)
+        const int rs = oy * P.Px + ox;  // patch row slot (prev / X rows)
         const int64_t rxy = (int64_t)(I.y0 + oy) * P.nx + (I.x0 + ox);
         // smem row of each in-plane position (the centre where the neighbour is outside
         // the grid: its DIA slot is zero there)
@@ -331,9 +327,10 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
             double2 yp = make_double2(0.0, 0.0), xa = make_double2(0.0, 0.0);
             if (act) {
                 if (real) {
-                    const double *vp = reinterpret_cast<const double *>(vring + (size_t)((step + VS - 1) % VS) * slot_bytes) + rs * Kp;
-                    const double *v0 = reinterpret_cast<const double *>(vring + (size_t)(step % VS) * slot_bytes) + rs * Kp;
-                    const double *vm = reinterpret_cast<const double *>(vring + (size_t)((step + 1) % VS) * slot_bytes) + rs * Kp;
+                    const size_t vo = (size_t)oy * vlb + (size_t)ox * Kp * 8;
+                    const double *vp = reinterpret_cast<const double *>(vring + (size_t)((step + VS - 1) % VS) * slot_bytes + vo);
+                    const double *v0 = reinterpret_cast<const double *>(vring + (size_t)(step % VS) * slot_bytes + vo);
+                    const double *vm = reinterpret_cast<const double *>(vring + (size_t)((step + 1) % VS) * slot_bytes + vo);
 #pragma unroll
                     for (int q = 0; q < Sh::NQ; ++q) {
                         const double2 y = S[qoff[q]];
@@ -459,8 +456,8 @@ template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
 int launch_st(arr_ctx *c, StencilLaunch &L) {
     auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X>;
     const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
-    const size_t ring = (size_t)(L.NS + 2) * L.Px * L.Py * L.Kpad * 8;
-    const size_t smem = 128 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
+    const size_t ring = (size_t)(L.NS + 2) * L.Py * vline_bytes(L.Px, L.Kpad);
+    const size_t smem = 256 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
     static LaunchCache cache;
     const int occ = cached_occupancy(cache, kern, kStThreads, smem);
     int64_t G = (int64_t)c->num_sms * occ;
@@ -469,6 +466,11 @@ int launch_st(arr_ctx *c, StencilLaunch &L) {
     if (G < L.npan) G = L.npan;
     kern<<<(unsigned)G, kStThreads, smem, c->stream>>>(L);
     c->launches++;
+    static const char *names[4] = {"stencil_kernel (27-point, DIA, TMA-staged 2.5-D)",
+                                   "stencil_kernel (7-point, DIA, TMA-staged 2.5-D)",
+                                   "stencil_kernel (2-D 5-point, DIA, TMA-staged 2.5-D)",
+                                   "stencil_kernel (1-D 3-point, DIA, TMA-staged 2.5-D)"};
+    c->last_kernel = names[SH];
     return (int)G;
 }
 
@@ -488,6 +490,34 @@ int dispatch_st_flags(arr_ctx *c, StencilLaunch &L, bool prev, bool ss, bool xa)
 
 bool al16(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// 2-D fp64 tensor map over a row-major block: cols x rows, row stride ld doubles, box
+// {box_cols, box_rows}; out-of-range elements are zero-filled.
+bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, int64_t ld, int box_cols,
+               int box_rows) {
+    auto enc = tensor_encoder();
+    if (!enc) return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim, gstride, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 // Host: geometry of one launch (patch, panels, z-chunks, stages) for block width w.
@@ -503,9 +533,11 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
     double best = 1e300;
     bool found = false;
     const int hx = S.hx, hy = S.hy;
-    for (int npan = 1; npan <= 8; ++npan) {
-        const int pwv = (wv + npan - 1) / npan;
-        if (pwv < 8 && npan > 1) break;
+    for (int npan = 1; npan <= 16; ++npan) {
+        // panel rows of a multiple of 8 vectors (128-byte TMA destinations), <= 256 doubles (TMA box)
+        const int pwv = ((wv + npan - 1) / npan + 7) / 8 * 8;
+        if (pwv > 128) continue;
+        if ((int64_t)(npan - 1) * pwv >= wv) break;  // an empty panel
         for (int Py = 1; Py <= (S.ny > 1 ? 16 : 1); ++Py) {
             for (int Px = 1; Px <= 64; ++Px) {
                 const int nrow = Px * Py;
@@ -513,23 +545,11 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
                 if (Px > S.nx || Py > S.ny) break;
                 const int bx = Px + 2 * hx, by = Py + 2 * hy;
                 const size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
-                const size_t slot = (size_t)nrow * S.Kpad * 8;
+                const size_t slot = (size_t)Py * (((size_t)Px * S.Kpad * 8 + 127) & ~(size_t)127);
                 int NS = 4;
                 while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
                 if (NS < 2) continue;
-                // staged rows actually read (the box minus unused corners)
-                int need = 0;
-                for (int ly = 0; ly < by; ++ly)
-                    for (int lx = 0; lx < bx; ++lx) {
-                        bool nd = false;
-                        switch (S.shape) {
-                            case 0: nd = shape_needs<0>(ly, lx, hy, hx, Py, Px); break;
-                            case 1: nd = shape_needs<1>(ly, lx, hy, hx, Py, Px); break;
-                            case 2: nd = shape_needs<2>(ly, lx, hy, hx, Py, Px); break;
-                            default: nd = shape_needs<3>(ly, lx, hy, hx, Py, Px); break;
-                        }
-                        need += nd;
-                    }
+                const int need = bx * by;  // staged rows: whole box lines (one TMA box per line)
                 const int npx = (S.nx + Px - 1) / Px, npy = (S.ny + Py - 1) / Py;
                 const double rag = (double)S.nx * S.ny / ((double)npx * Px * npy * Py);
                 // z-chunks: enough work items for >= ~12 per CTA, chunks of >= 8 planes
@@ -543,8 +563,11 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
                 const double tail = waves / std::ceil(waves);
                 const double warm = (double)(Lz + (nzc > 1 ? 1 : 0)) / Lz;
                 const double rowbytes = 16.0 * wv;
+                const double colfill = (double)wv / ((double)npan * pwv);  // OOB columns of the last panel
                 double cost = ((double)need / nrow * warm + 1.0 + (has_prev ? 1.0 : 0.0) + (has_x ? 1.0 : 0.0)) * rowbytes +
                               8.0 * S.Kpad * npan;
+                cost /= colfill;
+                cost *= 1.0 + 6.0 / nrow;  // fixed per-step cost (barriers, TMA issue) over the outputs of a step
                 cost /= rag * tail;
                 if (NS == 2) cost *= 1.05;
                 if (cost < best) {
@@ -583,6 +606,12 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     L.Xa = a.Xa; L.ld_xa = a.ld_xa;
     L.alpha = a.alpha; L.shift = a.shift; L.beta = a.beta; L.gxa = a.gxa;
     L.partials = a.partials;
+    const int64_t nrows = c->A.n;
+    if (!encode_2d(&L.tm_in, a.Yin, a.w, nrows, a.ld_in, 2 * L.pwv, L.box_x) ||
+        !encode_2d(&L.tm_val, c->st.dia, c->st.Kpad, nrows, c->st.Kpad, c->st.Kpad, L.Px) ||
+        (a.Yprev && !encode_2d(&L.tm_prev, a.Yprev, a.w, nrows, a.ld_prev, 2 * L.pwv, L.Px)) ||
+        (a.Xa && !encode_2d(&L.tm_xa, a.Xa, a.w, nrows, a.ld_xa, 2 * L.pwv, L.Px)))
+        return -1;
     const bool prev = a.Yprev != nullptr, ss = a.partials != nullptr, xa = a.Xa != nullptr;
     switch (c->st.shape) {
         case 0: return dispatch_st_flags<0>(c, L, prev, ss, xa);
