@@ -4,17 +4,19 @@
 
 One STEP = one full fixed-parameter eig_solve (every §8(a) row: interval,
 fused Chebyshev filter degrees + MPM normalisation, block-Krylov augmentation,
-DMMA Gram/projection products, small eig, residuals) of the N=1 workload
-BASELINE.json's metric is quoted on: configs[1] = cfg2, the 2-D 5-point
-Laplacian 300x300 (n=90,000), k=200, d=20, p=1, tol=1e-10, X0 ~ N(0,1) seed 1.
-value = eigenpairs/s = k * steps * N / (max-over-ranks device time).
-The filter's HBM GB/s (the metric's first half) is the `roofline` object.
+DMMA Gram/projection products, small eig, residuals) of the workload the
+metric's "1/2/4/8 B200" is quoted on: BASELINE.json configs[2] = cfg3, the 3-D
+7-point Laplacian 100^3 + diag(U[0,1)) (n = 1e6), k = 500 (w = 550), d = 20, p = 2,
+tol = 1e-10, seed 2 (--config selects another).  The 3-D grids run the stencil-aware
+filter path (eig_set_stencil; DIA + TMA-staged 2.5-D kernel), others the CSR kernels.
+value = eigenpairs/s = k * steps / (max-over-ranks device time).
+The filter's HBM GB/s (the metric's first half) is the `roofline` object; a shorter
+cfg2 solve (BASELINE.json configs[1]) is reported beside it as `secondary`.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N>1 (torchrun): configs 1-2 (single-GPU problems in BASELINE.json) run one replica
-per rank (weak scaling, no data-path collective); configs 3-5 (or --partition) are
-row-partitioned over the ranks: halo / all-gather exchange before every SpMM and
-Gram allreduce over NCCL inside libarrabit (strong scaling).
+N>1 (torchrun): the config is row-partitioned over the ranks (z-slabs / balanced
+blocks; halo or all-gather exchange before every SpMM and Gram allreduce over NCCL
+inside libarrabit; strong scaling); --replicas runs independent copies instead.
 """
 from __future__ import annotations
 
@@ -45,7 +47,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--spmm", default="auto", choices=["auto", "csr", "stencil"],
+                    help="filter kernels: auto = the stencil path for 3-D grids, CSR otherwise")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary cfg2 solve")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of a partition")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--filter", default="cheb", choices=["cheb", "interp"],
@@ -54,8 +60,6 @@ def parse():
                     help="the paper's adaptive options (bit mask: 1 p, 2 d, 4 continuation + deflation)")
     ap.add_argument("--inner-solver", default="mpm", choices=["mpm", "gn"],
                     help="inner solver of Alg. Arrabit2: mpm (default) or gn (Gauss-Newton)")
-    ap.add_argument("--partition", action="store_true",
-                    help="N>1: row-partition the config over the ranks even for configs 1-2")
     return ap.parse_args()
 
 
@@ -127,12 +131,63 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def filter_bytes_per_degree(n, nnz, w, d):
-    """Algorithmic bytes of one filter-degree launch: A once
-    (12 nnz + 8(n+1)), read Y_j, read Y_{j-1}, write Y_{j+1} (24 n w); the first
-    degree has no Y_{j-1} (16 n w).  Averaged over the d launches of a sweep."""
-    a = 12 * nnz + 8 * (n + 1)
+def filter_bytes_per_degree(n, nnz, w, d, K=0):
+    """Algorithmic bytes of one filter-degree launch: A once, read Y_j,
+    read Y_{j-1}, write Y_{j+1} (24 n w); the first degree has no Y_{j-1} (16 n w).
+    A is 12 nnz + 8(n+1) bytes as CSR, 8 K n as the stencil path's K diagonals.
+    Averaged over the d launches of a sweep."""
+    a = 8 * K * n if K else 12 * nnz + 8 * (n + 1)
     return (a + 16 * n * w + (d - 1) * (a + 24 * n * w)) / d
+
+
+def stencil_grid(spec):
+    """The grid a config's operator is declared on for the stencil path (x fastest);
+    a 2-D grid is declared (nx, 1, ny) so that the march runs along y."""
+    if spec.kind == "lap1d":
+        return (spec.size, 1, 1)
+    if spec.kind == "lap2d":
+        return (spec.size, 1, spec.size)
+    if spec.kind in ("lap3dV", "st27"):
+        return (spec.size, spec.size, spec.size)
+    return None
+
+
+def use_stencil(spec, args):
+    if args.spmm == "csr" or stencil_grid(spec) is None:
+        return False
+    return args.spmm == "stencil" or spec.kind in ("lap3dV", "st27")
+
+
+def config_dict(spec, A, args):
+    """The workload (identical in both arms)."""
+    return {"workload": spec.name, "n": int(A.n), "nnz": int(A.nnz), "k": spec.k, "w": spec.w, "d": spec.d,
+            "p": spec.p, "tol": spec.tol, "seed": spec.seed, "step": "one full eig_solve from X0",
+            "filter": {"cheb": "T_d (Eq. cheby-poly)", "interp": "psi_d (paper Section 5)"}[args.filter],
+            "adapt": args.adapt, "inner_solver": args.inner_solver,
+            "l2": "flushed between timed steps (256 MiB write), outside the events"}
+
+
+def cpu_info():
+    info = {"model": None, "sockets": None, "logical_cpus": os.cpu_count(), "ram_gb": None}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip())
+            elif k.strip() == "Core(s) per socket":
+                info["cores_per_socket"] = int(v.strip())
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            kb = int(f.readline().split()[1])
+        info["ram_gb"] = round(kb / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
 
 
 # ------------------------------------------------------------------ oracle arm
@@ -152,43 +207,84 @@ def oracle_sample(A, spec, X0):
     return t1 - t0, t2 - t1
 
 
+def oracle_filter_sample(A, spec, cols=16):
+    """Seconds of one oracle MPM sweep on `cols` columns of the workload."""
+    import oracle
+    X = synth.gaussian_block_rows(A.n, cols, spec.seed, 0, A.n)
+    a = oracle.gershgorin_lower(A)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    upper = float(np.bincount(rows, weights=np.abs(A.val), minlength=A.n).max())
+    t0 = time.perf_counter()
+    oracle.mpm_sweep(A, a, a + 0.9 * (upper - a), spec.d, X)
+    return time.perf_counter() - t0
+
+
+def oracle_step_estimate(A, spec, cid):
+    """Oracle seconds for one full solve of the workload, from a bounded sample:
+    cfg 1-2: one sweep + one ARR of the full block, times the oracle's own counts
+    (tests/golden/oracle_cfg<N>_counts.json); larger configs: a 16-column sweep x w/16
+    times the sweep count of the oracle's golden solve when there is one (ARR not
+    sampled: the oracle's ARR at these widths takes minutes)."""
+    cnt = oracle_counts(cid)
+    if cid <= 2:
+        S, O = (cnt["sweeps"], cnt["outer"]) if cnt else (38, 10)
+        ts, ta = oracle_sample(A, spec, configs.starting_block(spec))
+        smp = (f"{spec.name}: one MPM sweep (d={spec.d}, {ts:.2f} s) + one ARR(p={spec.p}) + residuals "
+               f"({ta:.2f} s) on the full block, extrapolated to the oracle's own full solve ({S} sweeps, {O} ARR)")
+        return S * ts + O * ta, smp
+    gold = oracle_golden(cid)
+    S = gold["sweeps"] if gold else 24
+    ts = oracle_filter_sample(A, spec) * spec.w / 16
+    smp = (f"{spec.name}: one MPM sweep of 16 of the {spec.w} columns ({ts * 16 / spec.w:.2f} s) x w/16, "
+           f"extrapolated to {S} sweeps ({'the oracle golden solve' if gold else 'assumed'}); ARR not sampled")
+    return S * ts, smp
+
+
+def oracle_golden(cid):
+    p = os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cid}_eigs.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def single_thread_leg(cid):
+    """The same oracle sample with OMP / BLAS threads pinned to 1 (a subprocess, since
+    the thread count is fixed when the libraries load)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    code = ("import sys, json; sys.path.insert(0, %r); import bench; from synth import configs; "
+            "A, spec = configs.build_config(%d); t, s = bench.oracle_step_estimate(A, spec, %d); "
+            "print(json.dumps({'seconds': t, 'sample': s}))") % (ROOT, cid, cid)
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001
+        return {"error": str(exc)[:200]}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     A, spec = configs.build_config(args.config)
-    X0 = synth.starting_block(spec) if args.config <= 2 else None
-    cnt = oracle_counts(args.config)
-    S, O = (cnt["sweeps"], cnt["outer"]) if cnt else (38, 10)
-    def sample():
-        if args.config <= 2:
-            return oracle_sample(A, spec, X0)
-        return oracle_filter_sample(A, spec) * spec.w / 16, 0.0
-
     for _ in range(args.warmup):
-        sample()
-    sw, ar, wall = [], [], []
+        oracle_step_estimate(A, spec, args.config)
+    est, wall = [], []
+    smp = ""
     for _ in range(args.steps):
         t = time.perf_counter()
-        s, r = sample()
+        e, smp = oracle_step_estimate(A, spec, args.config)
         wall.append(time.perf_counter() - t)
-        sw.append(s)
-        ar.append(r)
-    t_solve = S * statistics.mean(sw) + O * statistics.mean(ar)
-    value = spec.k / t_solve
+        est.append(e)
+    value = spec.k / statistics.mean(est)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    sample = (f"{spec.name}: per step one MPM sweep (d={spec.d}) + one ARR(p={spec.p}) + residuals on the full "
-              f"block; extrapolated to the oracle's own full solve ({S} sweeps, {O} ARR steps, "
-              f"tests/golden/oracle_cfg{args.config}_counts.json)") if args.config <= 2 else (
-              f"{spec.name}: per step one MPM sweep of 16 of the {spec.w} columns, x w/16, extrapolated to "
-              f"{S} sweeps (ARR not sampled: the oracle's QR at this size takes hours)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(wall), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "d": spec.d, "p": spec.p,
-                       "tol": spec.tol},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "impl": "reference", "parallelism": f"CPU oracle, {cores} host threads",
+            "config": config_dict(spec, A, args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": smp,
+                             "cpu": cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -203,6 +299,113 @@ def _partition_spec(spec):
     if spec.kind == "lap2d":
         return ("planes", spec.size, spec.size)
     return ("balanced",)
+
+
+def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps, warmup, plan=None, comm=None,
+              world=1, dist=None):
+    """Create a context, run warm-up + timed solves; return measurements."""
+    partitioned = plan is not None
+    ctx = arr.eig_init(Ad_of(arr, Aloc, dev, stream), spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm,
+                       plan=plan)
+    nrows = X.shape[0]
+    ctx_lean = ctx.workspace_bytes < 8 * nrows * spec.w * (spec.p + 2)
+    if args.filter != "cheb":
+        ctx.eig_set_filter(args.filter)
+    path = "csr"
+    if not partitioned and use_stencil(spec, args):
+        ctx.eig_set_stencil(*stencil_grid(spec))
+        path = f"stencil ({ctx.stencil_points}-point DIA)"
+    elif not partitioned and spec.kind in ("lap3dV", "st27"):
+        from paper_1507_06078_b200 import schedule
+        by, tile = {"lap3dV": (10, 16), "st27": (8, 32)}[spec.kind]
+        ctx.eig_set_schedule(*schedule.yband_3d(spec.size, spec.size, spec.size, by, tile))
+        path = f"csr, y-band order by={by}, {tile}-row tiles"
+
+    def one_solve():
+        return ctx.eig_solve(X, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max, adapt=args.adapt,
+                             inner_solver=args.inner_solver)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            X.copy_(X0, non_blocking=True)
+            one_solve()
+    ctx.eig_set_timing(True)
+    launches0 = ctx.launch_count
+    sampler = ClockSampler(dev.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    step_ms, infos = [], []
+    with torch.cuda.stream(stream):
+        for _ in range(steps):
+            X.copy_(X0, non_blocking=True)  # X <- X0 (outside the events)
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ev, res, info = one_solve()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            infos.append(info)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = ctx.launch_count - launches0
+    phase_ms, phase_cnt = ctx.eig_phase_times()
+    # the kernel the filter degrees launch (one more filter_step, outside the timed region)
+    with torch.cuda.stream(stream):
+        ctx.eig_set_interval(infos[-1].a, infos[-1].b)
+        ctx.filter_step(X, normalize=True)
+    kernel = ctx.last_spmm_kernel
+    return dict(ctx=ctx, step_ms=step_ms, infos=infos, clocks=clocks, launches=launches, phase_ms=phase_ms,
+                phase_cnt=phase_cnt, kernel=kernel, path=path, lean=ctx_lean, stencil_K=ctx.stencil_points,
+                eigenvalues=ev)
+
+
+_AD = {}
+
+
+def Ad_of(arr, Aloc, dev, stream):
+    key = id(Aloc)
+    if key not in _AD:
+        import torch
+        with torch.cuda.stream(stream):
+            _AD[key] = arr.to_device_csr(Aloc, device=dev)
+        stream.synchronize()
+    return _AD[key]
+
+
+def roofline_of(r, spec, nrow, nnz, args, steps, cid=None):
+    peak, peak_src = load_peaks()
+    deg_ms = r["phase_ms"][0] / max(1, r["phase_cnt"][0])
+    bpl = filter_bytes_per_degree(nrow, nnz, spec.w, spec.d, r["stencil_K"])
+    if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
+        bpl += 8 * nrow * spec.w
+    achieved = bpl / (deg_ms / 1000.0) / 1e9
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config if cid is None else cid}.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("kernel_family", "") and tj["kernel_family"] in r["kernel"]:
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_src = tj.get("source")
+        except Exception:
+            traffic = None
+    pm, st = r["phase_ms"], sum(r["step_ms"])
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "traffic_source": traffic_src, "kernel": r["kernel"],
+            "bytes_per_launch": bpl, "bytes_model": ("8 K n (DIA) + 24 n w" if r["stencil_K"] else
+                                                     "12 nnz + 8(n+1) + 24 n w") + " (16 n w on a sweep's first degree)",
+            "avg_launch_us": deg_ms * 1000.0, "launches": int(r["phase_cnt"][0]), "peak_source": peak_src,
+            "frac_of_8TBs": achieved / 8000.0, "share_of_step": pm[0] / st,
+            "phase_ms_per_step": {"filter_degrees": pm[0] / steps, "arr_project": pm[1] / steps,
+                                  "arr_basis": pm[3] / steps, "arr_H": pm[4] / steps, "arr_small_eig": pm[5] / steps,
+                                  "residuals": pm[2] / steps}}
 
 
 def run_ours(args):
@@ -220,10 +423,7 @@ def run_ours(args):
     from paper_1507_06078_b200 import partition as pt
 
     A, spec = configs.build_config(args.config)
-    # N > 1: configs 3-5 are row-partitioned over the ranks (halo / all-gather exchange,
-    # Gram allreduce over NCCL: strong scaling); configs 1-2 are single-GPU problems
-    # (BASELINE.json) and run as independent replicas (weak scaling).
-    partitioned = world > 1 and (args.partition or args.config >= 3)
+    partitioned = world > 1 and not args.replicas
     plan = comm = None
     if partitioned:
         ps = _partition_spec(spec)
@@ -251,7 +451,6 @@ def run_ours(args):
     blk = 8 * nrows * spec.w
     x0_on_host = blk * (spec.p + 4) > 0.9 * torch.cuda.get_device_properties(dev).total_memory
     with torch.cuda.stream(stream):
-        Ad = arr.to_device_csr(Aloc, device=dev)
         if x0_on_host:
             X0 = torch.from_numpy(X0h).pin_memory()
             X = torch.empty(X0.shape, dtype=torch.float64, device=dev)
@@ -262,58 +461,10 @@ def run_ours(args):
     stream.synchronize()
     if partitioned:
         comm = arr.Comm.from_torch_distributed()
-    ctx = arr.eig_init(Ad, spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm, plan=plan)
-    ctx_lean = ctx.workspace_bytes < 8 * nrows * spec.w * (spec.p + 2)
-    if args.filter != "cheb":
-        ctx.eig_set_filter(args.filter)
-    sched = None
-    if spec.kind in ("lap3dV", "st27") and not partitioned:
-        # 3-D grids: y-band processing order (results unchanged; shorter L2 reuse distance of the
-        # z-neighbour rows), band height and tile rows measured on B200 (profiles/)
-        from paper_1507_06078_b200 import schedule
-        by, tile = {"lap3dV": (10, 16), "st27": (8, 32)}[spec.kind]
-        ctx.eig_set_schedule(*schedule.yband_3d(spec.size, spec.size, spec.size, by, tile))
-        sched = f"y-band by={by}, {tile}-row tiles"
-
-    def reset_X():
-        X.copy_(X0, non_blocking=True)
-
-    def one_solve():
-        return ctx.eig_solve(X, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max, adapt=args.adapt,
-                             inner_solver=args.inner_solver)
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            reset_X()
-            ev, res, info = one_solve()
-    ctx.eig_set_timing(True)
-    launches0 = ctx.launch_count
-    sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    sampler.start()
-    step_ms = []
-    infos = []
-    with torch.cuda.stream(stream):
-        for _ in range(args.steps):
-            reset_X()  # X <- X0 (outside the events)
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            ev, res, info = one_solve()
-            e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            infos.append((info.converged, info.outer, info.sweeps, info.maxres, info.locked, info.p_final, info.d_final))
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    launches = ctx.launch_count - launches0
-    phase_ms, phase_cnt = ctx.eig_phase_times()
-    total_ms = float(sum(step_ms))
+    r = solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, args.steps, args.warmup, plan=plan,
+                  comm=comm, world=world, dist=dist)
+    ctx = r["ctx"]
+    total_ms = float(sum(r["step_ms"]))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -321,32 +472,9 @@ def run_ours(args):
     # eigenpairs/s: each replica (or the one partitioned job) finds k pairs per step
     jobs = 1 if partitioned else world
     value = spec.k * args.steps * jobs / (total_ms / 1000.0)
-
-    # roofline of the dominant kernel (filter degree), algorithmic bytes of this rank's rows
-    peak, peak_src = load_peaks()
-    deg_ms = phase_ms[0] / max(1, phase_cnt[0])
     nnz_loc = int(Aloc.nnz) if not partitioned else plan.nnz
-    bpl = filter_bytes_per_degree(r1 - r0, nnz_loc, spec.w, spec.d)
-    if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
-        bpl += 8 * (r1 - r0) * spec.w
-    achieved = bpl / (deg_ms / 1000.0) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "spmm_tile_kernel (one fused Chebyshev filter degree)",
-                "bytes_per_launch": bpl, "avg_launch_us": deg_ms * 1000.0, "launches": int(phase_cnt[0]),
-                "peak_source": peak_src,
-                "share_of_step": phase_ms[0] / sum(step_ms),
-                "phase_ms_per_step": {"filter_degrees": phase_ms[0] / args.steps, "arr_project": phase_ms[1] / args.steps,
-                                      "arr_basis": phase_ms[3] / args.steps, "arr_H": phase_ms[4] / args.steps,
-                                      "arr_small_eig": phase_ms[5] / args.steps,
-                                      "residuals": phase_ms[2] / args.steps}}
+    roofline = roofline_of(r, spec, r1 - r0, nnz_loc, args, args.steps)
+
     # the DMMA Gram kernel of A4 (X^T Y, n x w by n x w, 2 n w^2 flops) timed alone on this block
     dense = None
     try:
@@ -383,8 +511,34 @@ def run_ours(args):
                                                      + 16 * (r1 - r0) * spec.w)
     ctx.close()
     Y2 = G = None  # the dense-Gram measurement held X (or X0)
-    del X, X0, flush, Ad, Y2, G
+    del X, X0, Y2, G
+    _AD.clear()
     torch.cuda.empty_cache()
+
+    # secondary: the BASELINE.json configs[1] workload (cfg2), a short solve on one GPU
+    secondary = None
+    if world == 1 and not args.no_secondary and args.config != 2:
+        try:
+            A2, spec2 = configs.build_config(2)
+            with torch.cuda.stream(stream):
+                X02 = torch.from_numpy(configs.starting_block(spec2)).to(dev)
+                X2 = torch.empty_like(X02)
+            args2 = argparse.Namespace(**vars(args))
+            args2.config = 2
+            r2 = solve_run(arr, torch, spec2, A2, A2, X02, X2, flush, stream, dev, args2, 3, 2)
+            tot2 = float(sum(r2["step_ms"]))
+            i2 = r2["infos"][-1]
+            secondary = {"workload": spec2.name, "value": spec2.k * 3 / (tot2 / 1e3), "unit": UNIT,
+                         "ms_per_step": tot2 / 3, "steps": 3, "warmup": 2, "spmm_path": r2["path"],
+                         "converged": bool(i2.converged), "outer": i2.outer, "sweeps": i2.sweeps,
+                         "maxres": i2.maxres, "roofline": roofline_of(r2, spec2, A2.n, A2.nnz, args2, 3),
+                         "clocks": r2["clocks"]}
+            r2["ctx"].close()
+            del X2, X02
+            _AD.clear()
+            torch.cuda.empty_cache()
+        except Exception as exc:  # noqa: BLE001
+            secondary = {"error": str(exc)[:200]}
 
     # e2e through the public API with HOST buffers: H2D of the CSR + X0 and D2H of the
     # eigenpairs inside the timed region (one GPU: the eig_solve_host C-ABI call;
@@ -399,6 +553,7 @@ def run_ours(args):
             rp = torch.from_numpy(np.ascontiguousarray(Aloc.row_ptr)).pin_memory()
             ci = torch.from_numpy(np.ascontiguousarray(Aloc.col_idx)).pin_memory()
             va = torch.from_numpy(np.ascontiguousarray(Aloc.val)).pin_memory()
+            grid = stencil_grid(spec) if (not partitioned and use_stencil(spec, args)) else None
             e2e_s = []
             for _ in range(max(1, args.steps)):
                 if world > 1:
@@ -407,7 +562,7 @@ def run_ours(args):
                 t = time.perf_counter()
                 if not partitioned:
                     arr.eig_solve_host(A.n, rp, ci, va, spec.k, spec.p, spec.d, xp, tol=spec.tol, maxit=spec.maxit,
-                                       s_max=spec.s_max, evec=evec, stream=stream)
+                                       s_max=spec.s_max, evec=evec, stream=stream, grid=grid)
                 else:
                     with torch.cuda.stream(stream):
                         Ad2 = arr.DeviceCSR(plan.n_own, rp.to(dev, non_blocking=True), ci.to(dev, non_blocking=True),
@@ -429,7 +584,8 @@ def run_ours(args):
                    "h2d_bytes_per_step": int(8 * (r1 - r0 + 1) + 12 * nnz_loc + 8 * nrows * spec.w),
                    "d2h_bytes_per_step": int(16 * spec.k + 8 * (r1 - r0) * spec.k),
                    "step_ms": [round(1e3 * x, 3) for x in e2e_s],
-                   "api": ("eig_solve_host (C-ABI, pinned host buffers, device alloc + copies inside)" if not partitioned
+                   "api": ("eig_solve_host (C-ABI, pinned host buffers, device alloc + copies inside"
+                           + (", stencil grid declared" if grid else "") + ")" if not partitioned
                            else "per rank: H2D of local CSR + X0 rows, eig_init_dist + eig_solve, D2H of the local "
                                 "eigenvector rows (bytes of rank 0)")}
         except Exception as exc:  # noqa: BLE001  (e.g. ARR_ENOMEM: the host-buffer call needs its own copies)
@@ -437,58 +593,35 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cnt = oracle_counts(args.config)
-        S, O = (cnt["sweeps"], cnt["outer"]) if cnt else (infos[-1][2], infos[-1][1])
-        if args.config <= 2:
-            ts, ta = oracle_sample(A, spec, synth.starting_block(spec))
-            smp = f"one MPM sweep ({ts:.2f} s) + one ARR+residuals ({ta:.2f} s) of {spec.name}"
-        else:  # bounded: a 16-column filter sweep, scaled to w columns; the ARR is not sampled
-            ts = oracle_filter_sample(A, spec) * spec.w / 16
-            ta = 0.0
-            smp = f"one MPM sweep of 16 of the {spec.w} columns of {spec.name}, x w/16 (ARR not sampled)"
-        cpu = {"value": spec.k / (S * ts + O * ta), "unit": UNIT,
-               "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())), "kind": "oracle",
-               "sample": smp + f", extrapolated to {S} sweeps / {O} ARR steps "
-                               f"({'oracle full-solve counts, tests/golden' if cnt else 'GPU solve counts'})"}
+        ts, smp = oracle_step_estimate(A, spec, args.config)
+        one = single_thread_leg(args.config)
+        cpu = {"value": spec.k / ts, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
+               "kind": "oracle", "sample": smp, "cpu": cpu_info(),
+               "single_thread": ({"value": spec.k / one["seconds"], "unit": UNIT, "cores": 1,
+                                  "sample": one["sample"] + " (OMP/BLAS threads = 1)"} if "seconds" in one else one)}
 
     if rank == 0:
-        conv, outer, sweeps, maxres, locked, p_fin, d_fin = infos[-1]
+        info = r["infos"][-1]
         par = ("1 GPU" if world == 1 else
                (f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
                 if partitioned else f"{world} independent replicas (no collective)"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": spec.name, "n": A.n, "nnz": A.nnz, "k": spec.k, "w": spec.w, "d": spec.d,
-                           "p": spec.p, "tol": spec.tol, "step": "one full eig_solve from X0",
-                           "filter": {"cheb": "T_d (Eq. cheby-poly)", "interp": "psi_d (paper Section 5)"}[args.filter],
-                           "adapt": args.adapt, "inner_solver": args.inner_solver,
-                           "l2": "flushed between timed steps (256 MiB write), outside the events",
-                           "parallelism": par, "row_order": sched or "natural",
-                           "context": "lean (no scratch block)" if ctx_lean else "standard",
-                           "converged": bool(conv), "outer": outer, "sweeps": sweeps, "maxres": maxres,
-                           "locked": locked, "p_final": p_fin, "d_final": d_fin},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks}
+                "data": "synthetic", "parallelism": par,
+                "config": config_dict(spec, A, args),
+                "run": {"spmm_path": r["path"], "context": "lean (no scratch block)" if r["lean"] else "standard",
+                        "converged": bool(info.converged), "outer": info.outer, "sweeps": info.sweeps,
+                        "maxres": info.maxres, "locked": info.locked, "p_final": info.p_final,
+                        "d_final": info.d_final, "step_ms": [round(x, 3) for x in r["step_ms"]]},
+                "roofline": roofline, "secondary": secondary, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(r["launches"]), "clocks": r["clocks"]}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
-
-
-def oracle_filter_sample(A, spec):
-    """Seconds of one oracle MPM sweep on 16 columns of the workload."""
-    import oracle
-    X = synth.gaussian_block_rows(A.n, 16, spec.seed, 0, A.n)
-    a = oracle.gershgorin_lower(A)
-    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
-    upper = float(np.bincount(rows, weights=np.abs(A.val), minlength=A.n).max())
-    t0 = time.perf_counter()
-    oracle.mpm_sweep(A, a, a + 0.9 * (upper - a), spec.d, X)
-    return time.perf_counter() - t0
 
 
 def main():

@@ -429,7 +429,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
     d_cur = 3 if (adapt & 2) and d_max > 3 else d_max
     X = np.array(X0[:, :w], dtype=np.float64, copy=True)
     a = gershgorin_lower(A)
-    mu0, _, _ = rayleigh_ritz(A, X)
+    mu0, _, _ = arr(A, X, 0, method=arr_method)  # RR(A, X0) = ARR with p = 0
     b = float(mu0[w - 1])
     if not a < b:
         a = b - 1e-8 * (abs(b) + 1.0)
@@ -521,7 +521,7 @@ def solve_deflate(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10,
     gamma = None if filter == "cheb" else interp_coeffs(d)
     X = np.array(X0[:, :w], dtype=np.float64, copy=True)
     a = gershgorin_lower(A)
-    mu0, _, _ = rayleigh_ritz(A, X)
+    mu0, _, _ = arr(A, X, 0, method=arr_method)
     b, mu1 = float(mu0[w - 1]), float(mu0[0])
     if not a < b:
         a = b - 1e-8 * (abs(b) + 1.0)
