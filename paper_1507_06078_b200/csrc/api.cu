@@ -238,6 +238,81 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
     return rows;
 }
 
+// The d degree launches of one filter_step as a CUDA graph (single-GPU contexts): the
+// launches are captured once per (operands, interval, width, degree, path) and replayed;
+// a new interval re-captures and updates the instantiated graph in place (same topology,
+// new kernel arguments).  `run` issues the launches and returns the partial-row count of
+// the last launch (< 0 on an unsupported width).  ARRABIT_GRAPH=0 launches directly.
+struct GraphKey {
+    const void *X, *T, *part, *sched_row0;
+    int64_t ldx;
+    double a, b;
+    int w, d, kind, sign, normalize, stencil;
+    bool operator==(const GraphKey &o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+template <class Run>
+int run_degrees(arr_ctx *c, const GraphKey &key_in, Run run) {
+    static const bool enabled = [] { const char *e = getenv("ARRABIT_GRAPH"); return !(e && atoi(e) == 0); }();
+    if (!enabled || is_dist(c)) return run();
+    GraphKey key;
+    memset(&key, 0, sizeof(key));  // padding bytes compared by memcmp
+    key.X = key_in.X; key.T = key_in.T; key.part = key_in.part; key.sched_row0 = key_in.sched_row0;
+    key.ldx = key_in.ldx; key.a = key_in.a; key.b = key_in.b; key.w = key_in.w; key.d = key_in.d;
+    key.kind = key_in.kind; key.sign = key_in.sign; key.normalize = key_in.normalize; key.stencil = key_in.stencil;
+    if (!(c->g_exec && c->g_key_set && key == *reinterpret_cast<const GraphKey *>(c->g_key))) {
+        const uint64_t l0 = c->launches;
+        const int64_t s0 = c->spmm_blocks;
+        if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+            cudaGetLastError();
+            return run();
+        }
+        const int nb = run();
+        cudaGraph_t g = nullptr;
+        if (cudaStreamEndCapture(c->stream, &g) != cudaSuccess || nb < 0 || !g) {
+            cudaGetLastError();
+            if (g) cudaGraphDestroy(g);
+            c->launches = l0;
+            c->spmm_blocks = s0;
+            return nb < 0 ? nb : run();
+        }
+        bool ok = false;
+        if (c->g_exec) {
+            cudaGraphExecUpdateResultInfo info;
+            ok = cudaGraphExecUpdate(c->g_exec, g, &info) == cudaSuccess;
+            if (!ok) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(c->g_exec);
+                c->g_exec = nullptr;
+            }
+        }
+        if (!ok && cudaGraphInstantiate(&c->g_exec, g, 0) != cudaSuccess) {
+            cudaGetLastError();
+            c->g_exec = nullptr;
+            cudaGraphDestroy(g);
+            c->launches = l0;
+            c->spmm_blocks = s0;
+            return run();
+        }
+        cudaGraphDestroy(g);
+        c->g_kernels = c->launches - l0;
+        c->g_spmm = c->spmm_blocks - s0;
+        c->launches = l0;
+        c->spmm_blocks = s0;
+        c->g_nblk = nb;
+        memcpy(c->g_key, &key, sizeof(GraphKey));
+        c->g_key_set = true;
+    }
+    if (cudaGraphLaunch(c->g_exec, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        c->g_key_set = false;
+        return run();
+    }
+    c->launches += c->g_kernels;
+    c->spmm_blocks += c->g_spmm;
+    return c->g_nblk;
+}
+static_assert(sizeof(GraphKey) <= 128, "graph key storage");
+
 // G = X^T Y over the owned rows, summed over ranks.
 arr_status gram_x(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2, double *G,
                   int64_t ldg) {
@@ -280,27 +355,34 @@ arr_status filter_interp(arr_ctx *c, double *X, int64_t ldx, int normalize, doub
     else { buf[0] = c->Q; ldb[0] = ldQ(c); buf[1] = c->Q + w; ldb[1] = ldQ(c); }
     int nblk = 0;
     const int ev0 = t_mark(c);
-    for (int k = d - 1; k >= 0; --k) {
-        SpmmArgs s{};
-        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
-        s.n = c->A.n; s.w = w;
-        // S y = c_1 (A y + (c_0/c_1) y): alpha * (A y - shift * y) with shift = -c_0/c_1
-        s.shift = -c0 / c1;
-        s.alpha = (k == 0 ? 1.0 : 2.0) * c1;
-        double gx = a[k];
-        if (k == d - 1) { s.Yin = X; s.ld_in = ldx; s.alpha *= a[d]; }  // b_d = a_d X
-        else { s.Yin = buf[(k + 1) & 1]; s.ld_in = ldb[(k + 1) & 1]; }
-        if (k + 2 == d) gx -= a[d];  // - b_d = - a_d X folds into the X term
-        else if (k + 2 < d) { s.Yprev = buf[k & 1]; s.ld_prev = ldb[k & 1]; s.beta = -1.0; }
-        s.Xa = X; s.ld_xa = ldx; s.gxa = gx;
-        s.Yout = buf[k & 1]; s.ld_out = ldb[k & 1];
-        s.partials = (normalize && k == 0) ? c->part : nullptr;
-        arr_status st;
-        const int g = spmm_x(c, s, &st);
-        if (st != ARR_OK) return st;
-        if (g < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
-        nblk = g;
-    }
+    arr_status st = ARR_OK;
+    auto run = [&]() -> int {
+        int g = 0;
+        for (int k = d - 1; k >= 0; --k) {
+            SpmmArgs s{};
+            s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+            s.n = c->A.n; s.w = w;
+            // S y = c_1 (A y + (c_0/c_1) y): alpha * (A y - shift * y) with shift = -c_0/c_1
+            s.shift = -c0 / c1;
+            s.alpha = (k == 0 ? 1.0 : 2.0) * c1;
+            double gx = a[k];
+            if (k == d - 1) { s.Yin = X; s.ld_in = ldx; s.alpha *= a[d]; }  // b_d = a_d X
+            else { s.Yin = buf[(k + 1) & 1]; s.ld_in = ldb[(k + 1) & 1]; }
+            if (k + 2 == d) gx -= a[d];  // - b_d = - a_d X folds into the X term
+            else if (k + 2 < d) { s.Yprev = buf[k & 1]; s.ld_prev = ldb[k & 1]; s.beta = -1.0; }
+            s.Xa = X; s.ld_xa = ldx; s.gxa = gx;
+            s.Yout = buf[k & 1]; s.ld_out = ldb[k & 1];
+            s.partials = (normalize && k == 0) ? c->part : nullptr;
+            g = spmm_x(c, s, &st);
+            if (st != ARR_OK || g < 0) return g < 0 ? g : 0;
+        }
+        return g;
+    };
+    GraphKey key{X, buf[0], normalize ? c->part : nullptr, c->tile_row0, ldx, c->a, c->b, w, d, 1, c->sign, normalize,
+                 c->st.on ? 1 : 0};
+    nblk = run_degrees(c, key, run);
+    if (st != ARR_OK) return st;
+    if (nblk < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
     t_add(c, 0, ev0, t_mark(c), d);
     CHECK_LAUNCH();
     if (normalize) {
@@ -323,31 +405,39 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
     const int64_t lt = c->T ? ldT(c) : ldQ(c);
     double *cur = X;
     int64_t ldcur = ldx;
-    double *other = T;
-    int64_t ldother = lt;
     int nblk = 0;
     const int ev0 = t_mark(c);
-    for (int j = 0; j < c->d; ++j) {
-        SpmmArgs s{};
-        s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
-        s.n = c->A.n; s.w = w;
-        s.Yin = cur; s.ld_in = ldcur;
-        if (j == 0) {
-            s.Yprev = nullptr; s.alpha = 1.0 / e; s.beta = 0.0;
-        } else {
-            s.Yprev = other; s.ld_prev = ldother; s.alpha = 2.0 / e; s.beta = -1.0;
+    arr_status st = ARR_OK;
+    auto run = [&]() -> int {
+        double *cu = X, *ot = T;
+        int64_t ldc = ldx, ldo = lt;
+        int g = 0;
+        for (int j = 0; j < c->d; ++j) {
+            SpmmArgs s{};
+            s.row_ptr = c->A.row_ptr; s.col = c->A.col_idx; s.val = c->A.val;
+            s.n = c->A.n; s.w = w;
+            s.Yin = cu; s.ld_in = ldc;
+            if (j == 0) {
+                s.Yprev = nullptr; s.alpha = 1.0 / e; s.beta = 0.0;
+            } else {
+                s.Yprev = ot; s.ld_prev = ldo; s.alpha = 2.0 / e; s.beta = -1.0;
+            }
+            s.shift = cc;
+            s.Yout = ot; s.ld_out = ldo;
+            s.partials = (normalize && j == c->d - 1) ? c->part : nullptr;
+            g = spmm_x(c, s, &st);
+            if (st != ARR_OK || g < 0) return g < 0 ? g : 0;
+            std::swap(cu, ot);
+            std::swap(ldc, ldo);
         }
-        s.shift = cc;
-        s.Yout = other; s.ld_out = ldother;
-        s.partials = (normalize && j == c->d - 1) ? c->part : nullptr;
-        arr_status st;
-        const int g = spmm_x(c, s, &st);
-        if (st != ARR_OK) return st;
-        if (g < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
-        nblk = g;
-        std::swap(cur, other);
-        std::swap(ldcur, ldother);
-    }
+        return g;
+    };
+    GraphKey key{X, T, normalize ? c->part : nullptr, c->tile_row0, ldx, c->a, c->b, w, c->d, 0, c->sign, normalize,
+                 c->st.on ? 1 : 0};
+    nblk = run_degrees(c, key, run);
+    if (st != ARR_OK) return st;
+    if (nblk < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
+    if (c->d % 2 == 1) { cur = T; ldcur = lt; }  // Y_d is in the scratch block after an odd degree count
     t_add(c, 0, ev0, t_mark(c), c->d);
     CHECK_LAUNCH();
     if (normalize) {
@@ -924,6 +1014,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
     stencil_release(c);
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
                     c->trtri_dwork};

@@ -3,6 +3,7 @@
 // tcgen05 has no f64 kind).  Gram products are split over rows with a fixed-
 // order reduction of the partial tiles (deterministic, no atomics).
 #include <math.h>
+#include <stdlib.h>
 
 #include <cmath>
 
@@ -389,6 +390,188 @@ __global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gemm_kernel_ca(double 
 
 bool ca_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
 
+// ---------------------------------------------------------------- large tiles
+// 128 x 128 CTA tiles, 16 warps of 32 x 32 (4 x 4 DMMA m8n8k4 tiles each), KS = 16 rows
+// (Gram) / k-columns (GEMM) per stage, an S_BIG-stage cp.async ring (S_BIG - 1 stages in
+// flight): every staged 16 x 128 panel feeds 4x the DMMAs of the 64 x 64 kernels' (half
+// the L2 -> SM bytes per flop).  Warp sub-tiles that lie outside the output (or,
+// symmetric, strictly below the diagonal) skip their DMMAs, so a width w pays for
+// ceil(w / 32) warp columns, not ceil(w / 128) CTA columns.  Same fragments and
+// per-element k order as the 64 x 64 kernels (only the split and the tile sizes differ).
+constexpr int BT = 128, BWM = 32, BWN = 32, BTHREADS = 512;
+#ifndef ARR_DMMA_BIG_STAGES
+#define ARR_DMMA_BIG_STAGES 3
+#endif
+constexpr int S_BIG = ARR_DMMA_BIG_STAGES;
+constexpr int BPAD = 4;
+
+__global__ void __launch_bounds__(BTHREADS, 1) gram_kernel_big(const double *__restrict__ X, int64_t ldx, int m1,
+                                                              const double *__restrict__ Y, int64_t ldy, int m2,
+                                                              int64_t n, int64_t rows_per_split, bool sym,
+                                                              double *__restrict__ part) {
+    const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
+    if (sym && tb < ta) return;
+    const int a0 = ta * BT, b0 = tb * BT;
+    const int64_t k0 = (int64_t)split * rows_per_split;
+    int64_t k1 = k0 + rows_per_split;
+    if (k1 > n) k1 = n;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm);
+    double (*Ys)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm + S_BIG * KS * (BT + BPAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;  // 4 x 4 warps
+    const int ra0 = a0 + wm * BWM, cb0 = b0 + wn * BWN;
+    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + BWN);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // one stage = KS rows x 128 columns of X and of Y = 2 x 1024 chunks of 16 bytes, 2 + 2 per thread
+    auto load = [&](int64_t kb, int st) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int idx = tid + q * BTHREADS;
+            const int rr = idx >> 6, cc = (idx & 63) * 2;
+            const int64_t row = kb + rr;
+            const bool rok = row < k1;
+            const int nx = rok ? max(0, min(2, m1 - (a0 + cc))) : 0;
+            const int ny = rok ? max(0, min(2, m2 - (b0 + cc))) : 0;
+            ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
+            ca16(&Ys[st][rr][cc], ny ? Y + row * ldy + b0 + cc : Y, ny * 8);
+        }
+    };
+    const int64_t nk = (k1 - k0 + KS - 1) / KS;
+#pragma unroll
+    for (int st = 0; st < S_BIG - 1; ++st) {
+        if (st < nk) load(k0 + st * KS, st);
+        ca_commit();
+    }
+    for (int64_t it = 0; it < nk; ++it) {
+        ca_wait<S_BIG - 2>();
+        __syncthreads();
+        const int64_t nx = it + S_BIG - 1;
+        if (nx < nk) load(k0 + nx * KS, (int)(nx % S_BIG));
+        ca_commit();
+        const int buf = (int)(it % S_BIG);
+        if (work) {
+#pragma unroll
+            for (int kk = 0; kk < KS / 4; ++kk) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * BWM + mt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * BWN + nt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+            }
+        }
+    }
+    ca_wait<0>();
+    if (!work) return;
+    double *P = part + (int64_t)split * m1 * m2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int ra = ra0 + mt * 8 + (lane >> 2);
+                const int cb = cb0 + nt * 8 + (lane & 3) * 2 + e;
+                if (ra < m1 && cb < m2) P[(int64_t)ra * m2 + cb] = acc[mt][nt][e];
+            }
+}
+
+__global__ void __launch_bounds__(BTHREADS, 1) gemm_kernel_big(double alpha, const double *__restrict__ X, int64_t ldx,
+                                                              int m1, const double *__restrict__ B, int64_t ldb, int m2,
+                                                              double beta, const double *Cin, int64_t ldc, double *Out,
+                                                              int64_t ldo, int64_t n, int upper) {
+    const int nct = (m2 + BT - 1) / BT;
+    const int64_t r0 = (int64_t)(blockIdx.x / nct) * BT;
+    const int c0 = (int)(blockIdx.x % nct) * BT;
+    if (upper && c0 + BT < m1) m1 = c0 + BT;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[BT][KS + BPAD] = reinterpret_cast<double (*)[BT][KS + BPAD]>(dsm);
+    double (*Bs)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm + S_BIG * BT * (KS + BPAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;  // 4 x 4 warps
+    const bool work = (r0 + wm * BWM < n) && (c0 + wn * BWN < m2);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // one stage = 128 rows x 16 k of X (8 chunks per row) and 16 k x 128 columns of B (64 chunks per row)
+    auto load = [&](int kb, int st) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int idx = tid + q * BTHREADS;
+            const int xr = idx >> 3, xk = (idx & 7) * 2;
+            const int64_t row = r0 + xr;
+            const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
+            ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
+            const int bk = idx >> 6, bc = (idx & 63) * 2;
+            const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
+            ca16(&Bs[st][bk][bc], nb ? B + (int64_t)(kb + bk) * ldb + c0 + bc : B, nb * 8);
+        }
+    };
+    const int nk = (m1 + KS - 1) / KS;
+#pragma unroll
+    for (int st = 0; st < S_BIG - 1; ++st) {
+        if (st < nk) load(st * KS, st);
+        ca_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        ca_wait<S_BIG - 2>();
+        __syncthreads();
+        const int nx = it + S_BIG - 1;
+        if (nx < nk) load(nx * KS, nx % S_BIG);
+        ca_commit();
+        const int buf = it % S_BIG;
+        if (work) {
+#pragma unroll
+            for (int kk = 0; kk < KS / 4; ++kk) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * BWM + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * BWN + nt * 8 + (lane >> 2)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+            }
+        }
+    }
+    ca_wait<0>();
+    if (!work) return;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t row = r0 + wm * BWM + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * BWN + nt * 8 + (lane & 3) * 2 + e;
+                if (row < n && cb < m2) {
+                    double v = alpha * acc[mt][nt][e];
+                    if (beta != 0.0) v += beta * Cin[row * ldc + cb];
+                    Out[row * ldo + cb] = v;
+                }
+            }
+}
+
+// the large tiles pay off once both output dimensions span more than one 64-wide tile
+#ifndef ARR_DMMA_BIG_MIN
+#define ARR_DMMA_BIG_MIN 160
+#endif
+bool use_big(int d1, int d2) {
+    static const int mn = [] { const char *e = getenv("ARRABIT_DMMA_BIG"); return e ? atoi(e) : ARR_DMMA_BIG_MIN; }();
+    return mn > 0 && d1 >= mn && d2 >= mn;
+}
+
 // ---------------------------------------------------------------- small dense
 __global__ void svqb_prep_kernel(const double *__restrict__ G, int w, double *__restrict__ D,
                                  double *__restrict__ Gs) {
@@ -451,11 +634,14 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 // partial second wave would idle most SMs for a whole CTA lifetime), at least 512
 // rows each.  sym: only the upper tiles do work.
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
-    const int64_t ta = (m1 + TILE - 1) / TILE, tb = (m2 + TILE - 1) / TILE;
+    const bool big = use_big(m1, m2);
+    const int T = big ? BT : TILE;
+    const int64_t ta = (m1 + T - 1) / T, tb = (m2 + T - 1) / T;
     const int64_t tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
 #if ARR_DMMA_CA
-    static LaunchCache cache;
-    const int per_sm = cached_occupancy(cache, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
+    static LaunchCache cache, cache_big;
+    const int per_sm = big ? cached_occupancy(cache_big, gram_kernel_big, BTHREADS, sizeof(double) * 2 * S_BIG * KS * (BT + BPAD))
+                           : cached_occupancy(cache, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
 #else
     static const int per_sm = [] {
         int o = 0;
@@ -493,7 +679,13 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     rps = (rps + KS - 1) / KS * KS;
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
 #if ARR_DMMA_CA
-    if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
+    if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(Y, ldy)) {
+        const size_t smem = sizeof(double) * 2 * S_BIG * KS * (BT + BPAD);
+        static LaunchCache cache;
+        cached_occupancy(cache, gram_kernel_big, BTHREADS, smem);
+        dim3 gb((m1 + BT - 1) / BT, (m2 + BT - 1) / BT, ns);
+        gram_kernel_big<<<gb, BTHREADS, smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    } else if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
         const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
         static LaunchCache cache;
         cached_occupancy(cache, gram_kernel_ca, THREADS, smem);  // sets the smem attribute once
@@ -510,7 +702,14 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
                  int64_t n, int upper) {
     const unsigned grid = (unsigned)(((n + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE));
 #if ARR_DMMA_CA
-    if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
+    if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(B, ldb)) {
+        const size_t smem = sizeof(double) * S_BIG * (BT * (KS + BPAD) + KS * (BT + BPAD));
+        static LaunchCache cache;
+        cached_occupancy(cache, gemm_kernel_big, BTHREADS, smem);
+        const unsigned gb = (unsigned)(((n + BT - 1) / BT) * ((m2 + BT - 1) / BT));
+        gemm_kernel_big<<<gb, BTHREADS, smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n,
+                                                          upper);
+    } else if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
         const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));
         static LaunchCache cache;
         cached_occupancy(cache, gemm_kernel_ca, THREADS, smem);  // sets the smem attribute once

@@ -62,6 +62,8 @@ struct StencilLaunch {
     int nx, ny, nz;
     int Px, Py, Lz, npx, npy, nzc, npan, pwv, NS;
     int box_x, box_y, hx, hy;
+    int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
+    int pf;  // L2 prefetch distance in steps (0: off)
 };
 
 struct arr_ctx {
@@ -106,6 +108,13 @@ struct arr_ctx {
     int orth_mode;          // 0 = shifted CholeskyQR3 (fallback SVQB), 1 = SVQB only
     cusolverDnHandle_t solver;
     size_t ws_bytes;
+    // filter degree loop as a CUDA graph (api.cu run_degrees)
+    cudaGraphExec_t g_exec;
+    alignas(8) unsigned char g_key[128];
+    bool g_key_set;
+    uint64_t g_kernels;
+    int64_t g_spmm;
+    int g_nblk;
     // bookkeeping
     const char *last_kernel;  // name of the kernel the last fused SpMM launched (eig_last_spmm_kernel)
     uint64_t launches;

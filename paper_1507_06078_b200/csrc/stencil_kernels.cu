@@ -23,6 +23,9 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "internal.cuh"
@@ -61,6 +64,13 @@ __device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int c0
         "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+// the same box into L2 only (no shared memory, no barrier): issued a few steps ahead of the
+// load so that the load finds its lines in L2 and more DRAM requests are in flight per SM
+__device__ __forceinline__ void tma_2d_prefetch(const CUtensorMap *map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
 }
 __device__ __forceinline__ uint64_t pol_evict_last() {
     uint64_t p;
@@ -157,14 +167,31 @@ void shape_slots(StencilSlots &sl) {
 struct Item {
     int panel, x0, y0, pxe, pye, zc0, zc1;
 };
+// Order of the work items.  Panel-major (PM): it = ((zc npan + panel) npy + py) npx + px,
+// so the G items running together are ~G patches of ONE panel in raster order: the x and y
+// halo lines two neighbouring patches both stage are fetched from DRAM once and hit L2 the
+// second time (panel-minor waves cover only G / (npx npan) patch rows).  Launches that
+// reduce column norms keep the panel-minor order, where a CTA owns one panel and its
+// partial sums stay static.
+template <bool PM>
 __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) {
     Item r;
-    r.panel = (int)(it % P.npan);
-    int64_t q = it / P.npan;
-    const int px = (int)(q % P.npx);
-    q /= P.npx;
-    const int py = (int)(q % P.npy);
-    const int zc = (int)(q / P.npy);
+    int px, py, zc;
+    if (PM) {
+        px = (int)(it % P.npx);
+        int64_t q = it / P.npx;
+        py = (int)(q % P.npy);
+        q /= P.npy;
+        r.panel = (int)(q % P.npan);
+        zc = (int)(q / P.npan);
+    } else {
+        r.panel = (int)(it % P.npan);
+        int64_t q = it / P.npan;
+        px = (int)(q % P.npx);
+        q /= P.npx;
+        py = (int)(q % P.npy);
+        zc = (int)(q / P.npy);
+    }
     r.x0 = px * P.Px;
     r.y0 = py * P.Py;
     r.pxe = min(P.Px, P.nx - r.x0);
@@ -233,7 +260,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
         const uint32_t boxline = (uint32_t)P.box_x * pwv * 16u, pline = (uint32_t)P.Px * pwv * 16u;
         uint32_t step = 0;
         for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
-            const Item I = decode_item(P, it);
+            const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
             const int col0 = I.panel * pwv * 2;  // first column of the panel
             const int zs = max(I.zc0 - 1, 0);
             for (int z = zs; z <= I.zc1; ++z, ++step) {
@@ -281,6 +308,28 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                         tma_2d(slot + (size_t)oy * vlb, &P.tm_val, 0, (int)row, full + b, pol_once);
                     }
                 }
+                // L2 prefetch of step z + PF's boxes (same item)
+                const int zp = z + P.pf;
+                if (P.pf > 0 && zp <= I.zc1) {
+                    const bool preal = zp < P.nz, pfin = zp - 1 >= I.zc0;
+                    const int pnb = preal ? P.box_y : 0, pnp = (pfin && (HAS_PREV || HAS_X)) ? I.pye : 0;
+                    const int pnv = (zp + 1 < I.zc1) ? I.pye : 0;
+                    for (int j = lane; j < pnb + pnp + pnv; j += 32) {
+                        if (j < pnb) {
+                            const int gy = I.y0 - P.hy + j;
+                            if (gy < 0 || gy >= P.ny) continue;
+                            tma_2d_prefetch(&P.tm_in, col0, (int)(((int64_t)zp * P.ny + gy) * P.nx + (I.x0 - P.hx)));
+                        } else if (j < pnb + pnp) {
+                            const int oy = j - pnb;
+                            const int row = (int)(((int64_t)(zp - 1) * P.ny + I.y0 + oy) * P.nx + I.x0);
+                            if (HAS_PREV) tma_2d_prefetch(&P.tm_prev, col0, row);
+                            if (HAS_X) tma_2d_prefetch(&P.tm_xa, col0, row);
+                        } else {
+                            const int oy = j - pnb - pnp;
+                            tma_2d_prefetch(&P.tm_val, 0, (int)(((int64_t)(zp + 1) * P.ny + I.y0 + oy) * P.nx + I.x0));
+                        }
+                    }
+                }
             }
         }
         return;
@@ -292,7 +341,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
     double ss0 = 0.0, ss1 = 0.0;
     int panel_of_cta = (int)(blockIdx.x % P.npan);
     for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
-        const Item I = decode_item(P, it);
+        const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
         const int pw = min(pwv, P.wv - I.panel * pwv);
         const int nrow = I.pxe * I.pye;
         const int colv0 = I.panel * pwv;
@@ -461,7 +510,15 @@ int launch_st(arr_ctx *c, StencilLaunch &L) {
     static LaunchCache cache;
     const int occ = cached_occupancy(cache, kern, kStThreads, smem);
     int64_t G = (int64_t)c->num_sms * occ;
-    G = (G / L.npan) * L.npan;  // each CTA keeps one panel (static column partial sums)
+    static const int pm_env = [] { const char *e = getenv("ARRABIT_ST_ORDER"); return e ? atoi(e) : 1; }();
+    static const int pf_env = [] { const char *e = getenv("ARRABIT_ST_PF"); return e ? atoi(e) : 3; }();
+    L.pf = pf_env;
+    static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
+    if (verbose)
+        fprintf(stderr, "stencil plan: shape %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu\n",
+                SH, L.w, L.Px, L.Py, L.npan, L.pwv, L.NS, L.Lz, L.nzc, (long long)L.nitems, (long long)G, smem);
+    L.pm = SUMSQ ? 0 : pm_env;
+    if (!L.pm) G = (G / L.npan) * L.npan;  // panel-minor: each CTA keeps one panel (static column partial sums)
     if (G > L.nitems) G = L.nitems;
     if (G < L.npan) G = L.npan;
     kern<<<(unsigned)G, kStThreads, smem, c->stream>>>(L);
@@ -513,9 +570,18 @@ bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, i
     const cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
     const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
+    // no L2 promotion: rows are only 16-byte aligned (ld = w), and promoting a box row's
+    // sectors to 128/256-byte blocks would fetch the neighbouring panel's bytes too
+    static const CUtensorMapL2promotion promo = [] {
+        const char *e = getenv("ARRABIT_ST_PROMO");
+        const int v = e ? atoi(e) : 0;
+        return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                        : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                   : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    }();
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim, gstride, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
 }
 
 }  // namespace

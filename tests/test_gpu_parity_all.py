@@ -138,8 +138,8 @@ def _st27_top(N, k):
     best = np.empty(0)
     for tk in t:
         v = prod * tk
-        best = np.concatenate([best, np.partition(v, k)[:k]])
-        best = np.partition(best, k)[:k]
+        best = np.concatenate([best, np.partition(v, k - 1)[:k]])
+        best = np.partition(best, k - 1)[:k]
     return np.sort(27.0 - best)[::-1]
 
 
