@@ -174,6 +174,27 @@ arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w, int
  * behaves as eig_init_w.  The plan's host arrays are copied. */
 arr_status eig_init_dist(arr_ctx **out, const arr_csr *A_local, int32_t k, int32_t w, int32_t p, int32_t d,
                          const arr_dist *dist, arr_comm *comm, void *stream);
+/* Column-partitioned context (Survey §8f-3), collective over the ranks of comm.
+ * MPM filters every column independently ("x_i <- rho(A) x_i"), so with A
+ * replicated a rank filters its column slice with NO communication; only the ARR
+ * projection (Alg. ARR) needs the whole block.  Rank r owns columns
+ * [col_begins[r], col_begins[r+1]) of every n x w block it passes (X: n x w_r, all n
+ * rows) and, for the ARR projection and the residuals, an internal row-partitioned
+ * context (as eig_init_dist) on rows [row_begins[r], row_begins[r+1]): A_rows / rows
+ * are that row block's local CSR and exchange plan (partition.colsplit_plan builds
+ * them).  Between the two, the block moves by one all-to-all transpose each way
+ * (comm.cu comm_transpose; 2 n w doubles per outer iteration in total over all
+ * ranks, against d x sweeps halo / all-gather exchanges of the row partition).
+ * A_full: the whole matrix on every rank.  row_begins / col_begins: host [size+1],
+ * identical on every rank, col_begins[size] = w.  Supported calls: filter_step
+ * (local), arr_project(_p) and residuals (column slices in and out), eig_solve
+ * (fixed parameters: adapt / gn / inner / exits -> ARR_EINVAL), the interval /
+ * degree / filter / mode / stencil / schedule setters (applied to the column
+ * context), spmm (whole A on this rank's columns), timing; gram / gemm /
+ * orthonormalize return ARR_EINVAL. */
+arr_status eig_init_colsplit(arr_ctx **out, const arr_csr *A_full, int32_t k, int32_t w, int32_t p, int32_t d,
+                             const arr_csr *A_rows, const arr_dist *rows, const int64_t *row_begins,
+                             const int64_t *col_begins, arr_comm *comm, void *stream);
 arr_status eig_destroy(arr_ctx *c);
 const char *eig_last_error(const arr_ctx *c);
 size_t eig_workspace_bytes(const arr_ctx *c);

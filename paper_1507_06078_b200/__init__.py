@@ -9,8 +9,10 @@ from .api import (  # noqa: F401
     ArrError,
     Comm,
     DeviceCSR,
+    ColSplitContext,
     EigContext,
     eig_init,
+    eig_init_colsplit,
     eig_solve_host,
     to_device_csr,
 )

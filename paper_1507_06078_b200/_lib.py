@@ -19,7 +19,7 @@ EXPORTED = [
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "eig_set_filter", "eig_set_mode", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
     "eig_set_timing", "eig_phase_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active", "eig_last_spmm_kernel",
-    "eig_init_dist", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
+    "eig_init_dist", "eig_init_colsplit", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
 ]
 
 
@@ -69,6 +69,8 @@ def load(path: str = LIB_PATH):
         "eig_init_w": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, vp], ctypes.c_int),
         "eig_init_dist": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, ctypes.POINTER(arr_dist), vp, vp],
                           ctypes.c_int),
+        "eig_init_colsplit": ([pvp, ctypes.POINTER(arr_csr), i32, i32, i32, i32, ctypes.POINTER(arr_csr),
+                               ctypes.POINTER(arr_dist), vp, vp, vp, vp], ctypes.c_int),
         "comm_get_nccl_id": ([ctypes.c_char_p], ctypes.c_int),
         "comm_init_nccl": ([pvp, ctypes.c_char_p, i32, i32], ctypes.c_int),
         "comm_init_local_group": ([pvp, i32], ctypes.c_int),

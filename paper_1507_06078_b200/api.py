@@ -328,6 +328,54 @@ class EigContext:
         return ev, res, info
 
 
+class ColSplitContext(EigContext):
+    """A column-partitioned context (eig_init_colsplit): blocks are this rank's column
+    slice (n x w_r, all rows); A_full is the whole matrix on every rank, A_rows and
+    ``plan`` (partition.ColSplitPlan) the row block of the internal ARR context."""
+
+    def __init__(self, A_full: DeviceCSR, A_rows: DeviceCSR, plan, k: int, p: int, d: int, w: int, comm,
+                 stream=None):
+        self.lib = _lib.load()
+        self.A, self.A_rows = A_full, A_rows
+        self.k, self.p, self.d, self.w = k, p, d, w
+        self.comm, self.plan = comm, plan
+        self.handle_stream, self.stream = _stream_handle(stream)
+        self._csr = arr_csr(A_full.n, A_full.nnz, A_full.row_ptr.data_ptr(), A_full.col_idx.data_ptr(),
+                            A_full.val.data_ptr())
+        self._csr_rows = arr_csr(A_rows.n, A_rows.nnz, A_rows.row_ptr.data_ptr(), A_rows.col_idx.data_ptr(),
+                                 A_rows.val.data_ptr())
+        ds, _keep = _dist_struct(plan.rows)
+        self._rb = np.ascontiguousarray(plan.row_begins, dtype=np.int64)
+        self._cb = np.ascontiguousarray(plan.col_begins, dtype=np.int64)
+        h = ctypes.c_void_p()
+        st = self.lib.eig_init_colsplit(ctypes.byref(h), ctypes.byref(self._csr), k, w, p, d,
+                                        ctypes.byref(self._csr_rows), ctypes.byref(ds),
+                                        ctypes.c_void_p(self._rb.ctypes.data), ctypes.c_void_p(self._cb.ctypes.data),
+                                        comm.h, self.handle_stream)
+        if st != 0:
+            raise ArrError(st, "eig_init_colsplit failed")
+        self.h = h
+
+    def residuals(self, Y: torch.Tensor, mu) -> np.ndarray:
+        """Residuals of the first len(mu) pairs; Y is this rank's column slice of the block."""
+        py, ldy, _ = _blk(Y, "Y")
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        res = np.empty(len(mu))
+        self._check(self.lib.residuals(self.h, py, ldy, mu.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(mu),
+                                       res.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "residuals")
+        return res
+
+    @property
+    def w_local(self) -> int:
+        c0, c1 = self.plan.col_range
+        return c1 - c0
+
+
+def eig_init_colsplit(A_full: DeviceCSR, A_rows: DeviceCSR, plan, k: int, p: int, d: int, w: int, comm,
+                      stream=None) -> ColSplitContext:
+    return ColSplitContext(A_full, A_rows, plan, k, p, d, w, comm, stream)
+
+
 def eig_init(A: DeviceCSR, k: int, p: int, d: int, stream=None, w: int | None = None, comm=None,
              plan=None) -> EigContext:
     """eig_init (w = k) / eig_init_w (w >= k guard columns) / eig_init_dist (comm + plan)."""

@@ -294,6 +294,7 @@ int run_degrees(arr_ctx *c, const GraphKey &key_in, Run run) {
             return run();
         }
         cudaGraphDestroy(g);
+        c->g_last_kernel = c->last_kernel;
         c->g_kernels = c->launches - l0;
         c->g_spmm = c->spmm_blocks - s0;
         c->launches = l0;
@@ -309,6 +310,7 @@ int run_degrees(arr_ctx *c, const GraphKey &key_in, Run run) {
     }
     c->launches += c->g_kernels;
     c->spmm_blocks += c->g_spmm;
+    c->last_kernel = c->g_last_kernel;
     return c->g_nblk;
 }
 static_assert(sizeof(GraphKey) <= 128, "graph key storage");
@@ -861,8 +863,149 @@ arr_status solve_deflate(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opt
     return ARR_OK;
 }
 
+// ---------------------------------------------------------------- column-partitioned mode
+// (eig_init_colsplit; Survey §8f-3).  MPM filters every column independently
+// (P:552-566), so with A replicated the filter of a column slice needs no
+// communication at all; the ARR projection (Alg. ARR) needs the whole
+// block and runs on a row-partitioned context after an all-to-all transpose.
+namespace {
+arr_status cs_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *opts, double *eigval_host,
+                    double *res_host, arr_solve_info *info) {
+    ColSplit &S = *c->cs;
+    arr_ctx *cc = S.col, *cr = S.row;
+    if (opts->adapt || opts->gn || opts->inner || opts->exits)
+        return fail(c, ARR_EINVAL, "column split: only the fixed-parameter solve (no adapt / gn / inner / exits)");
+    const int w = c->w, k = c->k;
+    const int m = m_of(cr, cr->p);
+    std::vector<double> ritz(m), res(k), r0(w);
+    arr_solve_info inf{};
+    double a = 0.0;
+    arr_status st = eig_gershgorin_lower(cc, &a);  // the full A on every rank: the same bound
+    if (st != ARR_OK) return st;
+    if ((st = comm_transpose(c, S, 0, X, ldx, S.Xrow, S.ldrow)) != ARR_OK) return st;
+    if ((st = arr_core(cr, 0, S.Xrow, S.ldrow, nullptr, 0, r0.data(), nullptr)) != ARR_OK) return st;
+    double b = r0[w - 1], mu1 = r0[0];
+    if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    const int64_t spmm0 = cc->spmm_blocks + cr->spmm_blocks;
+    bool done = false, mono = false;
+    double prev_maxres = 0.0;
+    int32_t rank = 0;
+    for (int outer = 1; outer <= opts->maxit; ++outer) {
+        if ((st = eig_set_interval(cc, a, b)) != ARR_OK) return st;
+        const double ccen = 0.5 * (a + b), e = 0.5 * (b - a);
+        const double amp = fabs(cc->filter_kind == 1 ? psi_eval(cc->coef, (mu1 - ccen) / e) : chebT(cc->d, (mu1 - ccen) / e));
+        int s = opts->s_max;
+        if (amp > 1.0) s = !isfinite(amp) ? 1 : (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
+        CUDA_TRY(cudaMemsetAsync(cc->dinfo + INFO_BAD, 0, sizeof(int), cc->stream));
+        for (int q = 0; q < s; ++q)
+            if ((st = filter_core(cc, X, ldx, 1, nullptr)) != ARR_OK) return st;  // local: no exchange
+        inf.sweeps += s;
+        if ((st = comm_transpose(c, S, 0, X, ldx, S.Xrow, S.ldrow)) != ARR_OK) return st;
+        if ((st = arr_core(cr, cr->p, S.Xrow, S.ldrow, S.Xrow, S.ldrow, ritz.data(), &rank)) != ARR_OK) return st;
+        CUDA_TRY(cudaMemcpyAsync(cc->h_istage + 32, cc->dinfo + INFO_BAD, sizeof(int), cudaMemcpyDeviceToHost, cc->stream));
+        if ((st = residuals_core(cr, S.Xrow, S.ldrow, ritz.data(), k, res.data())) != ARR_OK) return st;
+        if ((st = comm_transpose(c, S, 1, S.Xrow, S.ldrow, X, ldx)) != ARR_OK) return st;  // Ritz vectors back
+        // the flag is a per-rank local value; every rank stops together on any rank's flag
+        c->h_stage[0] = cc->h_istage[32] ? 1.0 : 0.0;
+        CUDA_TRY(cudaMemcpyAsync(cr->vecw, c->h_stage, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        ST_TRY(comm_allreduce(cr, cr->vecw, 1, 2));
+        CUDA_TRY(cudaMemcpyAsync(c->h_stage, cr->vecw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (c->h_stage[0] != 0.0) return fail(c, ARR_ENUMERIC, "zero or non-finite column norm after filtering");
+        double maxres = 0.0;
+        for (int i = 0; i < k; ++i) maxres = std::max(maxres, res[i]);
+        inf.outer = outer;
+        inf.maxres = maxres;
+        inf.last_rank = rank;
+        inf.a = a; inf.b = b;
+        if (maxres <= opts->tol) { done = true; inf.exit_rule = 1; break; }
+        mono = mono || (outer > 1 && maxres > 10.0 * prev_maxres);  // R3, as eig_solve
+        prev_maxres = maxres;
+        const double bn = ritz[std::min(w, m - 1)];
+        b = mono ? std::max(b, bn) : bn;
+        mu1 = ritz[0];
+        if (!(a < b)) a = b - 1e-8 * (fabs(b) + 1.0);
+    }
+    inf.p_final = cr->p;
+    inf.d_final = cc->d;
+    inf.converged = done ? 1 : 0;
+    inf.spmm_blocks = cc->spmm_blocks + cr->spmm_blocks - spmm0;
+    for (int i = 0; i < k; ++i) { eigval_host[i] = cr->sign * ritz[i]; res_host[i] = res[i]; }
+    if (info) *info = inf;
+    return ARR_OK;
+}
+
+void cs_release(arr_ctx *c) {
+    ColSplit *S = c->cs;
+    if (!S) return;
+    cudaStreamSynchronize(c->stream);
+    if (S->col) eig_destroy(S->col);
+    if (S->row) eig_destroy(S->row);
+    if (S->sendbuf) cudaFree(S->sendbuf);
+    if (S->recvbuf) cudaFree(S->recvbuf);
+    if (S->Xrow) cudaFree(S->Xrow);
+    delete S;
+    c->cs = nullptr;
+}
+
+}  // namespace
+
 // ====================================================================== C-ABI
 extern "C" {
+
+arr_status eig_init_colsplit(arr_ctx **out, const arr_csr *A_full, int32_t k, int32_t w, int32_t p, int32_t d,
+                             const arr_csr *A_rows, const arr_dist *rows, const int64_t *row_begins,
+                             const int64_t *col_begins, arr_comm *comm, void *stream) {
+    if (!out || !A_full || !A_rows || !rows || !row_begins || !col_begins || !comm) return ARR_EINVAL;
+    *out = nullptr;
+    int32_t R = 0, G = 1;
+    if (comm_rank_size(comm, &R, &G) != ARR_OK) return ARR_EINVAL;
+    const int64_t n = A_full->n;
+    if (row_begins[0] != 0 || row_begins[G] != n || col_begins[0] != 0 || col_begins[G] != w) return ARR_EINVAL;
+    for (int q = 0; q < G; ++q)
+        if (row_begins[q + 1] < row_begins[q] || col_begins[q + 1] <= col_begins[q]) return ARR_EINVAL;
+    if (rows->row_begin != row_begins[R] || A_rows->n != row_begins[R + 1] - row_begins[R] || rows->n_global != n)
+        return ARR_EINVAL;
+    const int32_t wr = (int32_t)(col_begins[R + 1] - col_begins[R]);
+    arr_ctx *c = new (std::nothrow) arr_ctx();
+    if (!c) return ARR_ENOMEM;
+    c->k = k; c->w = w; c->p = p; c->d = d;
+    c->stream = (cudaStream_t)stream;
+    c->poisoned = ARR_OK;
+    c->comm = comm;
+    c->nranks = G;
+    c->sign = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    ColSplit *S = new (std::nothrow) ColSplit();
+    if (!S) { delete c; return ARR_ENOMEM; }
+    c->cs = S;
+    S->rb.assign(row_begins, row_begins + G + 1);
+    S->cb.assign(col_begins, col_begins + G + 1);
+    arr_status st = eig_init_w(&S->col, A_full, wr, wr, 0, d, stream);  // the filter of this rank's columns
+    if (st == ARR_OK) st = eig_init_dist(&S->row, A_rows, k, w, p, d, rows, comm, stream);  // the ARR projection
+    const int64_t nrow_blk = A_rows->n + rows->n_ghost;
+    S->ldrow = ((int64_t)w + 1) & ~int64_t(1);
+    const int64_t nr = row_begins[R + 1] - row_begins[R];
+    S->buf_elems = (size_t)std::max<int64_t>(n * (((int64_t)wr + 1) & ~int64_t(1)), nr * ((int64_t)w + 2 * G));
+    if (st == ARR_OK && (cudaMalloc(&S->Xrow, sizeof(double) * (size_t)nrow_blk * S->ldrow) != cudaSuccess ||
+                         cudaMalloc(&S->sendbuf, sizeof(double) * S->buf_elems) != cudaSuccess ||
+                         cudaMalloc(&S->recvbuf, sizeof(double) * S->buf_elems) != cudaSuccess ||
+                         cudaMallocHost(&c->h_stage, sizeof(double) * 64) != cudaSuccess)) {
+        cudaGetLastError();
+        st = ARR_ENOMEM;
+    }
+    if (st != ARR_OK) {
+        cs_release(c);
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        delete c;
+        return st;
+    }
+    c->ws_bytes = S->col->ws_bytes + S->row->ws_bytes + sizeof(double) * ((size_t)nrow_blk * S->ldrow + 2 * S->buf_elems);
+    *out = c;
+    return ARR_OK;
+}
 
 arr_status eig_init(arr_ctx **out, const arr_csr *A, int32_t k, int32_t p, int32_t d, void *stream) {
     return eig_init_w(out, A, k, k, p, d, stream);
@@ -1012,6 +1155,12 @@ arr_status eig_init_w(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_in, 
 
 arr_status eig_destroy(arr_ctx *c) {
     if (!c) return ARR_EINVAL;
+    if (c->cs) {
+        cs_release(c);
+        if (c->h_stage) cudaFreeHost(c->h_stage);
+        delete c;
+        return ARR_OK;
+    }
     cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
@@ -1031,10 +1180,14 @@ arr_status eig_destroy(arr_ctx *c) {
 
 const char *eig_last_error(const arr_ctx *c) { return c ? c->err.c_str() : "null context"; }
 size_t eig_workspace_bytes(const arr_ctx *c) { return c ? c->ws_bytes : 0; }
-uint64_t eig_launch_count(const arr_ctx *c) { return c ? c->launches : 0; }
+uint64_t eig_launch_count(const arr_ctx *c) {
+    if (c && c->cs) return c->launches + c->cs->col->launches + c->cs->row->launches;
+    return c ? c->launches : 0;
+}
 
 arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out) {
     GUARD(c);
+    if (c->cs) return eig_gershgorin_lower(c->cs->col, a_out);
     if (!a_out) return fail(c, ARR_EINVAL, "a_out is NULL");
     int nb = 0;
     launch_gershgorin(c, c->part, &nb);
@@ -1049,6 +1202,7 @@ arr_status eig_gershgorin_lower(arr_ctx *c, double *a_out) {
 
 arr_status eig_set_interval(arr_ctx *c, double a, double b) {
     GUARD(c);
+    if (c->cs) ST_TRY(eig_set_interval(c->cs->col, a, b));
     if (!(a < b) || !isfinite(a) || !isfinite(b)) return fail(c, ARR_EINVAL, "interval needs finite a < b");
     c->a = a; c->b = b; c->have_interval = true;
     return ARR_OK;
@@ -1056,6 +1210,7 @@ arr_status eig_set_interval(arr_ctx *c, double a, double b) {
 
 arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t *tile_len, int64_t ntiles) {
     GUARD(c);
+    if (c->cs) return eig_set_schedule(c->cs->col, tile_row0, tile_len, ntiles);
     if (is_dist(c)) return fail(c, ARR_EINVAL, "schedule: not supported on a distributed context");
     if (!tile_row0) {
         c->tile_row0 = nullptr; c->tile_len = nullptr; c->ntiles = 0;
@@ -1074,6 +1229,7 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
 
 arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
     GUARD(c);
+    if (c->cs) return eig_set_stencil(c->cs->col, nx, ny, nz);  // the column context has the whole A
     if (is_dist(c) && (nx || ny || nz)) return fail(c, ARR_EINVAL, "stencil path: single-GPU contexts only");
     const arr_status st = stencil_setup(c, nx, ny, nz);
     if (st == ARR_EINVAL)
@@ -1088,6 +1244,7 @@ const char *eig_last_spmm_kernel(const arr_ctx *c) { return c && c->last_kernel 
 
 arr_status eig_set_degree(arr_ctx *c, int32_t d) {
     GUARD(c);
+    if (c->cs) { ST_TRY(eig_set_degree(c->cs->col, d)); ST_TRY(eig_set_degree(c->cs->row, d)); c->d = d; return ARR_OK; }
     if (d < 1) return fail(c, ARR_EINVAL, "degree must be >= 1");
     c->d = d;
     if (c->filter_kind == 1) c->coef = interp_coef(d);
@@ -1096,6 +1253,7 @@ arr_status eig_set_degree(arr_ctx *c, int32_t d) {
 
 arr_status eig_set_mode(arr_ctx *c, int32_t smallest) {
     GUARD(c);
+    if (c->cs) { ST_TRY(eig_set_mode(c->cs->col, smallest)); ST_TRY(eig_set_mode(c->cs->row, smallest)); }
     c->sign = smallest ? -1 : 1;
     c->have_interval = false;  // an interval of A is not one of -A
     return ARR_OK;
@@ -1103,6 +1261,7 @@ arr_status eig_set_mode(arr_ctx *c, int32_t smallest) {
 
 arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
     GUARD(c);
+    if (c->cs) return eig_set_filter(c->cs->col, kind);
     if (kind != 0 && kind != 1) return fail(c, ARR_EINVAL, "filter kind must be 0 (T_d) or 1 (psi_d)");
     if (kind == 1 && !c->T && c->p < 1)
         return fail(c, ARR_EINVAL, "the interpolant filter needs two scratch blocks (p >= 1 in a lean context)");
@@ -1114,6 +1273,7 @@ arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
 arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev) {
     GUARD(c);
     Nvtx nvtx_("arrabit::filter_step");
+    if (c->cs) return filter_step(c->cs->col, X, ldx, normalize, colnorm_dev);  // this rank's columns: no exchange
     if (!c->have_interval) return fail(c, ARR_EINVAL, "eig_set_interval not called");
     if (!block_ok(X, ldx, c->w)) return fail(c, ARR_EINVAL, "bad block X / ldx");
     CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
@@ -1130,6 +1290,7 @@ arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, do
 
 arr_status eig_set_timing(arr_ctx *c, int32_t on) {
     GUARD(c);
+    if (c->cs) { ST_TRY(eig_set_timing(c->cs->col, on)); ST_TRY(eig_set_timing(c->cs->row, on)); }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->pending.clear();
     c->ev_next = 0;
@@ -1141,6 +1302,14 @@ arr_status eig_set_timing(arr_ctx *c, int32_t on) {
 arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts) {
     GUARD(c);
     if (!ms || !counts) return fail(c, ARR_EINVAL, "null output");
+    if (c->cs) {  // filter degrees from the column context, the ARR / residual phases from the row context
+        double m2[kPhases];
+        int64_t c2[kPhases];
+        ST_TRY(eig_phase_times(c->cs->col, ms, counts));
+        ST_TRY(eig_phase_times(c->cs->row, m2, c2));
+        for (int i = 1; i < kPhases; ++i) { ms[i] = m2[i]; counts[i] = c2[i]; }
+        return ARR_OK;
+    }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     t_resolve(c);
     for (int i = 0; i < kPhases; ++i) { ms[i] = c->phase_ms[i]; counts[i] = c->phase_cnt[i]; }
@@ -1150,6 +1319,7 @@ arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts) {
 arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t ldx, double *Y, int64_t ldy,
                 int32_t ncols) {
     GUARD(c);
+    if (c->cs) return spmm(c->cs->col, alpha, shift, X, ldx, Y, ldy, ncols);  // whole A, this rank's columns
     if (!block_ok(X, ldx, ncols) || !block_ok(Y, ldy, ncols) || ncols > ARR_MAX_W)
         return fail(c, ARR_EINVAL, "bad block / ncols");
     SpmmArgs s{};
@@ -1169,6 +1339,7 @@ arr_status spmm(arr_ctx *c, double alpha, double shift, const double *X, int64_t
 arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy, int32_t m2,
                 double *G, int64_t ldg) {
     GUARD(c);
+    if (c->cs) return fail(c, ARR_EINVAL, "gram: not available on a column-split context");
     if (!block_ok(X, ldx, m1) || !block_ok(Y, ldy, m2) || !G || ldg < m2) return fail(c, ARR_EINVAL, "bad gram args");
     if ((size_t)m1 * (size_t)m2 > c->part_elems)
         return fail(c, ARR_EINVAL, "gram: m1 * m2 exceeds the context's partial-sum buffer (m1 * m2 <= " +
@@ -1181,6 +1352,7 @@ arr_status gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const doub
 arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B, int64_t ldb,
                 int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo) {
     GUARD(c);
+    if (c->cs) return fail(c, ARR_EINVAL, "gemm: not available on a column-split context");
     if (!block_ok(X, ldx, m1) || !B || ldb < m2 || !block_ok(Out, ldo, m2) || (beta != 0.0 && !block_ok(Cin, ldc, m2)))
         return fail(c, ARR_EINVAL, "bad gemm args");
     if ((const void *)X == (const void *)Out) return fail(c, ARR_EINVAL, "gemm: X aliases Out");
@@ -1192,6 +1364,7 @@ arr_status gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t 
 arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int32_t *rank) {
     GUARD(c);
     Nvtx nvtx_("arrabit::orthonormalize");
+    if (c->cs) return fail(c, ARR_EINVAL, "orthonormalize: not available on a column-split context");
     if (!block_ok(X, ldx, ncols) || ncols > c->w) return fail(c, ARR_EINVAL, "bad block / ncols > w");
     // keep the input in the basis buffer: CholeskyQR3 X_copy -> X, SVQB fallback from the copy
     launch_copy_rows(c, X, ldx, c->Q, ldQ(c), c->A.n, ncols);
@@ -1214,6 +1387,16 @@ arr_status arr_project_p(arr_ctx *c, int32_t p_use, const double *X, int64_t ldx
                          double *ritz_host, int32_t *rank) {
     GUARD(c);
     Nvtx nvtx_("arrabit::arr_project");
+    if (c->cs) {  // column layout -> rows, the row context's ARR, Ritz vectors back to this rank's columns
+        ColSplit &S = *c->cs;
+        if (!block_ok(X, ldx, S.col->w) || (Y && !block_ok(Y, ldy, S.col->w)) || !ritz_host)
+            return fail(c, ARR_EINVAL, "bad arr_project args (column slices)");
+        ST_TRY(comm_transpose(c, S, 0, X, ldx, S.Xrow, S.ldrow));
+        ST_TRY(arr_project_p(S.row, p_use, S.Xrow, S.ldrow, Y ? S.Xrow : nullptr, S.ldrow, ritz_host, rank));
+        if (Y) ST_TRY(comm_transpose(c, S, 1, S.Xrow, S.ldrow, Y, ldy));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return ARR_OK;
+    }
     if (p_use < 0 || p_use > c->p) return fail(c, ARR_EINVAL, "p_use out of range");
     if (!block_ok(X, ldx, c->w) || (Y && !block_ok(Y, ldy, c->w)) || !ritz_host)
         return fail(c, ARR_EINVAL, "bad arr_project args");
@@ -1235,6 +1418,12 @@ arr_status residuals(arr_ctx *c, const double *Y, int64_t ldy, const double *mu_
                      double *res_host) {
     GUARD(c);
     Nvtx nvtx_("arrabit::residuals");
+    if (c->cs) {  // the block's columns gathered as rows, then the row context's residual pass
+        ColSplit &S = *c->cs;
+        if (ncols > c->w || !block_ok(Y, ldy, S.col->w)) return fail(c, ARR_EINVAL, "column split: ncols > w or bad Y");
+        ST_TRY(comm_transpose(c, S, 0, Y, ldy, S.Xrow, S.ldrow));
+        return residuals(S.row, S.Xrow, S.ldrow, mu_host, ncols, res_host);
+    }
     if (!block_ok(Y, ldy, ncols) || ncols > std::max(m_of(c, c->p), ARR_MAX_W) || !mu_host || !res_host)
         return fail(c, ARR_EINVAL, "bad residual args");
     if (c->sign > 0) return residuals_core(c, Y, ldy, mu_host, ncols, res_host);
@@ -1247,6 +1436,10 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                      double *res_host, arr_solve_info *info) {
     GUARD(c);
     Nvtx nvtx_("arrabit::eig_solve");
+    if (c->cs) {
+        if (!block_ok(X, ldx, c->cs->col->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
+        return cs_solve(c, X, ldx, opts, eigval_host, res_host, info);
+    }
     if (!block_ok(X, ldx, c->w) || !opts || !eigval_host || !res_host) return fail(c, ARR_EINVAL, "bad solve args");
     if (opts->gn && (c->p < 1 || (c->filter_kind == 1 && (c->T ? c->p < 1 : c->p < 2))))
         return fail(c, ARR_EINVAL, "GN inner solver: needs a spare basis block (p >= 1; p >= 2 with psi_d in a lean context)");

@@ -29,6 +29,7 @@
 struct LocalSlot {
     const double *ptr = nullptr;        // published buffer (allreduce / bcast source)
     std::vector<const double *> src;    // halo: source of the rows destined to peer index q
+    std::vector<int64_t> offs;          // column split: offsets of the pieces for each rank
     cudaEvent_t ready = nullptr, done = nullptr;
     const arr_ctx *ctx = nullptr;       // the context currently attached (peers, offsets)
 };
@@ -291,6 +292,98 @@ arr_status comm_halo_end(arr_ctx *c, double *Y) {
         CT(cudaGetLastError());
     }
     if (m->kind == 1) BARRIER(m->group);  // all waits on our events are queued before they are re-recorded
+    return ARR_OK;
+}
+
+// ---------------------------------------------------------------- column <-> row transposes
+// Column-partitioned mode (Survey §8f-3): rank r holds columns [cb[r], cb[r+1]) of every
+// n x w block (all rows; "column layout") and, for the ARR projection, rows
+// [rb[r], rb[r+1]) of all w columns ("row layout", the row context's owned rows).
+// col2row moves the column layout to the row layout, row2col back: one all-to-all each,
+// through packed buffers whose row stride is the (even) sender width.
+namespace {
+inline int64_t ev(int64_t x) { return (x + 1) & ~int64_t(1); }
+}  // namespace
+
+arr_status comm_transpose(arr_ctx *c, const ColSplit &S, int dir, const double *src, int64_t lds, double *dst,
+                          int64_t ldd) {
+    arr_comm *m = c->comm;
+    const int R = m->rank, G = m->size;
+    const int64_t wr = S.cb[R + 1] - S.cb[R], nr = S.rb[R + 1] - S.rb[R];
+    // send piece for peer q and where it lands on q (row layout: rows of q x my columns;
+    // column layout: my rows x q's columns), packed with row stride ev(width)
+    std::vector<int64_t> soff(G + 1, 0), roff(G + 1, 0);
+    for (int q = 0; q < G; ++q) {
+        const int64_t nq = S.rb[q + 1] - S.rb[q], wq = S.cb[q + 1] - S.cb[q];
+        soff[q + 1] = soff[q] + (dir == 0 ? nq * ev(wr) : nr * ev(wq));
+        roff[q + 1] = roff[q] + (dir == 0 ? nr * ev(wq) : nq * ev(wr));
+    }
+    if (soff[G] > (int64_t)S.buf_elems || roff[G] > (int64_t)S.buf_elems)
+        return cfail(c, ARR_EINVAL, "column split: transpose buffer too small");
+    // pack
+    for (int q = 0; q < G; ++q) {
+        const int64_t nq = S.rb[q + 1] - S.rb[q], wq = S.cb[q + 1] - S.cb[q];
+        if (dir == 0) {  // my columns, rows of q
+            if (nq && wr)
+                copy2d_kernel<<<grid_for(c, nq * wr), 256, 0, c->stream>>>(src + S.rb[q] * lds, lds, S.sendbuf + soff[q],
+                                                                           ev(wr), nq, (int)wr);
+        } else {  // my rows, columns of q
+            if (nr && wq)
+                copy2d_kernel<<<grid_for(c, nr * wq), 256, 0, c->stream>>>(src + S.cb[q], lds, S.sendbuf + soff[q],
+                                                                           ev(wq), nr, (int)wq);
+        }
+        c->launches++;
+    }
+    CT(cudaGetLastError());
+    if (m->kind == 0) {
+        if (roff[R + 1] > roff[R])  // own piece: a device copy
+            CT(cudaMemcpyAsync(S.recvbuf + roff[R], S.sendbuf + soff[R], sizeof(double) * (roff[R + 1] - roff[R]),
+                               cudaMemcpyDeviceToDevice, c->stream));
+        NT(ncclGroupStart());
+        for (int q = 0; q < G; ++q) {
+            if (q == R) continue;
+            if (soff[q + 1] > soff[q]) NT(ncclSend(S.sendbuf + soff[q], soff[q + 1] - soff[q], ncclFloat64, q, m->nccl, c->stream));
+            if (roff[q + 1] > roff[q]) NT(ncclRecv(S.recvbuf + roff[q], roff[q + 1] - roff[q], ncclFloat64, q, m->nccl, c->stream));
+        }
+        NT(ncclGroupEnd());
+    } else {
+        LocalGroup *g = m->group;
+        LocalSlot &me = g->slot[R];
+        me.src.assign(1, S.sendbuf);
+        me.offs = soff;
+        CT(cudaEventRecord(me.ready, c->stream));
+        BARRIER(g);
+        for (int q = 0; q < G; ++q) {
+            const LocalSlot &ps = g->slot[q];
+            const int64_t cnt = roff[q + 1] - roff[q];
+            if (!cnt) continue;
+            if ((int64_t)ps.offs.size() != G + 1 || ps.offs[R + 1] - ps.offs[R] != cnt)
+                return cfail(c, ARR_EINVAL, "column split: the ranks' transpose plans disagree");
+            if (q != R) CT(cudaStreamWaitEvent(c->stream, ps.ready, 0));
+            CT(cudaMemcpyAsync(S.recvbuf + roff[q], ps.src[0] + ps.offs[R], sizeof(double) * cnt,
+                               cudaMemcpyDeviceToDevice, c->stream));
+        }
+        CT(cudaEventRecord(me.done, c->stream));
+        BARRIER(g);
+        for (int q = 0; q < G; ++q)
+            if (q != R) CT(cudaStreamWaitEvent(c->stream, g->slot[q].done, 0));  // peers finished reading our sendbuf
+        BARRIER(g);
+    }
+    // unpack
+    for (int q = 0; q < G; ++q) {
+        const int64_t nq = S.rb[q + 1] - S.rb[q], wq = S.cb[q + 1] - S.cb[q];
+        if (dir == 0) {  // rows of mine x columns of q -> row layout
+            if (nr && wq)
+                copy2d_kernel<<<grid_for(c, nr * wq), 256, 0, c->stream>>>(S.recvbuf + roff[q], ev(wq), dst + S.cb[q], ldd,
+                                                                           nr, (int)wq);
+        } else {  // rows of q x my columns -> column layout
+            if (nq && wr)
+                copy2d_kernel<<<grid_for(c, nq * wr), 256, 0, c->stream>>>(S.recvbuf + roff[q], ev(wr), dst + S.rb[q] * ldd,
+                                                                           ldd, nq, (int)wr);
+        }
+        c->launches++;
+    }
+    CT(cudaGetLastError());
     return ARR_OK;
 }
 

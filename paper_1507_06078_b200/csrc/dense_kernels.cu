@@ -391,54 +391,65 @@ __global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gemm_kernel_ca(double 
 bool ca_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
 
 // ---------------------------------------------------------------- large tiles
-// 128 x 128 CTA tiles, 16 warps of 32 x 32 (4 x 4 DMMA m8n8k4 tiles each), KS = 16 rows
-// (Gram) / k-columns (GEMM) per stage, an S_BIG-stage cp.async ring (S_BIG - 1 stages in
-// flight): every staged 16 x 128 panel feeds 4x the DMMAs of the 64 x 64 kernels' (half
-// the L2 -> SM bytes per flop).  Warp sub-tiles that lie outside the output (or,
-// symmetric, strictly below the diagonal) skip their DMMAs, so a width w pays for
-// ceil(w / 32) warp columns, not ceil(w / 128) CTA columns.  Same fragments and
-// per-element k order as the 64 x 64 kernels (only the split and the tile sizes differ).
-constexpr int BT = 128, BWM = 32, BWN = 32, BTHREADS = 512;
+// BM x BN CTA tiles of 32 x 32 warp tiles (4 x 4 DMMA m8n8k4 tiles each; WM x WN warps),
+// KS = 16 rows (Gram) / k-columns (GEMM) per stage, an S_BIG-stage cp.async ring
+// (S_BIG - 1 stages in flight).  Warp sub-tiles outside the output (or, symmetric,
+// strictly below the diagonal) skip their DMMAs.  Same fragments and per-element k order
+// as the 64 x 64 kernels.  Selected with ARRABIT_DMMA_TILE = 1 (128 x 64, 8 warps, 2 CTAs
+// per SM) or 2 (128 x 128, 16 warps); measured on B200 (profiles/r02_dmma_tiles.log) the
+// 64 x 64 kernels above stay the default.
 #ifndef ARR_DMMA_BIG_STAGES
 #define ARR_DMMA_BIG_STAGES 3
 #endif
 constexpr int S_BIG = ARR_DMMA_BIG_STAGES;
 constexpr int BPAD = 4;
 
-__global__ void __launch_bounds__(BTHREADS, 1) gram_kernel_big(const double *__restrict__ X, int64_t ldx, int m1,
-                                                              const double *__restrict__ Y, int64_t ldy, int m2,
-                                                              int64_t n, int64_t rows_per_split, bool sym,
-                                                              double *__restrict__ part) {
+template <int BM, int BN>
+struct BigCfg {
+    static constexpr int WM = BM / 32, WN = BN / 32, THREADS = WM * WN * 32;
+    static constexpr int MINB = THREADS >= 512 ? 1 : 2;
+    static constexpr size_t gram_smem = sizeof(double) * S_BIG * KS * ((BM + BPAD) + (BN + BPAD));
+    static constexpr size_t gemm_smem = sizeof(double) * S_BIG * (BM * (KS + BPAD) + KS * (BN + BPAD));
+};
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
+    gram_kernel_big(const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ Y, int64_t ldy,
+                    int m2, int64_t n, int64_t rows_per_split, bool sym, double *__restrict__ part) {
+    using C = BigCfg<BM, BN>;
     const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
-    if (sym && tb < ta) return;
-    const int a0 = ta * BT, b0 = tb * BT;
+    const int a0 = ta * BM, b0 = tb * BN;
+    if (sym && b0 + BN <= a0) return;  // strictly below the diagonal
     const int64_t k0 = (int64_t)split * rows_per_split;
     int64_t k1 = k0 + rows_per_split;
     if (k1 > n) k1 = n;
     extern __shared__ __align__(16) double dsm[];
-    double (*Xs)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm);
-    double (*Ys)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm + S_BIG * KS * (BT + BPAD));
+    double (*Xs)[KS][BM + BPAD] = reinterpret_cast<double (*)[KS][BM + BPAD]>(dsm);
+    double (*Ys)[KS][BN + BPAD] = reinterpret_cast<double (*)[KS][BN + BPAD]>(dsm + S_BIG * KS * (BM + BPAD));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;  // 4 x 4 warps
-    const int ra0 = a0 + wm * BWM, cb0 = b0 + wn * BWN;
-    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + BWN);
+    const int wm = warp / C::WN, wn = warp % C::WN;
+    const int ra0 = a0 + wm * 32, cb0 = b0 + wn * 32;
+    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + 32);
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // one stage = KS rows x 128 columns of X and of Y = 2 x 1024 chunks of 16 bytes, 2 + 2 per thread
+    constexpr int CX = KS * BM / 2, CY = KS * BN / 2;  // 16-byte chunks per stage
     auto load = [&](int64_t kb, int st) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int idx = tid + q * BTHREADS;
-            const int rr = idx >> 6, cc = (idx & 63) * 2;
-            const int64_t row = kb + rr;
-            const bool rok = row < k1;
-            const int nx = rok ? max(0, min(2, m1 - (a0 + cc))) : 0;
-            const int ny = rok ? max(0, min(2, m2 - (b0 + cc))) : 0;
-            ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
-            ca16(&Ys[st][rr][cc], ny ? Y + row * ldy + b0 + cc : Y, ny * 8);
+        for (int idx = tid; idx < CX + CY; idx += C::THREADS) {
+            if (idx < CX) {
+                const int rr = idx / (BM / 2), cc = (idx % (BM / 2)) * 2;
+                const int64_t row = kb + rr;
+                const int nx = row < k1 ? max(0, min(2, m1 - (a0 + cc))) : 0;
+                ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
+            } else {
+                const int j = idx - CX;
+                const int rr = j / (BN / 2), cc = (j % (BN / 2)) * 2;
+                const int64_t row = kb + rr;
+                const int ny = row < k1 ? max(0, min(2, m2 - (b0 + cc))) : 0;
+                ca16(&Ys[st][rr][cc], ny ? Y + row * ldy + b0 + cc : Y, ny * 8);
+            }
         }
     };
     const int64_t nk = (k1 - k0 + KS - 1) / KS;
@@ -459,9 +470,9 @@ __global__ void __launch_bounds__(BTHREADS, 1) gram_kernel_big(const double *__r
             for (int kk = 0; kk < KS / 4; ++kk) {
                 double af[4], bf[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * BWM + mt * 8 + (lane >> 2)];
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * 32 + mt * 8 + (lane >> 2)];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * BWN + nt * 8 + (lane >> 2)];
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -484,37 +495,41 @@ __global__ void __launch_bounds__(BTHREADS, 1) gram_kernel_big(const double *__r
             }
 }
 
-__global__ void __launch_bounds__(BTHREADS, 1) gemm_kernel_big(double alpha, const double *__restrict__ X, int64_t ldx,
-                                                              int m1, const double *__restrict__ B, int64_t ldb, int m2,
-                                                              double beta, const double *Cin, int64_t ldc, double *Out,
-                                                              int64_t ldo, int64_t n, int upper) {
-    const int nct = (m2 + BT - 1) / BT;
-    const int64_t r0 = (int64_t)(blockIdx.x / nct) * BT;
-    const int c0 = (int)(blockIdx.x % nct) * BT;
-    if (upper && c0 + BT < m1) m1 = c0 + BT;
+template <int BM, int BN>
+__global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
+    gemm_kernel_big(double alpha, const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ B,
+                    int64_t ldb, int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
+                    int64_t n, int upper) {
+    using C = BigCfg<BM, BN>;
+    const int nct = (m2 + BN - 1) / BN;
+    const int64_t r0 = (int64_t)(blockIdx.x / nct) * BM;
+    const int c0 = (int)(blockIdx.x % nct) * BN;
+    if (upper && c0 + BN < m1) m1 = c0 + BN;
     extern __shared__ __align__(16) double dsm[];
-    double (*Xs)[BT][KS + BPAD] = reinterpret_cast<double (*)[BT][KS + BPAD]>(dsm);
-    double (*Bs)[KS][BT + BPAD] = reinterpret_cast<double (*)[KS][BT + BPAD]>(dsm + S_BIG * BT * (KS + BPAD));
+    double (*Xs)[BM][KS + BPAD] = reinterpret_cast<double (*)[BM][KS + BPAD]>(dsm);
+    double (*Bs)[KS][BN + BPAD] = reinterpret_cast<double (*)[KS][BN + BPAD]>(dsm + S_BIG * BM * (KS + BPAD));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;  // 4 x 4 warps
-    const bool work = (r0 + wm * BWM < n) && (c0 + wn * BWN < m2);
+    const int wm = warp / C::WN, wn = warp % C::WN;
+    const bool work = (r0 + wm * 32 < n) && (c0 + wn * 32 < m2);
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    // one stage = 128 rows x 16 k of X (8 chunks per row) and 16 k x 128 columns of B (64 chunks per row)
+    constexpr int CX = BM * KS / 2, CB = KS * BN / 2;
     auto load = [&](int kb, int st) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int idx = tid + q * BTHREADS;
-            const int xr = idx >> 3, xk = (idx & 7) * 2;
-            const int64_t row = r0 + xr;
-            const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
-            ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
-            const int bk = idx >> 6, bc = (idx & 63) * 2;
-            const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
-            ca16(&Bs[st][bk][bc], nb ? B + (int64_t)(kb + bk) * ldb + c0 + bc : B, nb * 8);
+        for (int idx = tid; idx < CX + CB; idx += C::THREADS) {
+            if (idx < CX) {
+                const int xr = idx / (KS / 2), xk = (idx % (KS / 2)) * 2;
+                const int64_t row = r0 + xr;
+                const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
+                ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
+            } else {
+                const int j = idx - CX;
+                const int bk = j / (BN / 2), bc = (j % (BN / 2)) * 2;
+                const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
+                ca16(&Bs[st][bk][bc], nb ? B + (int64_t)(kb + bk) * ldb + c0 + bc : B, nb * 8);
+            }
         }
     };
     const int nk = (m1 + KS - 1) / KS;
@@ -535,9 +550,9 @@ __global__ void __launch_bounds__(BTHREADS, 1) gemm_kernel_big(double alpha, con
             for (int kk = 0; kk < KS / 4; ++kk) {
                 double af[4], bf[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * BWM + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * 32 + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * BWN + nt * 8 + (lane >> 2)];
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -553,8 +568,8 @@ __global__ void __launch_bounds__(BTHREADS, 1) gemm_kernel_big(double alpha, con
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int64_t row = r0 + wm * BWM + mt * 8 + (lane >> 2);
-                const int cb = c0 + wn * BWN + nt * 8 + (lane & 3) * 2 + e;
+                const int64_t row = r0 + wm * 32 + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
                 if (row < n && cb < m2) {
                     double v = alpha * acc[mt][nt][e];
                     if (beta != 0.0) v += beta * Cin[row * ldc + cb];
@@ -563,13 +578,39 @@ __global__ void __launch_bounds__(BTHREADS, 1) gemm_kernel_big(double alpha, con
             }
 }
 
-// the large tiles pay off once both output dimensions span more than one 64-wide tile
-#ifndef ARR_DMMA_BIG_MIN
-#define ARR_DMMA_BIG_MIN 160
-#endif
-bool use_big(int d1, int d2) {
-    static const int mn = [] { const char *e = getenv("ARRABIT_DMMA_BIG"); return e ? atoi(e) : ARR_DMMA_BIG_MIN; }();
-    return mn > 0 && d1 >= mn && d2 >= mn;
+int dmma_tile_choice() {
+    static const int t = [] { const char *e = getenv("ARRABIT_DMMA_TILE"); return e ? atoi(e) : 0; }();
+    return t;
+}
+bool use_big(int d1, int d2) { return dmma_tile_choice() > 0 && d1 >= 128 && d2 >= 64; }
+
+template <int BM, int BN>
+void launch_gram_big(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
+                     int64_t n, int64_t rps, int ns, bool sym, double *partials) {
+    using C = BigCfg<BM, BN>;
+    static LaunchCache cache;
+    cached_occupancy(cache, gram_kernel_big<BM, BN>, C::THREADS, C::gram_smem);
+    dim3 gb((m1 + BM - 1) / BM, (m2 + BN - 1) / BN, ns);
+    gram_kernel_big<BM, BN><<<gb, C::THREADS, C::gram_smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+}
+template <int BM, int BN>
+void launch_gemm_big(arr_ctx *c, double alpha, const double *X, int64_t ldx, int m1, const double *B, int64_t ldb,
+                     int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo, int64_t n,
+                     int upper) {
+    using C = BigCfg<BM, BN>;
+    static LaunchCache cache;
+    cached_occupancy(cache, gemm_kernel_big<BM, BN>, C::THREADS, C::gemm_smem);
+    const unsigned gb = (unsigned)(((n + BM - 1) / BM) * ((m2 + BN - 1) / BN));
+    gemm_kernel_big<BM, BN><<<gb, C::THREADS, C::gemm_smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc,
+                                                                        Out, ldo, n, upper);
+}
+int big_per_sm(int num_sms) {
+    (void)num_sms;
+    static LaunchCache c1, c2;
+    return dmma_tile_choice() == 1
+               ? cached_occupancy(c1, gram_kernel_big<128, 64>, BigCfg<128, 64>::THREADS, BigCfg<128, 64>::gram_smem)
+               : cached_occupancy(c2, gram_kernel_big<128, 128>, BigCfg<128, 128>::THREADS,
+                                  BigCfg<128, 128>::gram_smem);
 }
 
 // ---------------------------------------------------------------- small dense
@@ -635,12 +676,12 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 // rows each.  sym: only the upper tiles do work.
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     const bool big = use_big(m1, m2);
-    const int T = big ? BT : TILE;
-    const int64_t ta = (m1 + T - 1) / T, tb = (m2 + T - 1) / T;
-    const int64_t tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
+    const int TM = big ? 128 : TILE, TN = big ? (dmma_tile_choice() == 1 ? 64 : 128) : TILE;
+    const int64_t ta = (m1 + TM - 1) / TM, tb = (m2 + TN - 1) / TN;
+    const int64_t tiles = sym ? (TM == TN ? ta * (ta + 1) / 2 : ta * tb - ta * (ta - 1)) : ta * tb;
 #if ARR_DMMA_CA
-    static LaunchCache cache, cache_big;
-    const int per_sm = big ? cached_occupancy(cache_big, gram_kernel_big, BTHREADS, sizeof(double) * 2 * S_BIG * KS * (BT + BPAD))
+    static LaunchCache cache;
+    const int per_sm = big ? big_per_sm(num_sms)
                            : cached_occupancy(cache, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
 #else
     static const int per_sm = [] {
@@ -680,11 +721,8 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
 #if ARR_DMMA_CA
     if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(Y, ldy)) {
-        const size_t smem = sizeof(double) * 2 * S_BIG * KS * (BT + BPAD);
-        static LaunchCache cache;
-        cached_occupancy(cache, gram_kernel_big, BTHREADS, smem);
-        dim3 gb((m1 + BT - 1) / BT, (m2 + BT - 1) / BT, ns);
-        gram_kernel_big<<<gb, BTHREADS, smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+        if (dmma_tile_choice() == 1) launch_gram_big<128, 64>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials);
+        else launch_gram_big<128, 128>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials);
     } else if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
         const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
         static LaunchCache cache;
@@ -703,12 +741,8 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
     const unsigned grid = (unsigned)(((n + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE));
 #if ARR_DMMA_CA
     if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(B, ldb)) {
-        const size_t smem = sizeof(double) * S_BIG * (BT * (KS + BPAD) + KS * (BT + BPAD));
-        static LaunchCache cache;
-        cached_occupancy(cache, gemm_kernel_big, BTHREADS, smem);
-        const unsigned gb = (unsigned)(((n + BT - 1) / BT) * ((m2 + BT - 1) / BT));
-        gemm_kernel_big<<<gb, BTHREADS, smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n,
-                                                          upper);
+        if (dmma_tile_choice() == 1) launch_gemm_big<128, 64>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
+        else launch_gemm_big<128, 128>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
     } else if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
         const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));
         static LaunchCache cache;

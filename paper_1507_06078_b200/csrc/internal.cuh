@@ -34,6 +34,19 @@ struct DistPlan {
     int64_t cur_ld = 0;
 };
 
+// Column-partitioned mode (eig_init_colsplit, Survey §8f-3): the outer context holds a
+// column context (the full A, this rank's w_loc columns: the filter, no communication)
+// and a row context (eig_init_dist on the rank's row block: the ARR projection and the
+// residuals), joined by all-to-all transposes of the n x w block (comm.cu).
+struct ColSplit {
+    std::vector<int64_t> rb, cb;  // [size+1] global row / column boundaries of every rank
+    double *sendbuf = nullptr, *recvbuf = nullptr;
+    size_t buf_elems = 0;
+    arr_ctx *col = nullptr, *row = nullptr;
+    double *Xrow = nullptr;       // row-layout block (row context rows x even(w))
+    int64_t ldrow = 0;
+};
+
 // Stencil-aware filter path (stencil_kernels.cu; eig_set_stencil): A stored as K
 // diagonals of a 3x3x3 neighbourhood on an nx x ny x nz grid (x fastest).
 struct StencilSlots {
@@ -115,6 +128,7 @@ struct arr_ctx {
     uint64_t g_kernels;
     int64_t g_spmm;
     int g_nblk;
+    const char *g_last_kernel;
     // bookkeeping
     const char *last_kernel;  // name of the kernel the last fused SpMM launched (eig_last_spmm_kernel)
     uint64_t launches;
@@ -134,6 +148,7 @@ struct arr_ctx {
     int nranks;  // size of comm (1 without one)
     DistPlan plan;
     StencilState st;
+    ColSplit *cs;  // column-partitioned outer context (nullptr otherwise)
     double *stage;
     size_t stage_elems;
     // pinned host staging
@@ -220,6 +235,10 @@ arr_status comm_bcast(arr_ctx *c, double *buf, size_t count, int root);
 arr_status comm_halo_begin(arr_ctx *c, const double *Y, int64_t ld, int ncols);
 arr_status comm_halo_end(arr_ctx *c, double *Y);
 arr_status comm_setup_plan(arr_ctx *c, const arr_dist *d, arr_comm *m);
+// dir 0: column layout (n x w_loc, ld lds) -> row layout (rows of this rank x w, ld ldd);
+// dir 1: back.  Collective over the column split's communicator.
+arr_status comm_transpose(arr_ctx *c, const ColSplit &S, int dir, const double *src, int64_t lds, double *dst,
+                          int64_t ldd);
 void comm_free_plan(arr_ctx *c);
 
 // ---------------------------------------------------------------- dense (DMMA)

@@ -511,7 +511,8 @@ int launch_st(arr_ctx *c, StencilLaunch &L) {
     const int occ = cached_occupancy(cache, kern, kStThreads, smem);
     int64_t G = (int64_t)c->num_sms * occ;
     static const int pm_env = [] { const char *e = getenv("ARRABIT_ST_ORDER"); return e ? atoi(e) : 1; }();
-    static const int pf_env = [] { const char *e = getenv("ARRABIT_ST_PF"); return e ? atoi(e) : 3; }();
+    // L2 prefetch ahead of the loads measured slower on B200 (cfg3 3.32 -> 4.27 ms per degree): off
+    static const int pf_env = [] { const char *e = getenv("ARRABIT_ST_PF"); return e ? atoi(e) : 0; }();
     L.pf = pf_env;
     static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
     if (verbose)

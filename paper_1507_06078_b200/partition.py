@@ -165,3 +165,70 @@ def scatter_rows(X: np.ndarray, p: LocalPlan, ld: int | None = None) -> np.ndarr
     out = np.zeros((p.n_rows_block, ld))
     out[:p.n_own, :w] = X[p.row_begin:p.row_begin + p.n_own]
     return out
+
+
+# ---------------------------------------------------------------- column partition (Survey §8f-3)
+def col_bounds(w: int, size: int) -> np.ndarray:
+    """Columns [cb[r], cb[r+1]) of every n x w block on rank r: even widths (16-byte
+    rows for the filter's 128-bit accesses), the remainder on the last ranks."""
+    if w < 2 * size:
+        raise ValueError(f"w = {w} too narrow for {size} column slices")
+    per = np.full(size, (w // size) & ~1, dtype=np.int64)
+    rest = w - int(per.sum())
+    r = size - 1
+    while rest > 0:  # hand out the remainder two columns at a time (one if w is odd)
+        step = 2 if rest >= 2 else 1
+        per[r] += step
+        rest -= step
+        r = r - 1 if r > 0 else size - 1
+    return np.concatenate([[0], np.cumsum(per)]).astype(np.int64)
+
+
+@dataclass
+class ColSplitPlan:
+    """What eig_init_colsplit needs on one rank: the row block of the internal ARR
+    context (its LocalPlan, rows balanced by traffic as bounds_balanced) and the row /
+    column boundaries of every rank."""
+    rows: LocalPlan
+    row_begins: np.ndarray  # int64 [size+1]
+    col_begins: np.ndarray  # int64 [size+1]
+    rank: int
+    size: int
+
+    @property
+    def col_range(self):
+        return int(self.col_begins[self.rank]), int(self.col_begins[self.rank + 1])
+
+
+def colsplit_plan(A, w: int, size: int, rank: int, row_bounds: np.ndarray | None = None) -> ColSplitPlan:
+    rb = bounds_balanced(A.row_ptr, size) if row_bounds is None else np.asarray(row_bounds, dtype=np.int64)
+    return ColSplitPlan(local_plan(A, rb, rank), rb.astype(np.int64), col_bounds(w, size), rank, size)
+
+
+def transpose_col2row(cols: list[np.ndarray], row_begins: np.ndarray, col_begins: np.ndarray) -> list[np.ndarray]:
+    """Host reference of the all-to-all (comm.cu comm_transpose, direction 0): rank r's
+    column slice (n x w_r) -> every rank's row slice (n_q x w).  Data movement only."""
+    size = len(cols)
+    w = int(col_begins[-1])
+    out = []
+    for q in range(size):
+        a, b = int(row_begins[q]), int(row_begins[q + 1])
+        blk = np.empty((b - a, w))
+        for r in range(size):
+            blk[:, col_begins[r]:col_begins[r + 1]] = cols[r][a:b]
+        out.append(blk)
+    return out
+
+
+def transpose_row2col(rows: list[np.ndarray], row_begins: np.ndarray, col_begins: np.ndarray) -> list[np.ndarray]:
+    """Inverse of transpose_col2row."""
+    size = len(rows)
+    n = int(row_begins[-1])
+    out = []
+    for r in range(size):
+        c0, c1 = int(col_begins[r]), int(col_begins[r + 1])
+        blk = np.empty((n, c1 - c0))
+        for q in range(size):
+            blk[row_begins[q]:row_begins[q + 1]] = rows[q][:, c0:c1]
+        out.append(blk)
+    return out
