@@ -52,6 +52,9 @@ def parse():
                     help="filter kernels: auto = the stencil path for 3-D grids, CSR otherwise")
     ap.add_argument("--no-secondary", action="store_true", help="skip the secondary cfg2 solve")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of a partition")
+    ap.add_argument("--partition", default="rows", choices=["rows", "column"],
+                    help="N>1: rows = row partition (halo / all-gather before every SpMM); column = the column split "
+                         "(eig_init_colsplit: A replicated, column-local filter, ARR on a row partition)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--filter", default="cheb", choices=["cheb", "interp"],
@@ -305,8 +308,13 @@ def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps,
               world=1, dist=None):
     """Create a context, run warm-up + timed solves; return measurements."""
     partitioned = plan is not None
-    ctx = arr.eig_init(Ad_of(arr, Aloc, dev, stream), spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm,
-                       plan=plan)
+    if isinstance(plan, arr.partition.ColSplitPlan):
+        ctx = arr.eig_init_colsplit(Ad_of(arr, A, dev, stream), Ad_of(arr, plan.rows, dev, stream), plan, spec.k,
+                                    spec.p, spec.d, spec.w, comm, stream=stream)
+        partitioned = False  # the column context has the whole A: the stencil path applies
+    else:
+        ctx = arr.eig_init(Ad_of(arr, Aloc, dev, stream), spec.k, spec.p, spec.d, stream=stream, w=spec.w, comm=comm,
+                           plan=plan)
     nrows = X.shape[0]
     ctx_lean = ctx.workspace_bytes < 8 * nrows * spec.w * (spec.p + 2)
     if args.filter != "cheb":
@@ -378,12 +386,13 @@ def Ad_of(arr, Aloc, dev, stream):
     return _AD[key]
 
 
-def roofline_of(r, spec, nrow, nnz, args, steps, cid=None):
+def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
     peak, peak_src = load_peaks()
+    w = spec.w if w is None else w  # the filtered width on this rank (the column split filters w_r columns)
     deg_ms = r["phase_ms"][0] / max(1, r["phase_cnt"][0])
-    bpl = filter_bytes_per_degree(nrow, nnz, spec.w, spec.d, r["stencil_K"])
+    bpl = filter_bytes_per_degree(nrow, nnz, w, spec.d, r["stencil_K"])
     if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
-        bpl += 8 * nrow * spec.w
+        bpl += 8 * nrow * w
     achieved = bpl / (deg_ms / 1000.0) / 1e9
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config if cid is None else cid}.json")
@@ -425,7 +434,14 @@ def run_ours(args):
     A, spec = configs.build_config(args.config)
     partitioned = world > 1 and not args.replicas
     plan = comm = None
-    if partitioned:
+    colsplit = partitioned and args.partition == "column"
+    c0, c1 = 0, spec.w
+    if colsplit:
+        plan = pt.colsplit_plan(A, spec.w, world, rank)
+        Aloc = A
+        c0, c1 = plan.col_range
+        r0, r1, nrows = 0, A.n, A.n
+    elif partitioned:
         ps = _partition_spec(spec)
         bounds = pt.bounds_planes(ps[1], ps[2], world) if ps[0] == "planes" else pt.bounds_balanced(A.row_ptr, world)
         plan = pt.local_plan(A, bounds, rank)
@@ -441,14 +457,14 @@ def run_ours(args):
         X[:r1 - r0, :spec.k] = synth.gaussian_block_rows(A.n, spec.k, spec.seed, r0, r1)
         if spec.q:
             X[:r1 - r0, spec.k:] = synth.gaussian_block_rows(A.n, spec.q, spec.seed, r0, r1, stream=2)
-        return X
+        return np.ascontiguousarray(X[:, c0:c1]) if colsplit else X
 
     X0h = host_X0()
     stream = torch.cuda.Stream(device=dev)
     # X0 stays on the device unless the solve's blocks would not fit next to it (cfg5 on
     # one GPU: X + the (p+1)-block basis is ~151 GB); then it is re-uploaded from pinned
     # host memory before each step, outside the timed region
-    blk = 8 * nrows * spec.w
+    blk = 8 * nrows * (c1 - c0)
     x0_on_host = blk * (spec.p + 4) > 0.9 * torch.cuda.get_device_properties(dev).total_memory
     with torch.cuda.stream(stream):
         if x0_on_host:
@@ -472,12 +488,14 @@ def run_ours(args):
     # eigenpairs/s: each replica (or the one partitioned job) finds k pairs per step
     jobs = 1 if partitioned else world
     value = spec.k * args.steps * jobs / (total_ms / 1000.0)
-    nnz_loc = int(Aloc.nnz) if not partitioned else plan.nnz
-    roofline = roofline_of(r, spec, r1 - r0, nnz_loc, args, args.steps)
+    nnz_loc = int(Aloc.nnz) if (not partitioned or colsplit) else plan.nnz
+    roofline = roofline_of(r, spec, r1 - r0, nnz_loc, args, args.steps, w=c1 - c0)
 
     # the DMMA Gram kernel of A4 (X^T Y, n x w by n x w, 2 n w^2 flops) timed alone on this block
     dense = None
     try:
+        if colsplit:
+            raise RuntimeError("gram is not exported on a column-split context")
         G = torch.empty((spec.w, spec.w), dtype=torch.float64, device=dev)
         nrow = r1 - r0
         with torch.cuda.stream(stream):
@@ -544,7 +562,9 @@ def run_ours(args):
     # eigenpairs inside the timed region (one GPU: the eig_solve_host C-ABI call;
     # partitioned: each rank uploads its local CSR + X0 rows, eig_init_dist, eig_solve)
     e2e = None
-    if not args.no_e2e and (args.filter != "cheb" or args.adapt or args.inner_solver != "mpm"):
+    if not args.no_e2e and colsplit:
+        e2e = {"value": None, "unit": UNIT, "error": "no host-buffer entry for the column split"}
+    elif not args.no_e2e and (args.filter != "cheb" or args.adapt or args.inner_solver != "mpm"):
         e2e = {"value": None, "unit": UNIT, "error": "the host-buffer entry eig_solve_host runs the fixed-parameter T_d solve only"}
     elif not args.no_e2e:
         try:
@@ -603,7 +623,9 @@ def run_ours(args):
     if rank == 0:
         info = r["infos"][-1]
         par = ("1 GPU" if world == 1 else
-               (f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
+               (f"column split over {world} GPUs (A replicated, column-local filter, ARR on a balanced row "
+                f"partition; NCCL all-to-all transposes + halo/all-gather + allreduce)" if colsplit else
+                f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
                 if partitioned else f"{world} independent replicas (no collective)"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

@@ -136,7 +136,13 @@ typedef struct {
                         whose X^T X is not positive definite returns ARR_ENUMERIC   */
     int64_t grid[3]; /* eig_solve_host only: {nx, ny, nz} != 0 declares A a stencil operator
                         (eig_set_stencil on the internal context); {0,0,0}: CSR kernels  */
+    double *log;     /* optional host [log_cap x ARR_LOG_FIELDS]: one row per outer iteration
+                        {outer, sweeps s, a, b, mu_1 that set s, max res, p, d, locked, tol_t,
+                        mu_k, mu_w} - the driver's decisions and the Ritz values they are
+                        taken from, for checking them against the rules                  */
+    int32_t log_cap; /* rows available in log (0: no log)                                */
 } arr_solve_opts;
+#define ARR_LOG_FIELDS 12
 
 typedef struct {
     int32_t converged;   /* 1 if max res <= tol                                   */

@@ -39,7 +39,8 @@ class arr_dist(ctypes.Structure):
 class arr_solve_opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("s_max", ctypes.c_int32),
                 ("exits", ctypes.c_int32), ("inner", ctypes.c_int32), ("adapt", ctypes.c_int32),
-                ("gn", ctypes.c_int32), ("grid", ctypes.c_int64 * 3)]
+                ("gn", ctypes.c_int32), ("grid", ctypes.c_int64 * 3), ("log", ctypes.c_void_p),
+                ("log_cap", ctypes.c_int32)]
 
 
 class arr_solve_info(ctypes.Structure):

@@ -17,6 +17,10 @@ from . import _lib
 from ._lib import arr_csr, arr_dist, arr_solve_info, arr_solve_opts
 
 
+LOG_FIELDS = 12  # ARR_LOG_FIELDS (include/arrabit.h)
+LOG_KEYS = ("outer", "s", "a", "b", "mu1", "maxres", "p", "d", "locked", "tol_t", "mu_k", "mu_w")
+
+
 class ArrError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{_lib.STATUS_NAMES.get(status, status)}: {msg}")
@@ -318,6 +322,9 @@ class EigContext:
         px, ld, _ = _blk(X, "X")
         opts = arr_solve_opts(tol, maxit, s_max, exits, 1 if inner == "rcond" else 0, adapt,
                               1 if inner_solver == "gn" else 0)
+        log = np.zeros((maxit, LOG_FIELDS))
+        opts.log = ctypes.c_void_p(log.ctypes.data)
+        opts.log_cap = maxit
         ev = np.empty(self.k)
         res = np.empty(self.k)
         info = arr_solve_info()
@@ -325,6 +332,8 @@ class EigContext:
                                        ev.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                        res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(info)),
                     "eig_solve")
+        n = min(int(info.outer), maxit)
+        self.last_log = [dict(zip(LOG_KEYS, row)) for row in log[:n]]
         return ev, res, info
 
 

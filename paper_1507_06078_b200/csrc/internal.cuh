@@ -13,7 +13,8 @@
 
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
 #define ARR_MAX_P 16    // deepest ARR augmentation (the paper uses p <= 3)
-constexpr int kPhases = 6;  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
+constexpr int kPhases = 6;
+constexpr int kOmegaCols = 8;  // columns of the re-orthogonality sketch (api.cu arr_core)  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
 
 // Row-partition plan of one rank (comm.cu; arr_dist in include/arrabit.h).
 struct DistPlan {
@@ -110,6 +111,7 @@ struct arr_ctx {
     double *vecw;     // [2*ARR_MAX_W] column norms / shifts / scales
     int *dinfo;       // cuSOLVER info + rank counters
     unsigned long long *sched;  // [2] SpMM tile ticket (zeroed at init, self-resetting)
+    double *omega;              // [w x kOmegaCols] seeded Gaussian sketch of the ARR re-orthogonality check
     const int64_t *tile_row0;   // eig_set_schedule (borrowed device arrays) or nullptr
     const int32_t *tile_len;
     int64_t ntiles;
