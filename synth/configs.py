@@ -89,6 +89,19 @@ def starting_block(spec: ConfigSpec, n: int | None = None):
     return np.ascontiguousarray(np.hstack([X0, G]))
 
 
+_CACHE: dict = {}
+
+
 def build_config(spec_or_id) -> tuple[g.CSR, ConfigSpec]:
+    """(CSR, spec).  The most recently built full-size matrix (n >= 1e6) is kept, so a
+    process that needs it twice (the GPU test suite) generates it once; treat it as
+    read-only."""
     spec = CONFIGS[spec_or_id] if isinstance(spec_or_id, int) else spec_or_id
-    return build_matrix(spec.kind, spec.size, spec.seed), spec
+    key = (spec.kind, spec.size, spec.seed)
+    if key in _CACHE:
+        return _CACHE[key], spec
+    A = build_matrix(spec.kind, spec.size, spec.seed)
+    if spec.n >= 1_000_000:
+        _CACHE.clear()
+        _CACHE[key] = A
+    return A, spec
