@@ -78,7 +78,6 @@ struct StencilLaunch {
     int box_x, box_y, hx, hy;
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
     int pf;  // L2 prefetch distance in steps (0: off)
-    int prev_ldg;  // 1: Y_{j-1} loaded by the consumers (not staged through shared memory)
 };
 
 struct arr_ctx {

@@ -82,13 +82,6 @@ __device__ __forceinline__ uint64_t pol_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ double2 ld_stream(const double *p, uint64_t pol) {
-    double2 r;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(r.x), "=d"(r.y)
-                 : "l"(p), "l"(pol));
-    return r;
-}
 __device__ __forceinline__ void st_stream(double *p, double2 v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
                  "l"(pol)
@@ -216,10 +209,10 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
 template <bool HAS_PREV, bool HAS_X>
 struct StageLayout {
     uint32_t box, prev, xa, bytes;
-    __host__ __device__ StageLayout(int nbox, int nrow_max, int pwv, bool prev_ldg = false) {
+    __host__ __device__ StageLayout(int nbox, int nrow_max, int pwv) {
         box = 0;
         prev = (uint32_t)nbox * pwv * 16u;
-        xa = prev + ((HAS_PREV && !prev_ldg) ? (uint32_t)nrow_max * pwv * 16u : 0u);
+        xa = prev + (HAS_PREV ? (uint32_t)nrow_max * pwv * 16u : 0u);
         bytes = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
     }
 };
@@ -236,7 +229,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
     const int tid = threadIdx.x;
     const int NS = P.NS, VS = P.NS + 2;
     const int nbox = P.box_x * P.box_y;
-    const StageLayout<HAS_PREV, HAS_X> SL(nbox, P.Px * P.Py, P.pwv, P.prev_ldg);
+    const StageLayout<HAS_PREV, HAS_X> SL(nbox, P.Px * P.Py, P.pwv);
     const uint32_t vlb = vline_bytes(P.Px, P.Kpad);
     const uint32_t slot_bytes = (uint32_t)P.Py * vlb;
     unsigned char *vring = stages + (size_t)NS * SL.bytes;
@@ -281,7 +274,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                 // job list: [0, box_y) box lines, [box_y, box_y + Py) prev lines,
                 // then X lines, then DIA lines (plane va0 .. va1, Py each)
                 const int nbl = real ? P.box_y : 0;
-                const int npl = (fin && HAS_PREV && !P.prev_ldg) ? I.pye : 0;
+                const int npl = (fin && HAS_PREV) ? I.pye : 0;
                 const int nxl = (fin && HAS_X) ? I.pye : 0;
                 const int nvl = va1 >= va0 ? (va1 - va0 + 1) * I.pye : 0;
                 uint32_t total = 0;
@@ -376,9 +369,6 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
             const bool fin = z - 1 >= I.zc0;                // out(z-1) completes in this step
             const bool mid = z >= I.zc0 && z < I.zc1;       // out(z) gets its plane-z terms
             const bool nxt = z + 1 < I.zc1;                 // out(z+1) starts with its plane-z terms
-            double2 ypl = make_double2(0.0, 0.0);
-            if (HAS_PREV && P.prev_ldg && fin && act)  // Y_{j-1} straight to registers, in flight during the wait
-                ypl = ld_stream(P.Yprev + ((int64_t)(z - 1) * nxy + rxy) * P.ld_prev + (int64_t)(colv0 + v) * 2, pols);
             mbar_wait(full + b, (step / NS) & 1);
             const unsigned char *st = stages + (size_t)b * SL.bytes;
             const double2 *S = reinterpret_cast<const double2 *>(st + SL.box);
@@ -400,7 +390,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                     }
                 }
                 if (fin) {
-                    if (HAS_PREV) yp = P.prev_ldg ? ypl : reinterpret_cast<const double2 *>(st + SL.prev)[rs * pwv + v];
+                    if (HAS_PREV) yp = reinterpret_cast<const double2 *>(st + SL.prev)[rs * pwv + v];
                     if (HAS_X) xa = reinterpret_cast<const double2 *>(st + SL.xa)[rs * pwv + v];
                 }
             }
@@ -514,7 +504,7 @@ __global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_
 template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
 int launch_st(arr_ctx *c, StencilLaunch &L) {
     auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X>;
-    const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv, L.prev_ldg);
+    const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
     const size_t ring = (size_t)(L.NS + 2) * L.Py * vline_bytes(L.Px, L.Kpad);
     const size_t smem = 256 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
     static LaunchCache cache;
@@ -603,8 +593,6 @@ bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, i
 // useful fraction of the launch (ragged patches, last wave of work items).
 bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLaunch &L) {
     const StencilState &S = c->st;
-    static const int prev_ldg = [] { const char *e = getenv("ARRABIT_ST_PREVLDG"); return e ? atoi(e) : 0; }();
-    L.prev_ldg = prev_ldg;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
     const int items_max = kStCons;  // one output vector per consumer thread (IPT = 2 spills at 1024 threads)
@@ -623,8 +611,7 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
                 if ((int64_t)nrow * pwv > items_max) break;
                 if (Px > S.nx || Py > S.ny) break;
                 const int bx = Px + 2 * hx, by = Py + 2 * hy;
-                const size_t stage =
-                    ((size_t)bx * by + (size_t)nrow * ((has_prev && !prev_ldg ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
+                const size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
                 const size_t slot = (size_t)Py * (((size_t)Px * S.Kpad * 8 + 127) & ~(size_t)127);
                 int NS = 4;
                 while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
