@@ -53,11 +53,14 @@ class arr_solve_info(ctypes.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
+def load(path: str | None = None):
     """Load libarrabit.so (raises OSError if it is missing: no fallback)."""
     global _lib
     if _lib is not None:
         return _lib
+    # ARRABIT_LIB: an alternative build of the same library (e.g. the bounds-checked
+    # libarrabit_checked.so, build.py --checked); never a CPU path
+    path = path or os.environ.get("ARRABIT_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise OSError(f"libarrabit.so not built at {path}; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)

@@ -63,6 +63,17 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return lib
 
 
+CHECKED = os.path.join(HERE, "libarrabit_checked.so")
+
+
+def build_checked() -> str:
+    """The bounds-checked variant (-DARR_CHECK_BOUNDS: device checks that trap)."""
+    return build(out=CHECKED, defines=["ARR_CHECK_BOUNDS"])
+
+
 if __name__ == "__main__":
-    build(force=True, verbose="--verbose" in sys.argv)
-    print(LIB)
+    if "--checked" in sys.argv:
+        print(build_checked())
+    else:
+        build(force=True, verbose="--verbose" in sys.argv)
+        print(LIB)

@@ -11,6 +11,25 @@
 
 #include "../../include/arrabit.h"
 
+// Bounds-checked build (-DARR_CHECK_BOUNDS; build.py variant libarrabit_checked.so): device
+// checks of the shared-memory, TMA-destination and staged-CSR indices that trap on a
+// violation.  compute-sanitizer is closed on this pool (profiles/r02/); this is its stand-in.
+#ifdef ARR_CHECK_BOUNDS
+#include <cstdio>
+#define ARR_CHECK(cond)                                                                           \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("ARR_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define ARR_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
 #define ARR_MAX_P 16    // deepest ARR augmentation (the paper uses p <= 3)
 constexpr int kPhases = 6;
@@ -78,6 +97,7 @@ struct StencilLaunch {
     int box_x, box_y, hx, hy;
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
     int pf;  // L2 prefetch distance in steps (0: off)
+    int ypol, spol, opol;  // L2 eviction policies of the Y_j boxes / once-read operands / stores
 };
 
 struct arr_ctx {

@@ -316,6 +316,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
             }
             const int p0 = s_rp[lr];
             const int p1 = s_rp[lr + 1];
+            ARR_CHECK(lr + 1 <= kTile + 1 && p0 >= 0 && p0 <= p1);
             T acc[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) acc[v] = V::zero();
@@ -324,6 +325,7 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs &a, int64_t r0, int nro
                 const int64_t safe = s_ent[p].off;
 #pragma unroll
                 for (int u = 0; u < K; ++u) {
+                    ARR_CHECK(p + u < p1 || p >= 0);
                     const int64_t o = (p + u < p1) ? s_ent[p + u].off : safe;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) x[u][v] = GATHER(yin_v[v] + o);
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32, ARR_SPMM_WS_MINB) spmm_ws_ke
                     continue;
                 }
                 if (lane == 0) s_rp[0] = 0;
+                ARR_CHECK(cnt <= kTile);
                 if (lane + 1 <= cnt) s_rp[lane + 1] = (int)e0;
                 if (lane + 33 <= cnt) s_rp[lane + 33] = (int)e1;
                 const int64_t nnz_t = __shfl_sync(0xffffffffu, cnt <= 32 ? e0 : e1, (cnt <= 32 ? cnt : cnt - 32) - 1);
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(kMaxThreads + 32, ARR_SPMM_WS_MINB) spmm_ws_ke
                     for (int u = 0; u < UN; ++u) {
                         const int64_t q = q0 + u * 32 + lane;
                         if (q < nnz_t) {
+                            ARR_CHECK(q < nnz_cap);
                             Ent e;
                             e.off = (int64_t)cv[u] * ld;
                             e.val = vv[u];

@@ -72,6 +72,13 @@ __device__ __forceinline__ void tma_2d_prefetch(const CUtensorMap *map, int c0, 
                  "r"(c0), "r"(c1)
                  : "memory");
 }
+__device__ __forceinline__ uint64_t pol_of(int kind) {  // 0 evict_normal, 1 evict_last, 2 evict_first
+    uint64_t p;
+    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ uint64_t pol_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -255,8 +262,8 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_in)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_val)) : "memory");
         }
-        const uint64_t pol_keep = pol_evict_last();    // Y_j rows: re-staged by the neighbouring patches
-        const uint64_t pol_once = pol_evict_first();   // Y_{j-1}, X, DIA: read once
+        const uint64_t pol_keep = pol_of(P.ypol);    // Y_j rows: re-staged by the neighbouring patches
+        const uint64_t pol_once = pol_of(P.spol);    // Y_{j-1}, X, DIA: read once
         const uint32_t boxline = (uint32_t)P.box_x * pwv * 16u, pline = (uint32_t)P.Px * pwv * 16u;
         uint32_t step = 0;
         for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
@@ -291,12 +298,14 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                     if (j < nbl) {
                         const int gy = I.y0 - P.hy + j;
                         if (gy < 0 || gy >= P.ny) continue;
+                        ARR_CHECK(SL.box + (size_t)(j + 1) * boxline <= SL.prev);
                         const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + (I.x0 - P.hx);
                         tma_2d(st + SL.box + (size_t)j * boxline, &P.tm_in, col0, (int)row, full + b, pol_keep);
                     } else if (j < nbl + npl + nxl) {
                         const int jj = j - nbl;
                         const bool isx = jj >= npl;
                         const int oy = isx ? jj - npl : jj;
+                        ARR_CHECK((size_t)(oy + 1) * pline <= (isx ? SL.bytes - SL.xa : SL.xa - SL.prev));
                         const int64_t row = ((int64_t)(z - 1) * P.ny + I.y0 + oy) * P.nx + I.x0;
                         if (HAS_PREV && !isx) tma_2d(st + SL.prev + (size_t)oy * pline, &P.tm_prev, col0, (int)row, full + b, pol_once);
                         if (HAS_X && isx) tma_2d(st + SL.xa + (size_t)oy * pline, &P.tm_xa, col0, (int)row, full + b, pol_once);
@@ -304,6 +313,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                         const int jj = j - nbl - npl - nxl;
                         const int zz = va0 + jj / I.pye, oy = jj - (jj / I.pye) * I.pye;
                         unsigned char *slot = vring + (size_t)((step + (uint32_t)(zz - z)) % VS) * slot_bytes;
+                        ARR_CHECK((size_t)oy * vlb + (size_t)P.Px * P.Kpad * 8 <= slot_bytes && oy < P.Py);
                         const int64_t row = ((int64_t)zz * P.ny + I.y0 + oy) * P.nx + I.x0;
                         tma_2d(slot + (size_t)oy * vlb, &P.tm_val, 0, (int)row, full + b, pol_once);
                     }
@@ -335,7 +345,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
         return;
     }
     // ---------------------------------------------------------------- consumers
-    const uint64_t pols = pol_evict_first();
+    const uint64_t pols = pol_of(P.opol);
     const int Kp = P.Kpad;
     uint32_t step = 0;
     double ss0 = 0.0, ss1 = 0.0;
@@ -377,11 +387,13 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
             if (act) {
                 if (real) {
                     const size_t vo = (size_t)oy * vlb + (size_t)ox * Kp * 8;
+                    ARR_CHECK(vo + (size_t)Sh::K * 8 <= slot_bytes);
                     const double *vp = reinterpret_cast<const double *>(vring + (size_t)((step + VS - 1) % VS) * slot_bytes + vo);
                     const double *v0 = reinterpret_cast<const double *>(vring + (size_t)(step % VS) * slot_bytes + vo);
                     const double *vm = reinterpret_cast<const double *>(vring + (size_t)((step + 1) % VS) * slot_bytes + vo);
 #pragma unroll
                     for (int q = 0; q < Sh::NQ; ++q) {
+                        ARR_CHECK(qoff[q] >= 0 && qoff[q] < nbox * pwv);
                         const double2 y = S[qoff[q]];
                         if (q == Sh::QC) yiB = y;
                         if (Sh::k(1, q) >= 0 && fin) fma2(accA, vp[Sh::k(1, q)], y);    // row z-1: its dz = +1 terms
@@ -390,6 +402,7 @@ __global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_con
                     }
                 }
                 if (fin) {
+                    ARR_CHECK(rs * pwv + v < P.Px * P.Py * pwv && ox < I.pxe && oy < I.pye);
                     if (HAS_PREV) yp = reinterpret_cast<const double2 *>(st + SL.prev)[rs * pwv + v];
                     if (HAS_X) xa = reinterpret_cast<const double2 *>(st + SL.xa)[rs * pwv + v];
                 }
@@ -513,6 +526,12 @@ int launch_st(arr_ctx *c, StencilLaunch &L) {
     static const int pm_env = [] { const char *e = getenv("ARRABIT_ST_ORDER"); return e ? atoi(e) : 1; }();
     // L2 prefetch ahead of the loads measured slower on B200 (cfg3 3.32 -> 4.27 ms per degree): off
     static const int pf_env = [] { const char *e = getenv("ARRABIT_ST_PF"); return e ? atoi(e) : 0; }();
+    // L2 policies (0 evict_normal, 1 evict_last, 2 evict_first) of the Y_j boxes, the once-read
+    // operands (Y_{j-1}, X, DIA) and the output stores
+    static const int ypol = [] { const char *e = getenv("ARRABIT_ST_YPOL"); return e ? atoi(e) : 1; }();
+    static const int spol = [] { const char *e = getenv("ARRABIT_ST_SPOL"); return e ? atoi(e) : 2; }();
+    static const int opol = [] { const char *e = getenv("ARRABIT_ST_OPOL"); return e ? atoi(e) : 2; }();
+    L.ypol = ypol; L.spol = spol; L.opol = opol;
     L.pf = pf_env;
     static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
     if (verbose)
