@@ -215,6 +215,23 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
         s.shift = -s.shift;
     }
     if (!is_dist(c)) return launch_spmm(c, s);
+    if (c->cs_link && !s.partials && !s.colshift && !s.Yprev && !s.Xa && s.w == c->w) {
+        // column split: A U for the ARR as (transpose -> A_full x this rank's columns -> transpose):
+        // two all-to-alls of the block instead of an all-gather / halo of its rows
+        ColSplit &S = *c->cs_link;
+        arr_ctx *cc = S.col;
+        const int64_t ltc = ((int64_t)cc->w + 1) & ~int64_t(1);
+        if ((*st = comm_transpose(c->cs_outer, S, 1, s.Yin, s.ld_in, cc->T, ltc)) != ARR_OK) return 0;
+        SpmmArgs t = s;
+        t.row_ptr = cc->A.row_ptr; t.col = cc->A.col_idx; t.val = cc->A.val;
+        t.n = cc->A.n; t.w = cc->w;
+        t.Yin = cc->T; t.ld_in = ltc;
+        t.Yout = cc->Q; t.ld_out = ltc;
+        const int g = launch_spmm(cc, t);
+        if (g < 0) return g;
+        if ((*st = comm_transpose(c->cs_outer, S, 0, cc->Q, ltc, s.Yout, s.ld_out)) != ARR_OK) return 0;
+        return 1;
+    }
     DistPlan &P = c->plan;
     if ((*st = comm_halo_begin(c, s.Yin, s.ld_in, s.w)) != ARR_OK) return 0;
     int rows = 0;
@@ -1020,6 +1037,10 @@ arr_status eig_init_colsplit(arr_ctx **out, const arr_csr *A_full, int32_t k, in
         return st;
     }
     c->ws_bytes = S->col->ws_bytes + S->row->ws_bytes + sizeof(double) * ((size_t)nrow_blk * S->ldrow + 2 * S->buf_elems);
+    if (!getenv("ARRABIT_COLSPLIT_ROWSPMM")) {  // the ARR's SpMMs in the column layout (default)
+        S->row->cs_link = S;
+        S->row->cs_outer = c;
+    }
     *out = c;
     return ARR_OK;
 }

@@ -171,6 +171,10 @@ struct arr_ctx {
     DistPlan plan;
     StencilState st;
     ColSplit *cs;  // column-partitioned outer context (nullptr otherwise)
+    // row context of a column split: its ARR SpMMs run in the column layout (transpose,
+    // local SpMM with the replicated A on the column context, transpose back)
+    ColSplit *cs_link;
+    arr_ctx *cs_outer;
     double *stage;
     size_t stage_elems;
     // pinned host staging
