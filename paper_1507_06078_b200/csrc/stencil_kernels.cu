@@ -32,8 +32,16 @@
 
 namespace {
 
-constexpr int kStThreads = 1024;  // 31 consumer warps (one output vector each per step) + 1 producer warp
-constexpr int kStCons = kStThreads - 32;
+// CTA sizes: NT = 1024 (31 consumer warps, one output vector each per step, + 1 producer
+// warp; one CTA per SM) or 512 (15 + 1; two CTAs per SM, two independent pipelines)
+template <int NT>
+struct StCta {
+    static constexpr int THREADS = NT, CONS = NT - 32, MINB = NT >= 1024 ? 1 : 2;
+};
+int st_threads() {
+    static const int t = [] { const char *e = getenv("ARRABIT_ST_THREADS"); return e && atoi(e) == 512 ? 512 : 1024; }();
+    return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -225,9 +233,10 @@ struct StageLayout {
 };
 __host__ __device__ inline uint32_t vline_bytes(int Px, int Kpad) { return ((uint32_t)Px * Kpad * 8u + 127u) & ~127u; }
 
-template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
-__global__ void __launch_bounds__(kStThreads, 1) stencil_kernel(const __grid_constant__ StencilLaunch P) {
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT>
+__global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __grid_constant__ StencilLaunch P) {
     using Sh = Shape<SH>;
+    constexpr int kStCons = StCta<NT>::CONS;
     extern __shared__ __align__(128) unsigned char sm_raw[];
     unsigned char *sm = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);  // 128-byte aligned base
     uint64_t *full = reinterpret_cast<uint64_t *>(sm);
@@ -514,9 +523,10 @@ __global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_
     }
 }
 
-template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
-int launch_st(arr_ctx *c, StencilLaunch &L) {
-    auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X>;
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT>
+int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
+    constexpr int kStCons = StCta<NT>::CONS, kStThreads = NT;
+    auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X, NT>;
     const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
     const size_t ring = (size_t)(L.NS + 2) * L.Py * vline_bytes(L.Px, L.Kpad);
     const size_t smem = 256 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
@@ -549,6 +559,12 @@ int launch_st(arr_ctx *c, StencilLaunch &L) {
                                    "stencil_kernel (1-D 3-point, DIA, TMA-staged 2.5-D)"};
     c->last_kernel = names[SH];
     return (int)G;
+}
+
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
+int launch_st(arr_ctx *c, StencilLaunch &L) {
+    return st_threads() == 512 ? launch_st_nt<SH, HAS_PREV, SUMSQ, HAS_X, 512>(c, L)
+                               : launch_st_nt<SH, HAS_PREV, SUMSQ, HAS_X, 1024>(c, L);
 }
 
 template <int SH>
@@ -614,8 +630,9 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
     const StencilState &S = c->st;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
-    const int items_max = kStCons;  // one output vector per consumer thread (IPT = 2 spills at 1024 threads)
-    size_t smem_max = (size_t)S.smem_optin - 256;
+    const int items_max = st_threads() - 32;  // one output vector per consumer thread (IPT = 2 spills)
+    // one CTA per SM at 1024 threads; two at 512 (each up to half the SM's shared memory)
+    size_t smem_max = st_threads() == 512 ? (size_t)S.smem_optin / 2 - 2048 : (size_t)S.smem_optin - 256;
     double best = 1e300;
     bool found = false;
     const int hx = S.hx, hy = S.hy;
