@@ -113,9 +113,20 @@ arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
 
 inline int64_t n_glob(const arr_ctx *c) { return c->nranks > 1 ? c->plan.n_global : c->A.n; }
 inline int64_t even_up(int64_t x) { return (x + 1) & ~int64_t(1); }
+// Leading dimension of the library's own n x (.) blocks: a multiple of ARRABIT_LD_ALIGN
+// doubles (default 16: every row starts on a 128-byte line, so a row segment of a column
+// panel touches no partial line; 2 = only 16-byte aligned rows).
+inline int64_t ld_up(int64_t x) {
+    static const int64_t a = [] {
+        const char *e = getenv("ARRABIT_LD_ALIGN");
+        const int64_t v = e ? atoll(e) : 16;
+        return v >= 2 && (v & (v - 1)) == 0 ? v : (int64_t)2;
+    }();
+    return (x + a - 1) / a * a;
+}
 inline int32_t m_of(const arr_ctx *c, int p) { return (p + 1) * c->w; }
-inline int64_t ldQ(const arr_ctx *c) { return even_up(m_of(c, c->p)); }
-inline int64_t ldT(const arr_ctx *c) { return even_up(c->w); }
+inline int64_t ldQ(const arr_ctx *c) { return ld_up(m_of(c, c->p)); }
+inline int64_t ldT(const arr_ctx *c) { return ld_up(c->w); }
 
 // small dense region layout: [H | V | B | G], each m*m doubles
 inline double *H_buf(arr_ctx *c) { const int64_t m = m_of(c, c->p); return c->small; }
@@ -555,6 +566,12 @@ arr_status svqb2(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_
     return ARR_OK;
 }
 
+// H's last block column restricted to its block-tridiagonal rows (ARRABIT_H_TRIDIAG=0: all rows)
+bool h_tridiag() {
+    static const bool v = [] { const char *e = getenv("ARRABIT_H_TRIDIAG"); return !(e && atoi(e) == 0); }();
+    return v;
+}
+
 arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double *Y, int64_t ldy,
                     double *ritz_host, int32_t *rank) {
     const int w = c->w;
@@ -670,8 +687,17 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         const int g = spmm_x(c, s, &st);
         if (st != ARR_OK) return st;
         if (g < 0) return fail(c, ARR_EINVAL, "arr_project: unsupported width");
-        // upper block triangle only: rows [0, (j+1)w) of column block j (H is symmetric)
-        launch_gram(c, Q, lq, (j + 1) * w, T, lt, w, c->A.n, H + (int64_t)j * w, m, c->part);
+        // upper block triangle only: rows [0, (j+1)w) of column block j (H is symmetric).
+        // Block-Lanczos structure (R22): A U_i lies in span(U_0..U_{i+1}) up to the
+        // rounding of the CGS2 + CholeskyQR steps, so U_i^T A U_j = (A U_i)^T U_j = O(u ||A||)
+        // for i <= j - 2: on one GPU the last block column keeps rows [(j-1)w, (j+1)w) only
+        // (p >= 2: 2 n w^2 fewer flops per ARR per skipped block) and the rest is exact zero.
+        const int i0 = (!is_dist(c) && j >= 2 && h_tridiag()) ? j - 1 : 0;
+        if (i0 > 0)
+            CUDA_TRY(cudaMemset2DAsync(H + (int64_t)j * w, sizeof(double) * m, 0, sizeof(double) * w, (size_t)i0 * w,
+                                       c->stream));
+        launch_gram(c, Q + (int64_t)i0 * w, lq, (j + 1 - i0) * w, T, lt, w, c->A.n, H + (int64_t)i0 * w * m + (int64_t)j * w,
+                    m, c->part);
     }
     if (is_dist(c)) ST_TRY(comm_allreduce(c, H, (size_t)m * m, 0));
     launch_symmetrize(c, H, m, w);
@@ -1076,7 +1102,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (c->num_sms <= 0) c->num_sms = 148;
     const int64_t n = A->n + (multi ? dist->n_ghost : 0), w = w_in, m = (int64_t)(p + 1) * w_in;
-    const int64_t lq = even_up(m), lt = even_up(w);
+    const int64_t lq = ld_up(m), lt = ld_up(w);
     const int64_t mm = std::max<int64_t>(m, ARR_MAX_W);
     c->part_elems = (size_t)std::max<int64_t>(16 * m * w, 4096 * mm);
     struct Alloc { void **p; size_t bytes; };
@@ -1652,7 +1678,7 @@ arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const 
     double *d_val = nullptr, *d_X = nullptr;
     arr_ctx *c = nullptr;
     arr_status st = ARR_OK;
-    const int64_t ldx = even_up(w);
+    const int64_t ldx = ld_up(w);
     auto cleanup = [&]() {
         if (c) eig_destroy(c);
         dev_free(d_rp, s); dev_free(d_ci, s); dev_free(d_val, s); dev_free(d_X, s);

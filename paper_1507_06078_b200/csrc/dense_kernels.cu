@@ -390,33 +390,28 @@ __global__ void __launch_bounds__(THREADS, ARR_DMMA_MINB) gemm_kernel_ca(double 
 
 bool ca_ok(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
 
-// ---------------------------------------------------------------- large tiles
-// BM x BN CTA tiles of 32 x 32 warp tiles (4 x 4 DMMA m8n8k4 tiles each; WM x WN warps),
-// KS = 16 rows (Gram) / k-columns (GEMM) per stage, an S_BIG-stage cp.async ring
-// (S_BIG - 1 stages in flight).  Warp sub-tiles outside the output (or, symmetric,
-// strictly below the diagonal) skip their DMMAs.  Same fragments and per-element k order
-// as the 64 x 64 kernels.  Selected with ARRABIT_DMMA_TILE = 1 (128 x 64, 8 warps, 2 CTAs
-// per SM) or 2 (128 x 128, 16 warps); measured on B200 (profiles/r02_dmma_tiles.log) the
-// 64 x 64 kernels above stay the default.
-#ifndef ARR_DMMA_BIG_STAGES
-#define ARR_DMMA_BIG_STAGES 3
-#endif
-constexpr int S_BIG = ARR_DMMA_BIG_STAGES;
+// ---------------------------------------------------------------- tile-shape variants
+// BM x BN CTA tiles of WTM x WTN warp tiles ((WTM/8) x (WTN/8) DMMA m8n8k4 tiles each),
+// KSX rows (Gram) / k-columns (GEMM) per stage, an SS-stage cp.async ring (SS - 1 stages in
+// flight).  Warp sub-tiles outside the output (or, symmetric, strictly below the diagonal)
+// skip their DMMAs.  Same fragments and per-element k order as the 64 x 64 kernels above
+// (bitwise the same sums).  Selected with ARRABIT_DMMA_TILE = 1..6 (tuning experiments;
+// profiles/r02 logs); 0 = the 64 x 64 kernels above.
 constexpr int BPAD = 4;
 
-template <int BM, int BN>
-struct BigCfg {
-    static constexpr int WM = BM / 32, WN = BN / 32, THREADS = WM * WN * 32;
-    static constexpr int MINB = THREADS >= 512 ? 1 : 2;
-    static constexpr size_t gram_smem = sizeof(double) * S_BIG * KS * ((BM + BPAD) + (BN + BPAD));
-    static constexpr size_t gemm_smem = sizeof(double) * S_BIG * (BM * (KS + BPAD) + KS * (BN + BPAD));
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+struct DCfg {
+    static constexpr int WM = BM / WTM, WN = BN / WTN, THREADS = WM * WN * 32;
+    static constexpr int FM = WTM / 8, FN = WTN / 8;
+    static constexpr size_t gram_smem = sizeof(double) * SS * KSX * ((BM + BPAD) + (BN + BPAD));
+    static constexpr size_t gemm_smem = sizeof(double) * SS * (BM * (KSX + BPAD) + KSX * (BN + BPAD));
 };
 
-template <int BM, int BN>
-__global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
-    gram_kernel_big(const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ Y, int64_t ldy,
-                    int m2, int64_t n, int64_t rows_per_split, bool sym, double *__restrict__ part) {
-    using C = BigCfg<BM, BN>;
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+__global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS, MINB)
+    gram_kernel_v(const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ Y, int64_t ldy,
+                  int m2, int64_t n, int64_t rows_per_split, bool sym, double *__restrict__ part) {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
     const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
     const int a0 = ta * BM, b0 = tb * BN;
     if (sym && b0 + BN <= a0) return;  // strictly below the diagonal
@@ -424,26 +419,28 @@ __global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
     int64_t k1 = k0 + rows_per_split;
     if (k1 > n) k1 = n;
     extern __shared__ __align__(16) double dsm[];
-    double (*Xs)[KS][BM + BPAD] = reinterpret_cast<double (*)[KS][BM + BPAD]>(dsm);
-    double (*Ys)[KS][BN + BPAD] = reinterpret_cast<double (*)[KS][BN + BPAD]>(dsm + S_BIG * KS * (BM + BPAD));
+    double (*Xs)[KSX][BM + BPAD] = reinterpret_cast<double (*)[KSX][BM + BPAD]>(dsm);
+    double (*Ys)[KSX][BN + BPAD] = reinterpret_cast<double (*)[KSX][BN + BPAD]>(dsm + SS * KSX * (BM + BPAD));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / C::WN, wn = warp % C::WN;
-    const int ra0 = a0 + wm * 32, cb0 = b0 + wn * 32;
-    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + 32);
-    double acc[4][4][2];
+    const int ra0 = a0 + wm * WTM, cb0 = b0 + wn * WTN;
+    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + WTN);
+    double acc[C::FM][C::FN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < C::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    constexpr int CX = KS * BM / 2, CY = KS * BN / 2;  // 16-byte chunks per stage
+        for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr int CX = KSX * BM / 2, CY = KSX * BN / 2;  // 16-byte chunks per stage
     auto load = [&](int64_t kb, int st) {
-        for (int idx = tid; idx < CX + CY; idx += C::THREADS) {
+#pragma unroll
+        for (int idx0 = 0; idx0 < CX + CY; idx0 += C::THREADS) {
+            const int idx = idx0 + tid;
             if (idx < CX) {
                 const int rr = idx / (BM / 2), cc = (idx % (BM / 2)) * 2;
                 const int64_t row = kb + rr;
                 const int nx = row < k1 ? max(0, min(2, m1 - (a0 + cc))) : 0;
                 ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
-            } else {
+            } else if (idx < CX + CY) {
                 const int j = idx - CX;
                 const int rr = j / (BN / 2), cc = (j % (BN / 2)) * 2;
                 const int64_t row = kb + rr;
@@ -452,31 +449,31 @@ __global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
             }
         }
     };
-    const int64_t nk = (k1 - k0 + KS - 1) / KS;
+    const int64_t nk = (k1 - k0 + KSX - 1) / KSX;
 #pragma unroll
-    for (int st = 0; st < S_BIG - 1; ++st) {
-        if (st < nk) load(k0 + st * KS, st);
+    for (int st = 0; st < SS - 1; ++st) {
+        if (st < nk) load(k0 + st * KSX, st);
         ca_commit();
     }
     for (int64_t it = 0; it < nk; ++it) {
-        ca_wait<S_BIG - 2>();
+        ca_wait<SS - 2>();
         __syncthreads();
-        const int64_t nx = it + S_BIG - 1;
-        if (nx < nk) load(k0 + nx * KS, (int)(nx % S_BIG));
+        const int64_t nx = it + SS - 1;
+        if (nx < nk) load(k0 + nx * KSX, (int)(nx % SS));
         ca_commit();
-        const int buf = (int)(it % S_BIG);
+        const int buf = (int)(it % SS);
         if (work) {
 #pragma unroll
-            for (int kk = 0; kk < KS / 4; ++kk) {
-                double af[4], bf[4];
+            for (int kk = 0; kk < KSX / 4; ++kk) {
+                double af[C::FM], bf[C::FN];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * 32 + mt * 8 + (lane >> 2)];
+                for (int mt = 0; mt < C::FM; ++mt) af[mt] = Xs[buf][kk * 4 + (lane & 3)][wm * WTM + mt * 8 + (lane >> 2)];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+                for (int nt = 0; nt < C::FN; ++nt) bf[nt] = Ys[buf][kk * 4 + (lane & 3)][wn * WTN + nt * 8 + (lane >> 2)];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
+                for (int mt = 0; mt < C::FM; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+                    for (int nt = 0; nt < C::FN; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
             }
         }
     }
@@ -484,9 +481,9 @@ __global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
     if (!work) return;
     double *P = part + (int64_t)split * m1 * m2;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < C::FM; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < C::FN; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int ra = ra0 + mt * 8 + (lane >> 2);
@@ -495,36 +492,38 @@ __global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
             }
 }
 
-template <int BM, int BN>
-__global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
-    gemm_kernel_big(double alpha, const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ B,
-                    int64_t ldb, int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
-                    int64_t n, int upper) {
-    using C = BigCfg<BM, BN>;
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+__global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS, MINB)
+    gemm_kernel_v(double alpha, const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ B,
+                  int64_t ldb, int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
+                  int64_t n, int upper) {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
     const int nct = (m2 + BN - 1) / BN;
     const int64_t r0 = (int64_t)(blockIdx.x / nct) * BM;
     const int c0 = (int)(blockIdx.x % nct) * BN;
     if (upper && c0 + BN < m1) m1 = c0 + BN;
     extern __shared__ __align__(16) double dsm[];
-    double (*Xs)[BM][KS + BPAD] = reinterpret_cast<double (*)[BM][KS + BPAD]>(dsm);
-    double (*Bs)[KS][BN + BPAD] = reinterpret_cast<double (*)[KS][BN + BPAD]>(dsm + S_BIG * BM * (KS + BPAD));
+    double (*Xs)[BM][KSX + BPAD] = reinterpret_cast<double (*)[BM][KSX + BPAD]>(dsm);
+    double (*Bs)[KSX][BN + BPAD] = reinterpret_cast<double (*)[KSX][BN + BPAD]>(dsm + SS * BM * (KSX + BPAD));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / C::WN, wn = warp % C::WN;
-    const bool work = (r0 + wm * 32 < n) && (c0 + wn * 32 < m2);
-    double acc[4][4][2];
+    const bool work = (r0 + wm * WTM < n) && (c0 + wn * WTN < m2);
+    double acc[C::FM][C::FN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < C::FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    constexpr int CX = BM * KS / 2, CB = KS * BN / 2;
+        for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr int CX = BM * KSX / 2, CB = KSX * BN / 2;
     auto load = [&](int kb, int st) {
-        for (int idx = tid; idx < CX + CB; idx += C::THREADS) {
+#pragma unroll
+        for (int idx0 = 0; idx0 < CX + CB; idx0 += C::THREADS) {
+            const int idx = idx0 + tid;
             if (idx < CX) {
-                const int xr = idx / (KS / 2), xk = (idx % (KS / 2)) * 2;
+                const int xr = idx / (KSX / 2), xk = (idx % (KSX / 2)) * 2;
                 const int64_t row = r0 + xr;
                 const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
                 ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
-            } else {
+            } else if (idx < CX + CB) {
                 const int j = idx - CX;
                 const int bk = j / (BN / 2), bc = (j % (BN / 2)) * 2;
                 const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
@@ -532,44 +531,44 @@ __global__ void __launch_bounds__(BigCfg<BM, BN>::THREADS, BigCfg<BM, BN>::MINB)
             }
         }
     };
-    const int nk = (m1 + KS - 1) / KS;
+    const int nk = (m1 + KSX - 1) / KSX;
 #pragma unroll
-    for (int st = 0; st < S_BIG - 1; ++st) {
-        if (st < nk) load(st * KS, st);
+    for (int st = 0; st < SS - 1; ++st) {
+        if (st < nk) load(st * KSX, st);
         ca_commit();
     }
     for (int it = 0; it < nk; ++it) {
-        ca_wait<S_BIG - 2>();
+        ca_wait<SS - 2>();
         __syncthreads();
-        const int nx = it + S_BIG - 1;
-        if (nx < nk) load(nx * KS, nx % S_BIG);
+        const int nx = it + SS - 1;
+        if (nx < nk) load(nx * KSX, nx % SS);
         ca_commit();
-        const int buf = it % S_BIG;
+        const int buf = it % SS;
         if (work) {
 #pragma unroll
-            for (int kk = 0; kk < KS / 4; ++kk) {
-                double af[4], bf[4];
+            for (int kk = 0; kk < KSX / 4; ++kk) {
+                double af[C::FM], bf[C::FN];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[buf][wm * 32 + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+                for (int mt = 0; mt < C::FM; ++mt) af[mt] = Xs[buf][wm * WTM + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * 32 + nt * 8 + (lane >> 2)];
+                for (int nt = 0; nt < C::FN; ++nt) bf[nt] = Bs[buf][kk * 4 + (lane & 3)][wn * WTN + nt * 8 + (lane >> 2)];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
+                for (int mt = 0; mt < C::FM; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
+                    for (int nt = 0; nt < C::FN; ++nt) dmma(acc[mt][nt], af[mt], bf[nt]);
             }
         }
     }
     ca_wait<0>();
     if (!work) return;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < C::FM; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < C::FN; ++nt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int64_t row = r0 + wm * 32 + mt * 8 + (lane >> 2);
-                const int cb = c0 + wn * 32 + nt * 8 + (lane & 3) * 2 + e;
+                const int64_t row = r0 + wm * WTM + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * WTN + nt * 8 + (lane & 3) * 2 + e;
                 if (row < n && cb < m2) {
                     double v = alpha * acc[mt][nt][e];
                     if (beta != 0.0) v += beta * Cin[row * ldc + cb];
@@ -582,35 +581,81 @@ int dmma_tile_choice() {
     static const int t = [] { const char *e = getenv("ARRABIT_DMMA_TILE"); return e ? atoi(e) : 0; }();
     return t;
 }
-bool use_big(int d1, int d2) { return dmma_tile_choice() > 0 && d1 >= 128 && d2 >= 64; }
 
-template <int BM, int BN>
-void launch_gram_big(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
-                     int64_t n, int64_t rps, int ns, bool sym, double *partials) {
-    using C = BigCfg<BM, BN>;
+// the variants (BM, BN, WTM, WTN, KSX, SS, MINB)
+#define DMMA_VARIANTS(X)                 \
+    X(1, 64, 64, 32, 32, 16, 3, 4)       \
+    X(2, 64, 64, 32, 32, 32, 2, 3)       \
+    X(3, 64, 128, 32, 64, 16, 3, 2)      \
+    X(4, 128, 64, 64, 32, 16, 3, 2)      \
+    X(5, 64, 64, 32, 64, 16, 3, 4)       \
+    X(6, 64, 64, 64, 32, 16, 3, 4)
+
+struct VarInfo {
+    int BM, BN;
+    int per_sm;
+};
+
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+VarInfo var_info() {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
     static LaunchCache cache;
-    cached_occupancy(cache, gram_kernel_big<BM, BN>, C::THREADS, C::gram_smem);
-    dim3 gb((m1 + BM - 1) / BM, (m2 + BN - 1) / BN, ns);
-    gram_kernel_big<BM, BN><<<gb, C::THREADS, C::gram_smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    return {BM, BN, cached_occupancy(cache, gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem)};
 }
-template <int BM, int BN>
-void launch_gemm_big(arr_ctx *c, double alpha, const double *X, int64_t ldx, int m1, const double *B, int64_t ldb,
+bool variant_info(int v, VarInfo &out) {
+    switch (v) {
+#define X_INFO(id, a, b, c, d, e, f, g) \
+    case id: out = var_info<a, b, c, d, e, f, g>(); return true;
+        DMMA_VARIANTS(X_INFO)
+#undef X_INFO
+    }
+    return false;
+}
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+void launch_gram_var(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
+                     int64_t n, int64_t rps, int ns, bool sym, double *partials) {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
+    static LaunchCache cache;
+    cached_occupancy(cache, gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem);
+    dim3 gb((m1 + BM - 1) / BM, (m2 + BN - 1) / BN, ns);
+    gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>
+        <<<gb, C::THREADS, C::gram_smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+}
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+void launch_gemm_var(arr_ctx *c, double alpha, const double *X, int64_t ldx, int m1, const double *B, int64_t ldb,
                      int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo, int64_t n,
                      int upper) {
-    using C = BigCfg<BM, BN>;
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
     static LaunchCache cache;
-    cached_occupancy(cache, gemm_kernel_big<BM, BN>, C::THREADS, C::gemm_smem);
+    cached_occupancy(cache, gemm_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gemm_smem);
     const unsigned gb = (unsigned)(((n + BM - 1) / BM) * ((m2 + BN - 1) / BN));
-    gemm_kernel_big<BM, BN><<<gb, C::THREADS, C::gemm_smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc,
-                                                                        Out, ldo, n, upper);
+    gemm_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB><<<gb, C::THREADS, C::gemm_smem, c->stream>>>(
+        alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
 }
-int big_per_sm(int num_sms) {
-    (void)num_sms;
-    static LaunchCache c1, c2;
-    return dmma_tile_choice() == 1
-               ? cached_occupancy(c1, gram_kernel_big<128, 64>, BigCfg<128, 64>::THREADS, BigCfg<128, 64>::gram_smem)
-               : cached_occupancy(c2, gram_kernel_big<128, 128>, BigCfg<128, 128>::THREADS,
-                                  BigCfg<128, 128>::gram_smem);
+bool gram_variant(int v, arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
+                  int64_t n, int64_t rps, int ns, bool sym, double *partials) {
+    switch (v) {
+#define X_GRAM(id, a, b, cc, d, e, f, g)                                                      \
+    case id:                                                                                  \
+        launch_gram_var<a, b, cc, d, e, f, g>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials); \
+        return true;
+        DMMA_VARIANTS(X_GRAM)
+#undef X_GRAM
+    }
+    return false;
+}
+bool gemm_variant(int v, arr_ctx *c, double alpha, const double *X, int64_t ldx, int m1, const double *B, int64_t ldb,
+                  int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo, int64_t n,
+                  int upper) {
+    switch (v) {
+#define X_GEMM(id, a, b, cc, d, e, f, g)                                                                          \
+    case id:                                                                                                      \
+        launch_gemm_var<a, b, cc, d, e, f, g>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper); \
+        return true;
+        DMMA_VARIANTS(X_GEMM)
+#undef X_GEMM
+    }
+    return false;
 }
 
 // ---------------------------------------------------------------- small dense
@@ -675,13 +720,20 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 // partial second wave would idle most SMs for a whole CTA lifetime), at least 512
 // rows each.  sym: only the upper tiles do work.
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
-    const bool big = use_big(m1, m2);
-    const int TM = big ? 128 : TILE, TN = big ? (dmma_tile_choice() == 1 ? 64 : 128) : TILE;
+    VarInfo vi{TILE, TILE, 0};
+    const bool var = dmma_tile_choice() > 0 && variant_info(dmma_tile_choice(), vi);
+    const int TM = vi.BM, TN = vi.BN;
     const int64_t ta = (m1 + TM - 1) / TM, tb = (m2 + TN - 1) / TN;
-    const int64_t tiles = sym ? (TM == TN ? ta * (ta + 1) / 2 : ta * tb - ta * (ta - 1)) : ta * tb;
+    // symmetric: tiles on or above the diagonal (tile b intersects columns >= the tile's first row)
+    int64_t tiles = ta * tb;
+    if (sym) {
+        tiles = 0;
+        for (int64_t i = 0; i < ta; ++i)
+            for (int64_t j = 0; j < tb; ++j) tiles += ((j + 1) * TN > i * TM) ? 1 : 0;
+    }
 #if ARR_DMMA_CA
     static LaunchCache cache;
-    const int per_sm = big ? big_per_sm(num_sms)
+    const int per_sm = var ? vi.per_sm
                            : cached_occupancy(cache, gram_kernel_ca, THREADS, sizeof(double) * 2 * S_CA * KS * (TILE + PAD));
 #else
     static const int per_sm = [] {
@@ -720,9 +772,8 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     rps = (rps + KS - 1) / KS * KS;
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
 #if ARR_DMMA_CA
-    if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(Y, ldy)) {
-        if (dmma_tile_choice() == 1) launch_gram_big<128, 64>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials);
-        else launch_gram_big<128, 128>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials);
+    if (dmma_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(Y, ldy) &&
+        gram_variant(dmma_tile_choice(), c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials)) {
     } else if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
         const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
         static LaunchCache cache;
@@ -740,9 +791,8 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
                  int64_t n, int upper) {
     const unsigned grid = (unsigned)(((n + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE));
 #if ARR_DMMA_CA
-    if (use_big(m1, m2) && ca_ok(X, ldx) && ca_ok(B, ldb)) {
-        if (dmma_tile_choice() == 1) launch_gemm_big<128, 64>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
-        else launch_gemm_big<128, 128>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
+    if (dmma_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(B, ldb) &&
+        gemm_variant(dmma_tile_choice(), c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper)) {
     } else if (ca_ok(X, ldx) && ca_ok(B, ldb)) {
         const size_t smem = sizeof(double) * S_CA * (TILE * (KS + PAD) + KS * (TILE + PAD));
         static LaunchCache cache;

@@ -84,6 +84,8 @@ struct StencilState {
 // One launch of the stencil kernel (kernel parameter, __grid_constant__).
 struct StencilLaunch {
     CUtensorMap tm_in, tm_prev, tm_xa, tm_val;  // TMA descriptors (64-byte aligned)
+    CUtensorMap tm_in_px;  // Y_j with Px-row boxes: the y-halo lines of a plus-shaped (7-point) box
+    int plus;              // 1: y-halo lines without their x-halo corners (7-point)
     const double *Yin, *Yprev, *Xa;
     double *Yout;
     int64_t ld_in, ld_prev, ld_out, ld_xa;
@@ -96,6 +98,8 @@ struct StencilLaunch {
     int Px, Py, Lz, npx, npy, nzc, npan, pwv, NS;
     int box_x, box_y, hx, hy;
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
+    int dyn;  // 1: work items from the atomic ticket `sched` (launches without column sums)
+    unsigned long long *sched;  // [2] ticket + finished-CTA count (self-resetting; the context's)
     int pf;  // L2 prefetch distance in steps (0: off)
     int ypol, spol, opol;  // L2 eviction policies of the Y_j boxes / once-read operands / stores
 };

@@ -43,6 +43,23 @@ int st_threads() {
     return t;
 }
 
+// work items from the atomic ticket in launches without column sums (ARRABIT_ST_DYN=0: static)
+int st_dyn() {
+    static const int v = [] { const char *e = getenv("ARRABIT_ST_DYN"); return e ? atoi(e) : 1; }();
+    return v;
+}
+// z-chunks per column of patches under the ticket (ARRABIT_ST_NZC; 0 = the static rule)
+int st_nzc() {
+    static const int v = [] { const char *e = getenv("ARRABIT_ST_NZC"); return e ? atoi(e) : 1; }();
+    return v;
+}
+
+// 7-point: the y-halo lines are staged without their corners (ARRABIT_ST_PLUS=0: whole lines)
+int st_plus() {
+    static const int v = [] { const char *e = getenv("ARRABIT_ST_PLUS"); return e ? atoi(e) : 1; }();
+    return v;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
@@ -241,6 +258,9 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     unsigned char *sm = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);  // 128-byte aligned base
     uint64_t *full = reinterpret_cast<uint64_t *>(sm);
     uint64_t *empty = full + 4;
+    // meta[b]: the work item whose first step stage b holds (-1: no more items), written by
+    // the producer before its arrive on full[b] (release) and read after the wait (acquire)
+    volatile int64_t *meta = reinterpret_cast<volatile int64_t *>(sm + 64);
     unsigned char *stages = sm + 128;
     const int tid = threadIdx.x;
     const int NS = P.NS, VS = P.NS + 2;
@@ -275,13 +295,18 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         const uint64_t pol_once = pol_of(P.spol);    // Y_{j-1}, X, DIA: read once
         const uint32_t boxline = (uint32_t)P.box_x * pwv * 16u, pline = (uint32_t)P.Px * pwv * 16u;
         uint32_t step = 0;
-        for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
+        // work items: static (it += G) or, dyn, in order from the atomic ticket (the items in
+        // flight stay one contiguous window: neighbouring patches run together and their
+        // shared halo lines are fetched from DRAM once)
+        const bool dyn = !SUMSQ && P.dyn;
+        for (int64_t it = blockIdx.x; it < P.nitems;) {
             const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
             const int col0 = I.panel * pwv * 2;  // first column of the panel
             const int zs = max(I.zc0 - 1, 0);
             for (int z = zs; z <= I.zc1; ++z, ++step) {
                 const int b = (int)(step % NS);
                 if (step >= (uint32_t)NS) mbar_wait(empty + b, ((step / NS) - 1) & 1);
+                if (z == zs && lane == 0) meta[b] = it;
                 const bool real = z < P.nz;
                 const bool fin = z - 1 >= I.zc0;
                 // DIA planes to load: z+1 (and z on the first step when z is an output plane)
@@ -296,7 +321,8 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                 uint32_t total = 0;
                 for (int ly = 0; ly < nbl; ++ly) {
                     const int gy = I.y0 - P.hy + ly;
-                    if (gy >= 0 && gy < P.ny) total += boxline;
+                    const bool yh = P.plus && (ly < P.hy || ly >= P.hy + P.Py);  // a y-halo line: Px rows
+                    if (gy >= 0 && gy < P.ny) total += yh ? pline : boxline;
                 }
                 total += (uint32_t)(npl + nxl) * pline + (uint32_t)nvl * (uint32_t)P.Px * P.Kpad * 8u;
                 if (lane == 0) mbar_expect_tx(full + b, total);
@@ -308,8 +334,15 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                         const int gy = I.y0 - P.hy + j;
                         if (gy < 0 || gy >= P.ny) continue;
                         ARR_CHECK(SL.box + (size_t)(j + 1) * boxline <= SL.prev);
-                        const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + (I.x0 - P.hx);
-                        tma_2d(st + SL.box + (size_t)j * boxline, &P.tm_in, col0, (int)row, full + b, pol_keep);
+                        if (P.plus && (j < P.hy || j >= P.hy + P.Py)) {
+                            // the 7-point stencil reads no corner of the box: rows x0 .. x0+Px-1 only
+                            const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + I.x0;
+                            tma_2d(st + SL.box + (size_t)j * boxline + (size_t)P.hx * pwv * 16, &P.tm_in_px, col0,
+                                   (int)row, full + b, pol_keep);
+                        } else {
+                            const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + (I.x0 - P.hx);
+                            tma_2d(st + SL.box + (size_t)j * boxline, &P.tm_in, col0, (int)row, full + b, pol_keep);
+                        }
                     } else if (j < nbl + npl + nxl) {
                         const int jj = j - nbl;
                         const bool isx = jj >= npl;
@@ -350,6 +383,31 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                     }
                 }
             }
+            if (dyn) {
+                int64_t nx = 0;
+                if (lane == 0) nx = G + (int64_t)atomicAdd(P.sched, 1ull);
+                it = __shfl_sync(0xffffffffu, nx, 0);
+            } else {
+                it += G;
+            }
+        }
+        // end of work: one more stage carrying meta = -1 (no bytes)
+        {
+            const int b = (int)(step % NS);
+            if (step >= (uint32_t)NS) mbar_wait(empty + b, ((step / NS) - 1) & 1);
+            if (lane == 0) {
+                meta[b] = -1;
+                mbar_arrive(full + b);
+            }
+        }
+        if (dyn && lane == 0) {
+            // the last CTA to finish resets the ticket for the next launch
+            __threadfence();
+            if (atomicAdd(P.sched + 1, 1ull) == (unsigned long long)G - 1) {
+                P.sched[0] = 0;
+                P.sched[1] = 0;
+                __threadfence();
+            }
         }
         return;
     }
@@ -359,7 +417,11 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     uint32_t step = 0;
     double ss0 = 0.0, ss1 = 0.0;
     int panel_of_cta = (int)(blockIdx.x % P.npan);
-    for (int64_t it = blockIdx.x; it < P.nitems; it += G) {
+    for (;;) {
+        // the next item is named by the stage of its first step
+        mbar_wait(full + (int)(step % NS), (step / NS) & 1);
+        const int64_t it = meta[(int)(step % NS)];
+        if (it < 0) break;
         const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
         const int pw = min(pwv, P.wv - I.panel * pwv);
         const int nrow = I.pxe * I.pye;
@@ -545,9 +607,12 @@ int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
     L.pf = pf_env;
     static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
     if (verbose)
-        fprintf(stderr, "stencil plan: shape %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu\n",
-                SH, L.w, L.Px, L.Py, L.npan, L.pwv, L.NS, L.Lz, L.nzc, (long long)L.nitems, (long long)G, smem);
+        fprintf(stderr, "stencil plan: shape %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu dyn %d\n",
+                SH, L.w, L.Px, L.Py, L.npan, L.pwv, L.NS, L.Lz, L.nzc, (long long)L.nitems, (long long)G, smem,
+                SUMSQ ? 0 : st_dyn());
     L.pm = SUMSQ ? 0 : pm_env;
+    L.dyn = SUMSQ ? 0 : st_dyn();
+    L.sched = c->sched;
     if (!L.pm) G = (G / L.npan) * L.npan;  // panel-minor: each CTA keeps one panel (static column partial sums)
     if (G > L.nitems) G = L.nitems;
     if (G < L.npan) G = L.npan;
@@ -626,7 +691,7 @@ bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, i
 // Cost model: L2 -> SM bytes per output row = staged rows per patch
 // row + the streamed operands, plus the DIA row once per panel, divided by the
 // useful fraction of the launch (ragged patches, last wave of work items).
-bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLaunch &L) {
+bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, StencilLaunch &L) {
     const StencilState &S = c->st;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
@@ -652,13 +717,17 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, StencilLau
                 int NS = 4;
                 while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
                 if (NS < 2) continue;
-                const int need = bx * by;  // staged rows: whole box lines (one TMA box per line)
+                // staged rows: whole box lines (one TMA box per line); plus-shaped: the y-halo
+                // lines without their corners
+                const int need = bx * by - ((S.shape == 1 && st_plus()) ? 2 * hy * 2 * hx : 0);
                 const int npx = (S.nx + Px - 1) / Px, npy = (S.ny + Py - 1) / Py;
                 const double rag = (double)S.nx * S.ny / ((double)npx * Px * npy * Py);
                 // z-chunks: enough work items for >= ~12 per CTA, chunks of >= 8 planes
                 const int64_t G = (int64_t)c->num_sms;
                 int nzc = 1;
-                while ((int64_t)npx * npy * npan * nzc < 12 * G && S.nz / (nzc + 1) >= 8) ++nzc;
+                if (dyn && st_nzc() > 0) nzc = std::min<int>(st_nzc(), (int)S.nz);
+                else
+                    while ((int64_t)npx * npy * npan * nzc < 12 * G && S.nz / (nzc + 1) >= 8) ++nzc;
                 const int Lz = (S.nz + nzc - 1) / nzc;
                 nzc = (S.nz + Lz - 1) / Lz;
                 const int64_t items = (int64_t)npx * npy * npan * nzc;
@@ -702,7 +771,8 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     if (a.Yprev && !al16(a.Yprev, a.ld_prev)) return -1;
     if (a.Xa && !al16(a.Xa, a.ld_xa)) return -1;
     StencilLaunch L{};
-    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, L)) return -1;
+    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L)) return -1;
+    L.plus = (c->st.shape == 1 && L.hy > 0 && st_plus()) ? 1 : 0;
     L.Yin = a.Yin; L.ld_in = a.ld_in;
     L.Yprev = a.Yprev; L.ld_prev = a.ld_prev;
     L.Yout = a.Yout; L.ld_out = a.ld_out;
@@ -712,6 +782,7 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     const int64_t nrows = c->A.n;
     if (!encode_2d(&L.tm_in, a.Yin, a.w, nrows, a.ld_in, 2 * L.pwv, L.box_x) ||
         !encode_2d(&L.tm_val, c->st.dia, c->st.Kpad, nrows, c->st.Kpad, c->st.Kpad, L.Px) ||
+        (L.plus && !encode_2d(&L.tm_in_px, a.Yin, a.w, nrows, a.ld_in, 2 * L.pwv, L.Px)) ||
         (a.Yprev && !encode_2d(&L.tm_prev, a.Yprev, a.w, nrows, a.ld_prev, 2 * L.pwv, L.Px)) ||
         (a.Xa && !encode_2d(&L.tm_xa, a.Xa, a.w, nrows, a.ld_xa, 2 * L.pwv, L.Px)))
         return -1;

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--paths", nargs="+", default=["csr", "st"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--yband", action="store_true", help="CSR path with the y-band row order for 3-D grids")
+    ap.add_argument("--ld-align", type=int, default=16, help="row stride of X rounded up to this many doubles")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -42,11 +43,12 @@ def main():
         A, spec = configs.build_config(cid)
         w, d = spec.w, spec.d
         Ad = arr.to_device_csr(A)
-        X = torch.empty((A.n, w), dtype=torch.float64, device="cuda")
+        ldx = (w + args.ld_align - 1) // args.ld_align * args.ld_align
+        X = torch.empty((A.n, ldx), dtype=torch.float64, device="cuda")[:, :w]
         for r0 in range(0, A.n, 1 << 21):
             r1 = min(A.n, r0 + (1 << 21))
             X[r0:r1] = torch.from_numpy(synth.gaussian_block_rows(A.n, w, spec.seed, r0, r1))
-        X0 = X.clone() if A.n * w * 8 < 40e9 else None
+        X0 = torch.empty_like(X).copy_(X) if A.n * w * 8 < 40e9 else None
         rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
         upper = float(np.bincount(rows, weights=np.abs(A.val), minlength=A.n).max())
         del rows

@@ -3,7 +3,7 @@ ARR shapes of the cfg2 / cfg3 solves.  Shapes: the Gram X^T Y of
 orthonormalisation and CGS passes (m1 x m2 = jw x w), the symmetric X^T X, and the
 update / Ritz GEMM X B (n x m1 by m1 x m2).
 
-    python scripts/micro_gram_shapes.py [--no-cublas]        (ARRABIT_DMMA_BIG=0: 64 x 64 tiles only)
+    python scripts/micro_gram_shapes.py [--no-cublas | --cublas-only]   (ARRABIT_DMMA_TILE=v: tile variant v)
 """
 import ctypes
 import os
@@ -68,7 +68,8 @@ class Diag:  # identity CSR of order n: the context only needs A.n for the dense
 
 def main():
     cub = "--no-cublas" not in sys.argv
-    tag = "arr(64x64 only)" if os.environ.get("ARRABIT_DMMA_BIG") == "0" else "arr"
+    tag = f"arr(tile variant {os.environ.get('ARRABIT_DMMA_TILE', '0')})"
+    only_cublas = "--cublas-only" in sys.argv
     syrk = cublas_syrk() if cub else None
     for n, m1, m2 in SHAPES:
         X = torch.randn(n, m1, dtype=torch.float64, device="cuda")
@@ -86,17 +87,23 @@ def main():
                 ms = t(lambda: syrk(X, C))
                 print(f"cuBLAS DSYRK X^T X  n={n} {m1}: {ms*1e3:8.0f} us {fl/2/ms/1e9:5.1f} TF/s (n w(w+1) flops)"
                       f"  {fl/ms/1e9:5.1f} TF/s (2nw^2)", flush=True)
+        if only_cublas:
+            continue
         w = max(m1, m2)
         ctx = arr.eig_init(arr.to_device_csr(Diag(n)), w, 2, 2, w=w)
         G = torch.empty(m1, m2, dtype=torch.float64, device="cuda")
         ms = t(lambda: ctx.gram(X, Y, G))
-        print(f"{tag} gram X^T Y    n={n} {m1}x{m2}: {ms*1e3:8.0f} us {fl/ms/1e9:5.1f} TF/s", flush=True)
+        ref = X.T @ Y
+        err = float((G - ref).abs().max() / ref.abs().max())
+        print(f"{tag} gram X^T Y    n={n} {m1}x{m2}: {ms*1e3:8.0f} us {fl/ms/1e9:5.1f} TF/s  (max rel dev from cuBLAS {err:.1e})", flush=True)
         if m1 == m2:
             ms = t(lambda: ctx.gram(X, X, G))
             print(f"{tag} gram X^T X    n={n} {m1}: {ms*1e3:8.0f} us {fl/2/ms/1e9:5.1f} TF/s (n w(w+1) flops)"
                   f"  {fl/ms/1e9:5.1f} TF/s (2nw^2)", flush=True)
         ms = t(lambda: ctx.gemm(X, B, O))
-        print(f"{tag} gemm X B      n={n} {m1}->{m2}: {ms*1e3:8.0f} us {fl/ms/1e9:5.1f} TF/s", flush=True)
+        ref = X @ B
+        err = float((O - ref).abs().max() / ref.abs().max())
+        print(f"{tag} gemm X B      n={n} {m1}->{m2}: {ms*1e3:8.0f} us {fl/ms/1e9:5.1f} TF/s  (max rel dev from cuBLAS {err:.1e})", flush=True)
         ctx.close()
         del X, Y, B, O, G
         torch.cuda.empty_cache()

@@ -242,6 +242,29 @@ def test_arr_exact_eigenvectors(arr):
     assert np.max(ctx.residuals(Yd, ritz[:k])) < 1e-12
 
 
+def test_arr_exact_eigenvectors_p2(arr):
+    """p = 2 on an exactly invariant X: the augmentation blocks U_1, U_2 are orthonormalised
+    rounding noise (no Krylov information), the case where the block-tridiagonal H of
+    reading R22 leans hardest on U_2 being orthogonal to U_0 and U_1.  The k wanted Ritz
+    pairs must still be the exact eigenpairs."""
+    n, k = 2000, 20
+    A = synth.laplacian_1d(n)
+    j = np.arange(1, n + 1)
+    lam = 2 - 2 * np.cos(j * np.pi / (n + 1))
+    top = np.argsort(-lam)[:k]
+    V = np.sin(np.outer(j, j[top]) * np.pi / (n + 1))
+    V /= np.linalg.norm(V, axis=0)
+    ctx = arr.eig_init(arr.to_device_csr(A), k=k, p=2, d=10)
+    Xd = dev_block(V @ np.random.default_rng(0).standard_normal((k, k)))
+    Yd = dev_block(np.zeros((n, k)))
+    ritz, _ = ctx.arr_project(Xd, Yd)
+    assert np.max(np.abs(ritz[:k] - lam[top]) / lam[top]) < 1e-13
+    assert np.max(ctx.residuals(Yd, ritz[:k])) < 1e-12
+    # every Ritz value of the 3k-dimensional space lies in the spectrum's range (a true
+    # Rayleigh quotient of an orthonormal basis)
+    assert ritz.min() > -1e-12 and ritz.max() < 4 + 1e-12
+
+
 # ---------------------------------------------------------------- residuals (A6)
 def test_residuals_vs_oracle(arr):
     A = synth.zipf_random(6000, 7)
