@@ -577,67 +577,283 @@ __global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS
             }
 }
 
+// Software-pipelined versions (the CUTLASS multistage pattern): the fragments of step kk+1
+// are loaded from shared memory while the DMMAs of step kk run (two fragment buffers), the
+// stage's cp.async copies are spread over its kk steps, and the wait + barrier for the next
+// stage sit before the last kk step's DMMAs.  Same fragments, same per-element k order:
+// bitwise the same sums as the kernels above.
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+__global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS, MINB)
+    gram_kernel_pv(const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ Y, int64_t ldy,
+                   int m2, int64_t n, int64_t rows_per_split, bool sym, double *__restrict__ part) {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
+    constexpr int KK = KSX / 4;
+    const int ta = blockIdx.x, tb = blockIdx.y, split = blockIdx.z;
+    const int a0 = ta * BM, b0 = tb * BN;
+    if (sym && b0 + BN <= a0) return;  // strictly below the diagonal
+    const int64_t k0 = (int64_t)split * rows_per_split;
+    int64_t k1 = k0 + rows_per_split;
+    if (k1 > n) k1 = n;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[KSX][BM + BPAD] = reinterpret_cast<double (*)[KSX][BM + BPAD]>(dsm);
+    double (*Ys)[KSX][BN + BPAD] = reinterpret_cast<double (*)[KSX][BN + BPAD]>(dsm + SS * KSX * (BM + BPAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / C::WN, wn = warp % C::WN;
+    const int ra0 = a0 + wm * WTM, cb0 = b0 + wn * WTN;
+    const bool work = (ra0 < m1) && (cb0 < m2) && !(sym && ra0 >= cb0 + WTN);
+    double acc[C::FM][C::FN][2];
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr int CX = KSX * BM / 2, CY = KSX * BN / 2;  // 16-byte chunks per stage
+    constexpr int NCH = (CX + CY + C::THREADS - 1) / C::THREADS;  // chunks per thread per stage
+    auto load_chunk = [&](int64_t kb, int st, int q) {
+        const int idx = q * C::THREADS + tid;
+        if (idx < CX) {
+            const int rr = idx / (BM / 2), cc = (idx % (BM / 2)) * 2;
+            const int64_t row = kb + rr;
+            const int nx = row < k1 ? max(0, min(2, m1 - (a0 + cc))) : 0;
+            ca16(&Xs[st][rr][cc], nx ? X + row * ldx + a0 + cc : X, nx * 8);
+        } else if (idx < CX + CY) {
+            const int j = idx - CX;
+            const int rr = j / (BN / 2), cc = (j % (BN / 2)) * 2;
+            const int64_t row = kb + rr;
+            const int ny = row < k1 ? max(0, min(2, m2 - (b0 + cc))) : 0;
+            ca16(&Ys[st][rr][cc], ny ? Y + row * ldy + b0 + cc : Y, ny * 8);
+        }
+    };
+    const int64_t nk = (k1 - k0 + KSX - 1) / KSX;
+#pragma unroll
+    for (int st = 0; st < SS - 1; ++st) {
+        if (st < nk)
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) load_chunk(k0 + st * KSX, st, q);
+        ca_commit();
+    }
+    ca_wait<SS - 2>();
+    __syncthreads();
+    double af[2][C::FM], bf[2][C::FN];
+    auto frag = [&](int buf, int kk, int f) {
+#pragma unroll
+        for (int mt = 0; mt < C::FM; ++mt) af[f][mt] = Xs[buf][kk * 4 + (lane & 3)][wm * WTM + mt * 8 + (lane >> 2)];
+#pragma unroll
+        for (int nt = 0; nt < C::FN; ++nt) bf[f][nt] = Ys[buf][kk * 4 + (lane & 3)][wn * WTN + nt * 8 + (lane >> 2)];
+    };
+    if (nk > 0) frag(0, 0, 0);
+    for (int64_t it = 0; it < nk; ++it) {
+        const int buf = (int)(it % SS);
+        const int64_t nx = it + SS - 1;
+        const int nbuf = (int)(nx % SS);
+#pragma unroll
+        for (int kk = 0; kk < KK; ++kk) {
+            // this stage's share of the copies of stage it + SS - 1 (into the buffer every warp
+            // finished reading before the previous barrier)
+#pragma unroll
+            for (int q = kk; q < NCH; q += KK)
+                if (nx < nk) load_chunk(k0 + nx * KSX, nbuf, q);
+            if (kk == KK - 1) {
+                ca_commit();
+                if (it + 1 < nk) {
+                    ca_wait<SS - 2>();
+                    __syncthreads();
+                    frag((int)((it + 1) % SS), 0, (kk + 1) & 1);
+                }
+            } else {
+                frag(buf, kk + 1, (kk + 1) & 1);
+            }
+            if (work) {
+#pragma unroll
+                for (int mt = 0; mt < C::FM; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < C::FN; ++nt) dmma(acc[mt][nt], af[kk & 1][mt], bf[kk & 1][nt]);
+            }
+        }
+    }
+    ca_wait<0>();
+    if (!work) return;
+    double *P = part + (int64_t)split * m1 * m2;
+#pragma unroll
+    for (int mt = 0; mt < C::FM; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::FN; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int ra = ra0 + mt * 8 + (lane >> 2);
+                const int cb = cb0 + nt * 8 + (lane & 3) * 2 + e;
+                if (ra < m1 && cb < m2) P[(int64_t)ra * m2 + cb] = acc[mt][nt][e];
+            }
+}
+
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+__global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS, MINB)
+    gemm_kernel_pv(double alpha, const double *__restrict__ X, int64_t ldx, int m1, const double *__restrict__ B,
+                   int64_t ldb, int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
+                   int64_t n, int upper) {
+    using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
+    constexpr int KK = KSX / 4;
+    const int nct = (m2 + BN - 1) / BN;
+    const int64_t r0 = (int64_t)(blockIdx.x / nct) * BM;
+    const int c0 = (int)(blockIdx.x % nct) * BN;
+    if (upper && c0 + BN < m1) m1 = c0 + BN;
+    extern __shared__ __align__(16) double dsm[];
+    double (*Xs)[BM][KSX + BPAD] = reinterpret_cast<double (*)[BM][KSX + BPAD]>(dsm);
+    double (*Bs)[KSX][BN + BPAD] = reinterpret_cast<double (*)[KSX][BN + BPAD]>(dsm + SS * BM * (KSX + BPAD));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / C::WN, wn = warp % C::WN;
+    const bool work = (r0 + wm * WTM < n) && (c0 + wn * WTN < m2);
+    double acc[C::FM][C::FN][2];
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    constexpr int CX = BM * KSX / 2, CB = KSX * BN / 2;
+    constexpr int NCH = (CX + CB + C::THREADS - 1) / C::THREADS;
+    auto load_chunk = [&](int kb, int st, int q) {
+        const int idx = q * C::THREADS + tid;
+        if (idx < CX) {
+            const int xr = idx / (KSX / 2), xk = (idx % (KSX / 2)) * 2;
+            const int64_t row = r0 + xr;
+            const int nx = row < n ? max(0, min(2, m1 - (kb + xk))) : 0;
+            ca16(&Xs[st][xr][xk], nx ? X + row * ldx + kb + xk : X, nx * 8);
+        } else if (idx < CX + CB) {
+            const int j = idx - CX;
+            const int bk = j / (BN / 2), bc = (j % (BN / 2)) * 2;
+            const int nb = (kb + bk < m1) ? max(0, min(2, m2 - (c0 + bc))) : 0;
+            ca16(&Bs[st][bk][bc], nb ? B + (int64_t)(kb + bk) * ldb + c0 + bc : B, nb * 8);
+        }
+    };
+    const int nk = (m1 + KSX - 1) / KSX;
+#pragma unroll
+    for (int st = 0; st < SS - 1; ++st) {
+        if (st < nk)
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) load_chunk(st * KSX, st, q);
+        ca_commit();
+    }
+    ca_wait<SS - 2>();
+    __syncthreads();
+    double af[2][C::FM], bf[2][C::FN];
+    auto frag = [&](int buf, int kk, int f) {
+#pragma unroll
+        for (int mt = 0; mt < C::FM; ++mt) af[f][mt] = Xs[buf][wm * WTM + mt * 8 + (lane >> 2)][kk * 4 + (lane & 3)];
+#pragma unroll
+        for (int nt = 0; nt < C::FN; ++nt) bf[f][nt] = Bs[buf][kk * 4 + (lane & 3)][wn * WTN + nt * 8 + (lane >> 2)];
+    };
+    if (nk > 0) frag(0, 0, 0);
+    for (int it = 0; it < nk; ++it) {
+        const int buf = it % SS;
+        const int nx = it + SS - 1;
+        const int nbuf = nx % SS;
+#pragma unroll
+        for (int kk = 0; kk < KK; ++kk) {
+#pragma unroll
+            for (int q = kk; q < NCH; q += KK)
+                if (nx < nk) load_chunk(nx * KSX, nbuf, q);
+            if (kk == KK - 1) {
+                ca_commit();
+                if (it + 1 < nk) {
+                    ca_wait<SS - 2>();
+                    __syncthreads();
+                    frag((it + 1) % SS, 0, (kk + 1) & 1);
+                }
+            } else {
+                frag(buf, kk + 1, (kk + 1) & 1);
+            }
+            if (work) {
+#pragma unroll
+                for (int mt = 0; mt < C::FM; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < C::FN; ++nt) dmma(acc[mt][nt], af[kk & 1][mt], bf[kk & 1][nt]);
+            }
+        }
+    }
+    ca_wait<0>();
+    if (!work) return;
+#pragma unroll
+    for (int mt = 0; mt < C::FM; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::FN; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t row = r0 + wm * WTM + mt * 8 + (lane >> 2);
+                const int cb = c0 + wn * WTN + nt * 8 + (lane & 3) * 2 + e;
+                if (row < n && cb < m2) {
+                    double v = alpha * acc[mt][nt][e];
+                    if (beta != 0.0) v += beta * Cin[row * ldc + cb];
+                    Out[row * ldo + cb] = v;
+                }
+            }
+}
+
 int dmma_tile_choice() {
     static const int t = [] { const char *e = getenv("ARRABIT_DMMA_TILE"); return e ? atoi(e) : 0; }();
     return t;
 }
 
 // the variants (BM, BN, WTM, WTN, KSX, SS, MINB)
-#define DMMA_VARIANTS(X)                 \
-    X(1, 64, 64, 32, 32, 16, 3, 4)       \
-    X(2, 64, 64, 32, 32, 32, 2, 3)       \
-    X(3, 64, 128, 32, 64, 16, 3, 2)      \
-    X(4, 128, 64, 64, 32, 16, 3, 2)      \
-    X(5, 64, 64, 32, 64, 16, 3, 4)       \
-    X(6, 64, 64, 64, 32, 16, 3, 4)
+#define DMMA_VARIANTS(X)                    \
+    X(1, 64, 64, 32, 32, 16, 3, 4, false)   \
+    X(2, 64, 64, 32, 32, 32, 2, 3, false)   \
+    X(3, 64, 128, 32, 64, 16, 3, 2, false)  \
+    X(4, 128, 64, 64, 32, 16, 3, 2, false)  \
+    X(5, 64, 64, 32, 64, 16, 3, 4, false)   \
+    X(6, 64, 64, 64, 32, 16, 3, 4, false)   \
+    X(7, 64, 64, 32, 32, 16, 4, 3, true)    \
+    X(8, 64, 64, 32, 32, 16, 3, 4, true)    \
+    X(9, 64, 128, 32, 64, 16, 3, 2, true)   \
+    X(10, 128, 64, 64, 32, 16, 3, 2, true)  \
+    X(11, 64, 64, 32, 32, 32, 3, 2, true)
 
 struct VarInfo {
     int BM, BN;
     int per_sm;
 };
 
-template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB, bool PIPE>
 VarInfo var_info() {
     using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
     static LaunchCache cache;
-    return {BM, BN, cached_occupancy(cache, gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem)};
+    return {BM, BN,
+            PIPE ? cached_occupancy(cache, gram_kernel_pv<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem)
+                 : cached_occupancy(cache, gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem)};
 }
 bool variant_info(int v, VarInfo &out) {
     switch (v) {
-#define X_INFO(id, a, b, c, d, e, f, g) \
-    case id: out = var_info<a, b, c, d, e, f, g>(); return true;
+#define X_INFO(id, a, b, c, d, e, f, g, pipe) \
+    case id: out = var_info<a, b, c, d, e, f, g, pipe>(); return true;
         DMMA_VARIANTS(X_INFO)
 #undef X_INFO
     }
     return false;
 }
-template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB, bool PIPE>
 void launch_gram_var(arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
                      int64_t n, int64_t rps, int ns, bool sym, double *partials) {
     using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
+    auto kern = PIPE ? gram_kernel_pv<BM, BN, WTM, WTN, KSX, SS, MINB> : gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>;
     static LaunchCache cache;
-    cached_occupancy(cache, gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gram_smem);
+    cached_occupancy(cache, kern, C::THREADS, C::gram_smem);
     dim3 gb((m1 + BM - 1) / BM, (m2 + BN - 1) / BN, ns);
-    gram_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>
-        <<<gb, C::THREADS, C::gram_smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    kern<<<gb, C::THREADS, C::gram_smem, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
 }
-template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB>
+template <int BM, int BN, int WTM, int WTN, int KSX, int SS, int MINB, bool PIPE>
 void launch_gemm_var(arr_ctx *c, double alpha, const double *X, int64_t ldx, int m1, const double *B, int64_t ldb,
                      int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo, int64_t n,
                      int upper) {
     using C = DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>;
+    auto kern = PIPE ? gemm_kernel_pv<BM, BN, WTM, WTN, KSX, SS, MINB> : gemm_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>;
     static LaunchCache cache;
-    cached_occupancy(cache, gemm_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB>, C::THREADS, C::gemm_smem);
+    cached_occupancy(cache, kern, C::THREADS, C::gemm_smem);
     const unsigned gb = (unsigned)(((n + BM - 1) / BM) * ((m2 + BN - 1) / BN));
-    gemm_kernel_v<BM, BN, WTM, WTN, KSX, SS, MINB><<<gb, C::THREADS, C::gemm_smem, c->stream>>>(
-        alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
+    kern<<<gb, C::THREADS, C::gemm_smem, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
 }
 bool gram_variant(int v, arr_ctx *c, const double *X, int64_t ldx, int m1, const double *Y, int64_t ldy, int m2,
                   int64_t n, int64_t rps, int ns, bool sym, double *partials) {
     switch (v) {
-#define X_GRAM(id, a, b, cc, d, e, f, g)                                                      \
+#define X_GRAM(id, a, b, cc, d, e, f, g, pipe)                                                \
     case id:                                                                                  \
-        launch_gram_var<a, b, cc, d, e, f, g>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials); \
+        launch_gram_var<a, b, cc, d, e, f, g, pipe>(c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials); \
         return true;
         DMMA_VARIANTS(X_GRAM)
 #undef X_GRAM
@@ -648,9 +864,9 @@ bool gemm_variant(int v, arr_ctx *c, double alpha, const double *X, int64_t ldx,
                   int m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo, int64_t n,
                   int upper) {
     switch (v) {
-#define X_GEMM(id, a, b, cc, d, e, f, g)                                                                          \
+#define X_GEMM(id, a, b, cc, d, e, f, g, pipe)                                                                    \
     case id:                                                                                                      \
-        launch_gemm_var<a, b, cc, d, e, f, g>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper); \
+        launch_gemm_var<a, b, cc, d, e, f, g, pipe>(c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper); \
         return true;
         DMMA_VARIANTS(X_GEMM)
 #undef X_GEMM

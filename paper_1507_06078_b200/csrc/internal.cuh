@@ -84,8 +84,6 @@ struct StencilState {
 // One launch of the stencil kernel (kernel parameter, __grid_constant__).
 struct StencilLaunch {
     CUtensorMap tm_in, tm_prev, tm_xa, tm_val;  // TMA descriptors (64-byte aligned)
-    CUtensorMap tm_in_px;  // Y_j with Px-row boxes: the y-halo lines of a plus-shaped (7-point) box
-    int plus;              // 1: y-halo lines without their x-halo corners (7-point)
     const double *Yin, *Yprev, *Xa;
     double *Yout;
     int64_t ld_in, ld_prev, ld_out, ld_xa;
@@ -100,7 +98,6 @@ struct StencilLaunch {
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
     int dyn;  // 1: work items from the atomic ticket `sched` (launches without column sums)
     unsigned long long *sched;  // [2] ticket + finished-CTA count (self-resetting; the context's)
-    int pf;  // L2 prefetch distance in steps (0: off)
     int ypol, spol, opol;  // L2 eviction policies of the Y_j boxes / once-read operands / stores
 };
 

@@ -54,12 +54,6 @@ int st_nzc() {
     return v;
 }
 
-// 7-point: the y-halo lines are staged without their corners (ARRABIT_ST_PLUS=0: whole lines)
-int st_plus() {
-    static const int v = [] { const char *e = getenv("ARRABIT_ST_PLUS"); return e ? atoi(e) : 1; }();
-    return v;
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
@@ -80,22 +74,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
             : "r"(smem_u32(b)), "r"(parity)
             : "memory");
     } while (!ok);
-}
-// one 2-D box of a tensor map global -> shared (TMA; out-of-range rows are zero-filled)
-__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar,
-                                       uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-// the same box into L2 only (no shared memory, no barrier): issued a few steps ahead of the
-// load so that the load finds its lines in L2 and more DRAM requests are in flight per SM
-__device__ __forceinline__ void tma_2d_prefetch(const CUtensorMap *map, int c0, int c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1)
-                 : "memory");
 }
 __device__ __forceinline__ uint64_t pol_of(int kind) {  // 0 evict_normal, 1 evict_last, 2 evict_first
     uint64_t p;
@@ -233,10 +211,10 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
     return r;
 }
 
-// Shared memory of one CTA: [full[4] | empty[4] mbarriers (128 B)] [NS stages] [val ring],
-// every region 128-byte aligned (TMA destinations):
-// stage:    box lines of Y_j (box_y lines x box_x rows x 2 pwv doubles) | Y_{j-1} lines |
-//           X lines (Py lines x Px rows each)
+// Shared memory of one CTA: [full[4] | empty[4] mbarriers | meta[4] (128 B)] [NS stages]
+// [val ring], every region 128-byte aligned (TMA destinations):
+// stage:    box of Y_j (box_y lines x box_x rows x pwv 16-byte vectors) | Y_{j-1} rows |
+//           X rows (Py lines x Px rows each)
 // val ring: VS = NS + 2 slots, one plane of the patch's DIA rows (Py lines x Px rows x Kpad)
 template <bool HAS_PREV, bool HAS_X>
 struct StageLayout {
@@ -248,7 +226,20 @@ struct StageLayout {
         bytes = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
     }
 };
-__host__ __device__ inline uint32_t vline_bytes(int Px, int Kpad) { return ((uint32_t)Px * Kpad * 8u + 127u) & ~127u; }
+// one DIA plane of a patch (the TMA box's bytes) and its ring slot (128-byte aligned)
+__host__ __device__ inline uint32_t vplane_bytes(int Px, int Py, int Kpad) { return (uint32_t)Px * Py * Kpad * 8u; }
+__host__ __device__ inline uint32_t vslot_bytes(int Px, int Py, int Kpad) { return (vplane_bytes(Px, Py, Kpad) + 127u) & ~127u; }
+
+// one 4-D box (columns, x, y, z) of a tensor map global -> shared; coordinates outside the
+// grid (x = -1 / nx, y = -1 / ny, columns >= w) are zero-filled and count in complete_tx
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap *map, int c0, int x, int y, int z,
+                                       uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3, %4, %5}], [%6], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(x), "r"(y), "r"(z), "r"(bar), "l"(pol)
+        : "memory");
+}
 
 template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT>
 __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __grid_constant__ StencilLaunch P) {
@@ -264,10 +255,8 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     unsigned char *stages = sm + 128;
     const int tid = threadIdx.x;
     const int NS = P.NS, VS = P.NS + 2;
-    const int nbox = P.box_x * P.box_y;
-    const StageLayout<HAS_PREV, HAS_X> SL(nbox, P.Px * P.Py, P.pwv);
-    const uint32_t vlb = vline_bytes(P.Px, P.Kpad);
-    const uint32_t slot_bytes = (uint32_t)P.Py * vlb;
+    const StageLayout<HAS_PREV, HAS_X> SL(P.box_x * P.box_y, P.Px * P.Py, P.pwv);
+    const uint32_t slot_bytes = vslot_bytes(P.Px, P.Py, P.Kpad);
     unsigned char *vring = stages + (size_t)NS * SL.bytes;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -278,129 +267,70 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     }
     __syncthreads();
     const int64_t G = gridDim.x;
-    const int64_t nxy = (int64_t)P.nx * P.ny;
     const int pwv = P.pwv;  // smem row stride in 16-byte vectors (a multiple of 8: 128-byte rows)
     if (tid >= kStCons) {
-        // ------------------------------------------------------------ producer warp
-        // Per step (plane z of the march; z == nz is a tail step with no plane), one TMA
-        // box per grid-line run, completing on full[b]: the box lines of plane z that exist
-        // (box_x rows with the x halo), the Y_{j-1} (and X) lines of the outputs of plane
-        // z-1, and the DIA lines of plane z+1 (and of plane z on an item's first step).
-        const int lane = tid - kStCons;
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_in)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_val)) : "memory");
-        }
+        // ------------------------------------------------------------ producer warp (lane 0)
+        // Per step (plane z of the march; z == nz is a tail step with no plane) at most five
+        // TMA boxes completing on full[b]: the Y_j box of plane z (box_x x box_y rows with the
+        // x/y halo), the Y_{j-1} (and X) rows of the outputs of plane z-1, and the DIA rows
+        // of plane z+1 (and of plane z on an item's first step).
+        if (tid != kStCons) return;
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_in)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tm_val)) : "memory");
         const uint64_t pol_keep = pol_of(P.ypol);    // Y_j rows: re-staged by the neighbouring patches
         const uint64_t pol_once = pol_of(P.spol);    // Y_{j-1}, X, DIA: read once
-        const uint32_t boxline = (uint32_t)P.box_x * pwv * 16u, pline = (uint32_t)P.Px * pwv * 16u;
-        uint32_t step = 0;
-        // work items: static (it += G) or, dyn, in order from the atomic ticket (the items in
-        // flight stay one contiguous window: neighbouring patches run together and their
-        // shared halo lines are fetched from DRAM once)
+        const uint32_t box_b = (uint32_t)P.box_x * P.box_y * pwv * 16u;
+        const uint32_t row_b = (uint32_t)P.Px * P.Py * pwv * 16u;
+        const uint32_t val_b = vplane_bytes(P.Px, P.Py, P.Kpad);
+        const uint32_t st0 = smem_u32(stages), vr0 = smem_u32(vring), fb0 = smem_u32(full);
+        int b = 0;
+        uint32_t eph = 0;   // parity of the empty-barrier phase to wait for (from the second round on)
+        bool wrapped = false;
+        int vs = 0;         // ring slot of the current step's plane
         const bool dyn = !SUMSQ && P.dyn;
         for (int64_t it = blockIdx.x; it < P.nitems;) {
             const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
             const int col0 = I.panel * pwv * 2;  // first column of the panel
             const int zs = max(I.zc0 - 1, 0);
-            for (int z = zs; z <= I.zc1; ++z, ++step) {
-                const int b = (int)(step % NS);
-                if (step >= (uint32_t)NS) mbar_wait(empty + b, ((step / NS) - 1) & 1);
-                if (z == zs && lane == 0) meta[b] = it;
+            for (int z = zs; z <= I.zc1; ++z) {
+                if (wrapped) mbar_wait(empty + b, eph);
                 const bool real = z < P.nz;
                 const bool fin = z - 1 >= I.zc0;
                 // DIA planes to load: z+1 (and z on the first step when z is an output plane)
                 const int va0 = (z == zs && z >= I.zc0 && real) ? z : z + 1;
                 const int va1 = (z + 1 < I.zc1) ? z + 1 : z;  // inclusive; empty if va1 < va0
-                // job list: [0, box_y) box lines, [box_y, box_y + Py) prev lines,
-                // then X lines, then DIA lines (plane va0 .. va1, Py each)
-                const int nbl = real ? P.box_y : 0;
-                const int npl = (fin && HAS_PREV) ? I.pye : 0;
-                const int nxl = (fin && HAS_X) ? I.pye : 0;
-                const int nvl = va1 >= va0 ? (va1 - va0 + 1) * I.pye : 0;
-                uint32_t total = 0;
-                for (int ly = 0; ly < nbl; ++ly) {
-                    const int gy = I.y0 - P.hy + ly;
-                    const bool yh = P.plus && (ly < P.hy || ly >= P.hy + P.Py);  // a y-halo line: Px rows
-                    if (gy >= 0 && gy < P.ny) total += yh ? pline : boxline;
+                const int nv = va1 >= va0 ? va1 - va0 + 1 : 0;
+                const uint32_t total = (real ? box_b : 0u) + (fin ? (HAS_PREV ? row_b : 0u) + (HAS_X ? row_b : 0u) : 0u) +
+                                       (uint32_t)nv * val_b;
+                if (z == zs) meta[b] = it;
+                const uint32_t fb = fb0 + 8u * b;
+                mbar_expect_tx(full + b, total);
+                const uint32_t st = st0 + (uint32_t)b * SL.bytes;
+                if (real) tma_4d(st + SL.box, &P.tm_in, col0, I.x0 - P.hx, I.y0 - P.hy, z, fb, pol_keep);
+                if (fin) {
+                    if (HAS_PREV) tma_4d(st + SL.prev, &P.tm_prev, col0, I.x0, I.y0, z - 1, fb, pol_once);
+                    if (HAS_X) tma_4d(st + SL.xa, &P.tm_xa, col0, I.x0, I.y0, z - 1, fb, pol_once);
                 }
-                total += (uint32_t)(npl + nxl) * pline + (uint32_t)nvl * (uint32_t)P.Px * P.Kpad * 8u;
-                if (lane == 0) mbar_expect_tx(full + b, total);
-                __syncwarp();
-                unsigned char *st = stages + (size_t)b * SL.bytes;
-                const int njobs = nbl + npl + nxl + nvl;
-                for (int j = lane; j < njobs; j += 32) {
-                    if (j < nbl) {
-                        const int gy = I.y0 - P.hy + j;
-                        if (gy < 0 || gy >= P.ny) continue;
-                        ARR_CHECK(SL.box + (size_t)(j + 1) * boxline <= SL.prev);
-                        if (P.plus && (j < P.hy || j >= P.hy + P.Py)) {
-                            // the 7-point stencil reads no corner of the box: rows x0 .. x0+Px-1 only
-                            const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + I.x0;
-                            tma_2d(st + SL.box + (size_t)j * boxline + (size_t)P.hx * pwv * 16, &P.tm_in_px, col0,
-                                   (int)row, full + b, pol_keep);
-                        } else {
-                            const int64_t row = ((int64_t)z * P.ny + gy) * P.nx + (I.x0 - P.hx);
-                            tma_2d(st + SL.box + (size_t)j * boxline, &P.tm_in, col0, (int)row, full + b, pol_keep);
-                        }
-                    } else if (j < nbl + npl + nxl) {
-                        const int jj = j - nbl;
-                        const bool isx = jj >= npl;
-                        const int oy = isx ? jj - npl : jj;
-                        ARR_CHECK((size_t)(oy + 1) * pline <= (isx ? SL.bytes - SL.xa : SL.xa - SL.prev));
-                        const int64_t row = ((int64_t)(z - 1) * P.ny + I.y0 + oy) * P.nx + I.x0;
-                        if (HAS_PREV && !isx) tma_2d(st + SL.prev + (size_t)oy * pline, &P.tm_prev, col0, (int)row, full + b, pol_once);
-                        if (HAS_X && isx) tma_2d(st + SL.xa + (size_t)oy * pline, &P.tm_xa, col0, (int)row, full + b, pol_once);
-                    } else {
-                        const int jj = j - nbl - npl - nxl;
-                        const int zz = va0 + jj / I.pye, oy = jj - (jj / I.pye) * I.pye;
-                        unsigned char *slot = vring + (size_t)((step + (uint32_t)(zz - z)) % VS) * slot_bytes;
-                        ARR_CHECK((size_t)oy * vlb + (size_t)P.Px * P.Kpad * 8 <= slot_bytes && oy < P.Py);
-                        const int64_t row = ((int64_t)zz * P.ny + I.y0 + oy) * P.nx + I.x0;
-                        tma_2d(slot + (size_t)oy * vlb, &P.tm_val, 0, (int)row, full + b, pol_once);
-                    }
+                for (int zz = va0; zz <= va1; ++zz) {
+                    int sl = vs + (zz - z);
+                    if (sl >= VS) sl -= VS;
+                    tma_4d(vr0 + (uint32_t)sl * slot_bytes, &P.tm_val, 0, I.x0, I.y0, zz, fb, pol_once);
                 }
-                // L2 prefetch of step z + PF's boxes (same item)
-                const int zp = z + P.pf;
-                if (P.pf > 0 && zp <= I.zc1) {
-                    const bool preal = zp < P.nz, pfin = zp - 1 >= I.zc0;
-                    const int pnb = preal ? P.box_y : 0, pnp = (pfin && (HAS_PREV || HAS_X)) ? I.pye : 0;
-                    const int pnv = (zp + 1 < I.zc1) ? I.pye : 0;
-                    for (int j = lane; j < pnb + pnp + pnv; j += 32) {
-                        if (j < pnb) {
-                            const int gy = I.y0 - P.hy + j;
-                            if (gy < 0 || gy >= P.ny) continue;
-                            tma_2d_prefetch(&P.tm_in, col0, (int)(((int64_t)zp * P.ny + gy) * P.nx + (I.x0 - P.hx)));
-                        } else if (j < pnb + pnp) {
-                            const int oy = j - pnb;
-                            const int row = (int)(((int64_t)(zp - 1) * P.ny + I.y0 + oy) * P.nx + I.x0);
-                            if (HAS_PREV) tma_2d_prefetch(&P.tm_prev, col0, row);
-                            if (HAS_X) tma_2d_prefetch(&P.tm_xa, col0, row);
-                        } else {
-                            const int oy = j - pnb - pnp;
-                            tma_2d_prefetch(&P.tm_val, 0, (int)(((int64_t)(zp + 1) * P.ny + I.y0 + oy) * P.nx + I.x0));
-                        }
-                    }
+                if (++b == NS) {
+                    b = 0;
+                    if (wrapped) eph ^= 1u;
+                    wrapped = true;
                 }
+                if (++vs == VS) vs = 0;
             }
-            if (dyn) {
-                int64_t nx = 0;
-                if (lane == 0) nx = G + (int64_t)atomicAdd(P.sched, 1ull);
-                it = __shfl_sync(0xffffffffu, nx, 0);
-            } else {
-                it += G;
-            }
+            if (dyn) it = G + (int64_t)atomicAdd(P.sched, 1ull);
+            else it += G;
         }
         // end of work: one more stage carrying meta = -1 (no bytes)
-        {
-            const int b = (int)(step % NS);
-            if (step >= (uint32_t)NS) mbar_wait(empty + b, ((step / NS) - 1) & 1);
-            if (lane == 0) {
-                meta[b] = -1;
-                mbar_arrive(full + b);
-            }
-        }
-        if (dyn && lane == 0) {
+        if (wrapped) mbar_wait(empty + b, eph);
+        meta[b] = -1;
+        mbar_arrive(full + b);
+        if (dyn) {
             // the last CTA to finish resets the ticket for the next launch
             __threadfence();
             if (atomicAdd(P.sched + 1, 1ull) == (unsigned long long)G - 1) {
@@ -414,13 +344,16 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     // ---------------------------------------------------------------- consumers
     const uint64_t pols = pol_of(P.opol);
     const int Kp = P.Kpad;
-    uint32_t step = 0;
+    int b = 0;
+    uint32_t fph = 0;   // parity of the full-barrier phase of stage b
+    int vs = 0;         // ring slot of the current step's plane (as the producer's)
     double ss0 = 0.0, ss1 = 0.0;
     int panel_of_cta = (int)(blockIdx.x % P.npan);
+    const int64_t nxy = (int64_t)P.nx * P.ny;
     for (;;) {
         // the next item is named by the stage of its first step
-        mbar_wait(full + (int)(step % NS), (step / NS) & 1);
-        const int64_t it = meta[(int)(step % NS)];
+        mbar_wait(full + b, fph);
+        const int64_t it = meta[b];
         if (it < 0) break;
         const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
         const int pw = min(pwv, P.wv - I.panel * pwv);
@@ -433,6 +366,7 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         const int cb = (oy + P.hy) * P.box_x + (ox + P.hx);
         const int rs = oy * P.Px + ox;  // patch row slot (prev / X rows)
         const int64_t rxy = (int64_t)(I.y0 + oy) * P.nx + (I.x0 + ox);
+        const uint32_t vo = (uint32_t)rs * Kp * 8u;  // this row's DIA entries within a ring slot
         // smem row of each in-plane position (the centre where the neighbour is outside
         // the grid: its DIA slot is zero there)
         int qoff[Sh::NQ];
@@ -442,29 +376,30 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
             const bool in = gx >= 0 && gx < P.nx && gy >= 0 && gy < P.ny;
             qoff[q] = (in ? cb + Sh::dy(q) * P.box_x + Sh::dx(q) : cb) * pwv + v;
         }
+        double *outp = P.Yout + (rxy + (int64_t)I.zc0 * nxy) * P.ld_out + (int64_t)(colv0 + v) * 2;
+        const int64_t out_step = nxy * P.ld_out;
         double2 accA = make_double2(0.0, 0.0), accB = make_double2(0.0, 0.0), yiA = make_double2(0.0, 0.0);
         const int zs = max(I.zc0 - 1, 0);
-        for (int z = zs; z <= I.zc1; ++z, ++step) {
-            const int b = (int)(step % NS);
+        for (int z = zs; z <= I.zc1; ++z) {
             const bool real = z < P.nz;
             const bool fin = z - 1 >= I.zc0;                // out(z-1) completes in this step
             const bool mid = z >= I.zc0 && z < I.zc1;       // out(z) gets its plane-z terms
             const bool nxt = z + 1 < I.zc1;                 // out(z+1) starts with its plane-z terms
-            mbar_wait(full + b, (step / NS) & 1);
+            mbar_wait(full + b, fph);
             const unsigned char *st = stages + (size_t)b * SL.bytes;
             const double2 *S = reinterpret_cast<const double2 *>(st + SL.box);
             double2 accC = make_double2(0.0, 0.0), yiB = make_double2(0.0, 0.0);
             double2 yp = make_double2(0.0, 0.0), xa = make_double2(0.0, 0.0);
             if (act) {
                 if (real) {
-                    const size_t vo = (size_t)oy * vlb + (size_t)ox * Kp * 8;
+                    const int sp = vs == 0 ? VS - 1 : vs - 1, sn = vs + 1 == VS ? 0 : vs + 1;
                     ARR_CHECK(vo + (size_t)Sh::K * 8 <= slot_bytes);
-                    const double *vp = reinterpret_cast<const double *>(vring + (size_t)((step + VS - 1) % VS) * slot_bytes + vo);
-                    const double *v0 = reinterpret_cast<const double *>(vring + (size_t)(step % VS) * slot_bytes + vo);
-                    const double *vm = reinterpret_cast<const double *>(vring + (size_t)((step + 1) % VS) * slot_bytes + vo);
+                    const double *vp = reinterpret_cast<const double *>(vring + (size_t)sp * slot_bytes + vo);
+                    const double *v0 = reinterpret_cast<const double *>(vring + (size_t)vs * slot_bytes + vo);
+                    const double *vm = reinterpret_cast<const double *>(vring + (size_t)sn * slot_bytes + vo);
 #pragma unroll
                     for (int q = 0; q < Sh::NQ; ++q) {
-                        ARR_CHECK(qoff[q] >= 0 && qoff[q] < nbox * pwv);
+                        ARR_CHECK(qoff[q] >= 0 && qoff[q] < P.box_x * P.box_y * pwv);
                         const double2 y = S[qoff[q]];
                         if (q == Sh::QC) yiB = y;
                         if (Sh::k(1, q) >= 0 && fin) fma2(accA, vp[Sh::k(1, q)], y);    // row z-1: its dz = +1 terms
@@ -480,8 +415,9 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
             }
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive(empty + b);  // this warp is done with stage b
+            if (++b == NS) { b = 0; fph ^= 1u; }
+            if (++vs == VS) vs = 0;
             if (fin && act) {
-                const int64_t row = (int64_t)(z - 1) * nxy + rxy;
                 double2 out;
                 out.x = epi(P.alpha, accA.x, P.shift, yiA.x);
                 out.y = epi(P.alpha, accA.y, P.shift, yiA.y);
@@ -497,8 +433,9 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                     ss0 = fma(out.x, out.x, ss0);
                     ss1 = fma(out.y, out.y, ss1);
                 }
-                st_stream(P.Yout + row * P.ld_out + (int64_t)(colv0 + v) * 2, out, pols);
+                st_stream(outp, out, pols);
             }
+            if (fin) outp += out_step;
             accA = accB;
             accB = accC;
             yiA = yiB;
@@ -590,21 +527,18 @@ int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
     constexpr int kStCons = StCta<NT>::CONS, kStThreads = NT;
     auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X, NT>;
     const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
-    const size_t ring = (size_t)(L.NS + 2) * L.Py * vline_bytes(L.Px, L.Kpad);
+    const size_t ring = (size_t)(L.NS + 2) * vslot_bytes(L.Px, L.Py, L.Kpad);
     const size_t smem = 256 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
     static LaunchCache cache;
     const int occ = cached_occupancy(cache, kern, kStThreads, smem);
     int64_t G = (int64_t)c->num_sms * occ;
     static const int pm_env = [] { const char *e = getenv("ARRABIT_ST_ORDER"); return e ? atoi(e) : 1; }();
-    // L2 prefetch ahead of the loads measured slower on B200 (cfg3 3.32 -> 4.27 ms per degree): off
-    static const int pf_env = [] { const char *e = getenv("ARRABIT_ST_PF"); return e ? atoi(e) : 0; }();
     // L2 policies (0 evict_normal, 1 evict_last, 2 evict_first) of the Y_j boxes, the once-read
     // operands (Y_{j-1}, X, DIA) and the output stores
     static const int ypol = [] { const char *e = getenv("ARRABIT_ST_YPOL"); return e ? atoi(e) : 1; }();
     static const int spol = [] { const char *e = getenv("ARRABIT_ST_SPOL"); return e ? atoi(e) : 2; }();
     static const int opol = [] { const char *e = getenv("ARRABIT_ST_OPOL"); return e ? atoi(e) : 2; }();
     L.ypol = ypol; L.spol = spol; L.opol = opol;
-    L.pf = pf_env;
     static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
     if (verbose)
         fprintf(stderr, "stencil plan: shape %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu dyn %d\n",
@@ -661,17 +595,18 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
     return fn;
 }
 
-// 2-D fp64 tensor map over a row-major block: cols x rows, row stride ld doubles, box
-// {box_cols, box_rows}; out-of-range elements are zero-filled.
-bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, int64_t ld, int box_cols,
-               int box_rows) {
+// 4-D fp64 tensor map (columns, x, y, z) over a row-major n x (.) block of an nx x ny x nz
+// grid (row = x + nx (y + ny z)), row stride ld doubles; box {box_cols, box_x, box_y, 1};
+// out-of-range coordinates are zero-filled.
+bool encode_4d(CUtensorMap *m, const double *base, int64_t cols, int64_t ld, int64_t nx, int64_t ny, int64_t nz,
+               int box_cols, int box_x, int box_y) {
     auto enc = tensor_encoder();
     if (!enc) return false;
-    const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    const cuuint64_t gstride[1] = {(cuuint64_t)ld * 8};
-    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-    const cuuint32_t estr[2] = {1, 1};
-    // no L2 promotion: rows are only 16-byte aligned (ld = w), and promoting a box row's
+    const cuuint64_t gdim[4] = {(cuuint64_t)cols, (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    const cuuint64_t gstride[3] = {(cuuint64_t)ld * 8, (cuuint64_t)(ld * nx) * 8, (cuuint64_t)(ld * nx * ny) * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)box_cols, (cuuint32_t)box_x, (cuuint32_t)box_y, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    // no L2 promotion: a box row is a column panel's segment of a grid row; promoting its
     // sectors to 128/256-byte blocks would fetch the neighbouring panel's bytes too
     static const CUtensorMapL2promotion promo = [] {
         const char *e = getenv("ARRABIT_ST_PROMO");
@@ -680,7 +615,7 @@ bool encode_2d(CUtensorMap *m, const double *base, int64_t cols, int64_t rows, i
                         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                    : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     }();
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim, gstride, box, estr,
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), gdim, gstride, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
 }
@@ -713,13 +648,11 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 if (Px > S.nx || Py > S.ny) break;
                 const int bx = Px + 2 * hx, by = Py + 2 * hy;
                 const size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
-                const size_t slot = (size_t)Py * (((size_t)Px * S.Kpad * 8 + 127) & ~(size_t)127);
+                const size_t slot = vslot_bytes(Px, Py, S.Kpad);
                 int NS = 4;
                 while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
                 if (NS < 2) continue;
-                // staged rows: whole box lines (one TMA box per line); plus-shaped: the y-halo
-                // lines without their corners
-                const int need = bx * by - ((S.shape == 1 && st_plus()) ? 2 * hy * 2 * hx : 0);
+                const int need = bx * by;  // staged rows: the whole box (one TMA box per plane)
                 const int npx = (S.nx + Px - 1) / Px, npy = (S.ny + Py - 1) / Py;
                 const double rag = (double)S.nx * S.ny / ((double)npx * Px * npy * Py);
                 // z-chunks: enough work items for >= ~12 per CTA, chunks of >= 8 planes
@@ -772,19 +705,17 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     if (a.Xa && !al16(a.Xa, a.ld_xa)) return -1;
     StencilLaunch L{};
     if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L)) return -1;
-    L.plus = (c->st.shape == 1 && L.hy > 0 && st_plus()) ? 1 : 0;
     L.Yin = a.Yin; L.ld_in = a.ld_in;
     L.Yprev = a.Yprev; L.ld_prev = a.ld_prev;
     L.Yout = a.Yout; L.ld_out = a.ld_out;
     L.Xa = a.Xa; L.ld_xa = a.ld_xa;
     L.alpha = a.alpha; L.shift = a.shift; L.beta = a.beta; L.gxa = a.gxa;
     L.partials = a.partials;
-    const int64_t nrows = c->A.n;
-    if (!encode_2d(&L.tm_in, a.Yin, a.w, nrows, a.ld_in, 2 * L.pwv, L.box_x) ||
-        !encode_2d(&L.tm_val, c->st.dia, c->st.Kpad, nrows, c->st.Kpad, c->st.Kpad, L.Px) ||
-        (L.plus && !encode_2d(&L.tm_in_px, a.Yin, a.w, nrows, a.ld_in, 2 * L.pwv, L.Px)) ||
-        (a.Yprev && !encode_2d(&L.tm_prev, a.Yprev, a.w, nrows, a.ld_prev, 2 * L.pwv, L.Px)) ||
-        (a.Xa && !encode_2d(&L.tm_xa, a.Xa, a.w, nrows, a.ld_xa, 2 * L.pwv, L.Px)))
+    const StencilState &S = c->st;
+    if (!encode_4d(&L.tm_in, a.Yin, a.w, a.ld_in, S.nx, S.ny, S.nz, 2 * L.pwv, L.box_x, L.box_y) ||
+        !encode_4d(&L.tm_val, S.dia, S.Kpad, S.Kpad, S.nx, S.ny, S.nz, S.Kpad, L.Px, L.Py) ||
+        (a.Yprev && !encode_4d(&L.tm_prev, a.Yprev, a.w, a.ld_prev, S.nx, S.ny, S.nz, 2 * L.pwv, L.Px, L.Py)) ||
+        (a.Xa && !encode_4d(&L.tm_xa, a.Xa, a.w, a.ld_xa, S.nx, S.ny, S.nz, 2 * L.pwv, L.Px, L.Py)))
         return -1;
     const bool prev = a.Yprev != nullptr, ss = a.partials != nullptr, xa = a.Xa != nullptr;
     switch (c->st.shape) {
