@@ -134,12 +134,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def filter_bytes_per_degree(n, nnz, w, d, K=0):
+def filter_bytes_per_degree(n, nnz, w, d, abytes=None):
     """Algorithmic bytes of one filter-degree launch: A once, read Y_j,
     read Y_{j-1}, write Y_{j+1} (24 n w); the first degree has no Y_{j-1} (16 n w).
-    A is 12 nnz + 8(n+1) bytes as CSR, 8 K n as the stencil path's K diagonals.
-    Averaged over the d launches of a sweep."""
-    a = 8 * K * n if K else 12 * nnz + 8 * (n + 1)
+    A is 12 nnz + 8(n+1) bytes as CSR; on the stencil path `abytes` per row (8 K for the
+    K diagonals, 8 for the diagonal of a constant-off-diagonal operator, 0 when every
+    coefficient is constant: eig_stencil_abytes).  Averaged over the d launches of a sweep."""
+    a = abytes * n if abytes is not None and abytes >= 0 else 12 * nnz + 8 * (n + 1)
     return (a + 16 * n * w + (d - 1) * (a + 24 * n * w)) / d
 
 
@@ -158,7 +159,7 @@ def stencil_grid(spec):
 def use_stencil(spec, args):
     if args.spmm == "csr" or stencil_grid(spec) is None:
         return False
-    return args.spmm == "stencil" or spec.kind in ("lap3dV", "st27")
+    return args.spmm == "stencil" or spec.kind in ("lap1d", "lap2d", "lap3dV", "st27")
 
 
 def config_dict(spec, A, args):
@@ -322,7 +323,7 @@ def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps,
     path = "csr"
     if not partitioned and use_stencil(spec, args):
         ctx.eig_set_stencil(*stencil_grid(spec))
-        path = f"stencil ({ctx.stencil_points}-point DIA)"
+        path = f"stencil ({ctx.stencil_points}-point, A {ctx.stencil_abytes} B/row)"
     elif not partitioned and spec.kind in ("lap3dV", "st27"):
         from paper_1507_06078_b200 import schedule
         by, tile = {"lap3dV": (10, 16), "st27": (8, 32)}[spec.kind]
@@ -370,6 +371,7 @@ def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps,
     kernel = ctx.last_spmm_kernel
     return dict(ctx=ctx, step_ms=step_ms, infos=infos, clocks=clocks, launches=launches, phase_ms=phase_ms,
                 phase_cnt=phase_cnt, kernel=kernel, path=path, lean=ctx_lean, stencil_K=ctx.stencil_points,
+                stencil_abytes=ctx.stencil_abytes if ctx.stencil_points else None,
                 eigenvalues=ev)
 
 
@@ -390,7 +392,7 @@ def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
     peak, peak_src = load_peaks()
     w = spec.w if w is None else w  # the filtered width on this rank (the column split filters w_r columns)
     deg_ms = r["phase_ms"][0] / max(1, r["phase_cnt"][0])
-    bpl = filter_bytes_per_degree(nrow, nnz, w, spec.d, r["stencil_K"])
+    bpl = filter_bytes_per_degree(nrow, nnz, w, spec.d, r["stencil_abytes"])
     if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
         bpl += 8 * nrow * w
     achieved = bpl / (deg_ms / 1000.0) / 1e9
@@ -408,8 +410,9 @@ def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
     pm, st = r["phase_ms"], sum(r["step_ms"])
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "kernel": r["kernel"],
-            "bytes_per_launch": bpl, "bytes_model": ("8 K n (DIA) + 24 n w" if r["stencil_K"] else
-                                                     "12 nnz + 8(n+1) + 24 n w") + " (16 n w on a sweep's first degree)",
+            "bytes_per_launch": bpl, "bytes_model": (
+                {None: "12 nnz + 8(n+1)", 0: "0 (all coefficients constant)", 8: "8 n (diagonal; constant off-diagonals)"}.get(
+                    r["stencil_abytes"], "8 K n (K diagonals)") + " + 24 n w (16 n w on a sweep's first degree)"),
             "avg_launch_us": deg_ms * 1000.0, "launches": int(r["phase_cnt"][0]), "peak_source": peak_src,
             "frac_of_8TBs": achieved / 8000.0, "share_of_step": pm[0] / st,
             "phase_ms_per_step": {"filter_degrees": pm[0] / steps, "arr_project": pm[1] / steps,

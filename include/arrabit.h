@@ -249,6 +249,13 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
 arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
 /* K of the active stencil path (0 = the CSR kernels). */
 int32_t eig_stencil_active(const arr_ctx *c);
+/* Bytes of A the stencil path reads per row and column panel: eig_set_stencil detects
+ * constant coefficients (every neighbour slot's value the same on all rows whose neighbour
+ * is in the grid, as in the finite-difference operators of P:1624-1627) and then keeps
+ * only the diagonal (8 bytes per row; needs nx even) or nothing (0: all coefficients
+ * constant, the operator applied matrix-free); otherwise the K diagonals (8 K).  -1 when
+ * no stencil is active.  ARRABIT_ST_VMODE=0 forces the K diagonals. */
+int32_t eig_stencil_abytes(const arr_ctx *c);
 /* Name of the kernel the context's last fused SpMM launched (static string; "" if none). */
 const char *eig_last_spmm_kernel(const arr_ctx *c);
 /* Change the degree d used by filter_step (1 <= d). */

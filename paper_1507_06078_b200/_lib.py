@@ -18,7 +18,7 @@ EXPORTED = [
     "eig_init", "eig_init_w", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "eig_set_filter", "eig_set_mode", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
-    "eig_set_timing", "eig_phase_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active", "eig_last_spmm_kernel",
+    "eig_set_timing", "eig_phase_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active", "eig_stencil_abytes", "eig_last_spmm_kernel",
     "eig_init_dist", "eig_init_colsplit", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
 ]
 
@@ -89,6 +89,7 @@ def load(path: str | None = None):
         "eig_set_degree": ([vp, i32], ctypes.c_int),
         "eig_set_stencil": ([vp, i64, i64, i64], ctypes.c_int),
         "eig_stencil_active": ([vp], ctypes.c_int32),
+        "eig_stencil_abytes": ([vp], ctypes.c_int32),
         "eig_last_spmm_kernel": ([vp], ctypes.c_char_p),
         "eig_set_filter": ([vp, i32], ctypes.c_int),
         "eig_set_mode": ([vp, i32], ctypes.c_int),

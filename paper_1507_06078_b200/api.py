@@ -233,6 +233,11 @@ class EigContext:
         """K of the active stencil path (0: CSR kernels)."""
         return int(self.lib.eig_stencil_active(self.h))
 
+    @property
+    def stencil_abytes(self) -> int:
+        """Bytes of A per row the stencil path reads (8 K, 8 or 0; -1: no stencil)."""
+        return int(self.lib.eig_stencil_abytes(self.h))
+
     def eig_set_degree(self, d: int):
         self._check(self.lib.eig_set_degree(self.h, int(d)), "eig_set_degree")
         self.d = d

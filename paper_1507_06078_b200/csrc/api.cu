@@ -1326,6 +1326,12 @@ int32_t eig_stencil_active(const arr_ctx *c) {
     if (c && c->cs) return eig_stencil_active(c->cs->col);
     return c && c->st.on ? c->st.K : 0;
 }
+
+int32_t eig_stencil_abytes(const arr_ctx *c) {
+    if (c && c->cs) return eig_stencil_abytes(c->cs->col);
+    if (!c || !c->st.on) return -1;
+    return c->st.vmode == 0 ? 8 * c->st.K : (c->st.vmode == 1 ? 8 : 0);
+}
 const char *eig_last_spmm_kernel(const arr_ctx *c) {
     if (c && c->cs) return eig_last_spmm_kernel(c->cs->col);
     return c && c->last_kernel ? c->last_kernel : "";

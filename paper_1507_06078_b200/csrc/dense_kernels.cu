@@ -786,8 +786,20 @@ __global__ void __launch_bounds__(DCfg<BM, BN, WTM, WTN, KSX, SS, MINB>::THREADS
             }
 }
 
+// Tile variant of the GEMMs (ARRABIT_DMMA_TILE, default 0: the 64 x 64 cp.async kernels) and of
+// the Grams (ARRABIT_DMMA_GRAM, default 7: 64 x 64, 4 stages, software-pipelined; measured on
+// B200 at the ARR shapes: +2-10% over variant 0, profiles/r02/dmma_pipelined_variants.log)
 int dmma_tile_choice() {
     static const int t = [] { const char *e = getenv("ARRABIT_DMMA_TILE"); return e ? atoi(e) : 0; }();
+    return t;
+}
+int gram_tile_choice() {
+    static const int t = [] {
+        const char *e = getenv("ARRABIT_DMMA_GRAM");
+        if (e) return atoi(e);
+        const char *g = getenv("ARRABIT_DMMA_TILE");
+        return g ? atoi(g) : 7;
+    }();
     return t;
 }
 
@@ -937,7 +949,7 @@ inline unsigned nblk(int64_t total, int threads) { return (unsigned)((total + th
 // rows each.  sym: only the upper tiles do work.
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
     VarInfo vi{TILE, TILE, 0};
-    const bool var = dmma_tile_choice() > 0 && variant_info(dmma_tile_choice(), vi);
+    const bool var = gram_tile_choice() > 0 && variant_info(gram_tile_choice(), vi);
     const int TM = vi.BM, TN = vi.BN;
     const int64_t ta = (m1 + TM - 1) / TM, tb = (m2 + TN - 1) / TN;
     // symmetric: tiles on or above the diagonal (tile b intersects columns >= the tile's first row)
@@ -988,8 +1000,8 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     rps = (rps + KS - 1) / KS * KS;
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
 #if ARR_DMMA_CA
-    if (dmma_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(Y, ldy) &&
-        gram_variant(dmma_tile_choice(), c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials)) {
+    if (gram_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(Y, ldy) &&
+        gram_variant(gram_tile_choice(), c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials)) {
     } else if (ca_ok(X, ldx) && ca_ok(Y, ldy)) {
         const size_t smem = sizeof(double) * 2 * S_CA * KS * (TILE + PAD);
         static LaunchCache cache;

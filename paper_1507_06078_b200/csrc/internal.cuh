@@ -77,7 +77,11 @@ struct StencilState {
     bool on = false;
     int64_t nx = 0, ny = 0, nz = 0;
     int K = 0, Kpad = 0;
-    double *dia = nullptr;  // [n][Kpad] (K rounded up to even: 16-byte rows), owned
+    double *dia = nullptr;  // vmode 0: [n][Kpad] (K rounded up to even: 16-byte rows); vmode 1: the diagonal [n]; owned
+    // value mode: 0 = K diagonals (DIA); 1 = constant off-diagonal coefficients coef[slot] and
+    // the diagonal per row; 2 = every coefficient constant (no matrix bytes at all)
+    int vmode = 0;
+    double coef[27] = {};
     int shape = 0, hx = 0, hy = 0;  // stencil_kernels.cu Shape<>: 0 27-pt, 1 7-pt, 2 2-D 5-pt, 3 1-D 3-pt
     int smem_optin = 0;
 };
@@ -90,6 +94,8 @@ struct StencilLaunch {
     double alpha, shift, beta, gxa;
     double *partials;
     const double *val;
+    double coef[27];  // constant coefficients by DIA slot (vmode 1: off-diagonal slots; vmode 2: all)
+    int vmode, Pxe;   // value mode (StencilState); the diagonal's box width (Px rounded up to even)
     int64_t nitems;
     int w, wv, K, Kpad;
     int nx, ny, nz;

@@ -27,30 +27,27 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "internal.cuh"
 
 namespace {
 
-// CTA sizes: NT = 1024 (31 consumer warps, one output vector each per step, + 1 producer
-// warp; one CTA per SM) or 512 (15 + 1; two CTAs per SM, two independent pipelines)
+// One CTA per SM: 31 consumer warps (one output vector each per step) + 1 producer warp
 template <int NT>
 struct StCta {
-    static constexpr int THREADS = NT, CONS = NT - 32, MINB = NT >= 1024 ? 1 : 2;
+    static constexpr int THREADS = NT, CONS = NT - 32, MINB = 1;
 };
-int st_threads() {
-    static const int t = [] { const char *e = getenv("ARRABIT_ST_THREADS"); return e && atoi(e) == 512 ? 512 : 1024; }();
-    return t;
-}
+constexpr int kStThreads = 1024;
 
 // work items from the atomic ticket in launches without column sums (ARRABIT_ST_DYN=0: static)
 int st_dyn() {
     static const int v = [] { const char *e = getenv("ARRABIT_ST_DYN"); return e ? atoi(e) : 1; }();
     return v;
 }
-// z-chunks per column of patches under the ticket (ARRABIT_ST_NZC; 0 = the static rule)
+// z-chunks per column of patches under the ticket (ARRABIT_ST_NZC; 0 = automatic)
 int st_nzc() {
-    static const int v = [] { const char *e = getenv("ARRABIT_ST_NZC"); return e ? atoi(e) : 1; }();
+    static const int v = [] { const char *e = getenv("ARRABIT_ST_NZC"); return e ? atoi(e) : 0; }();
     return v;
 }
 
@@ -218,14 +215,17 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
 // val ring: VS = NS + 2 slots, one plane of the patch's DIA rows (Py lines x Px rows x Kpad)
 template <bool HAS_PREV, bool HAS_X>
 struct StageLayout {
-    uint32_t box, prev, xa, bytes;
-    __host__ __device__ StageLayout(int nbox, int nrow_max, int pwv) {
+    uint32_t box, prev, xa, dg, bytes;
+    // dg_bytes: the diagonal of the patch's plane (value mode 1), 0 otherwise
+    __host__ __device__ StageLayout(int nbox, int nrow_max, int pwv, uint32_t dg_bytes = 0) {
         box = 0;
         prev = (uint32_t)nbox * pwv * 16u;
         xa = prev + (HAS_PREV ? (uint32_t)nrow_max * pwv * 16u : 0u);
-        bytes = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
+        dg = xa + (HAS_X ? (uint32_t)nrow_max * pwv * 16u : 0u);
+        bytes = dg + ((dg_bytes + 127u) & ~127u);
     }
 };
+__host__ __device__ inline uint32_t vdiag_bytes(int Pxe, int Py) { return (uint32_t)Pxe * Py * 8u; }
 // one DIA plane of a patch (the TMA box's bytes) and its ring slot (128-byte aligned)
 __host__ __device__ inline uint32_t vplane_bytes(int Px, int Py, int Kpad) { return (uint32_t)Px * Py * Kpad * 8u; }
 __host__ __device__ inline uint32_t vslot_bytes(int Px, int Py, int Kpad) { return (vplane_bytes(Px, Py, Kpad) + 127u) & ~127u; }
@@ -241,7 +241,20 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap *map, int
         : "memory");
 }
 
-template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT>
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap *map, int x, int y, int z, uint32_t bar,
+                                       uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+// VM: value mode (StencilState::vmode): 0 the K diagonals staged per plane (ring of NS + 2
+// planes: the dz = +1 / 0 / -1 terms of one staged Y_j plane need the DIA rows of planes
+// z - 1, z, z + 1); 1 constant off-diagonal coefficients (kernel parameters) and the
+// diagonal of plane z staged with the plane's box; 2 all coefficients constant.
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT, int VM>
 __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __grid_constant__ StencilLaunch P) {
     using Sh = Shape<SH>;
     constexpr int kStCons = StCta<NT>::CONS;
@@ -255,8 +268,9 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     unsigned char *stages = sm + 128;
     const int tid = threadIdx.x;
     const int NS = P.NS, VS = P.NS + 2;
-    const StageLayout<HAS_PREV, HAS_X> SL(P.box_x * P.box_y, P.Px * P.Py, P.pwv);
-    const uint32_t slot_bytes = vslot_bytes(P.Px, P.Py, P.Kpad);
+    const StageLayout<HAS_PREV, HAS_X> SL(P.box_x * P.box_y, P.Px * P.Py, P.pwv,
+                                           VM == 1 ? vdiag_bytes(P.Pxe, P.Py) : 0u);
+    const uint32_t slot_bytes = VM == 0 ? vslot_bytes(P.Px, P.Py, P.Kpad) : 0u;
     unsigned char *vring = stages + (size_t)NS * SL.bytes;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -281,7 +295,8 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         const uint64_t pol_once = pol_of(P.spol);    // Y_{j-1}, X, DIA: read once
         const uint32_t box_b = (uint32_t)P.box_x * P.box_y * pwv * 16u;
         const uint32_t row_b = (uint32_t)P.Px * P.Py * pwv * 16u;
-        const uint32_t val_b = vplane_bytes(P.Px, P.Py, P.Kpad);
+        const uint32_t val_b = VM == 0 ? vplane_bytes(P.Px, P.Py, P.Kpad) : 0u;
+        const uint32_t dg_b = VM == 1 ? vdiag_bytes(P.Pxe, P.Py) : 0u;
         const uint32_t st0 = smem_u32(stages), vr0 = smem_u32(vring), fb0 = smem_u32(full);
         int b = 0;
         uint32_t eph = 0;   // parity of the empty-barrier phase to wait for (from the second round on)
@@ -299,19 +314,20 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                 // DIA planes to load: z+1 (and z on the first step when z is an output plane)
                 const int va0 = (z == zs && z >= I.zc0 && real) ? z : z + 1;
                 const int va1 = (z + 1 < I.zc1) ? z + 1 : z;  // inclusive; empty if va1 < va0
-                const int nv = va1 >= va0 ? va1 - va0 + 1 : 0;
-                const uint32_t total = (real ? box_b : 0u) + (fin ? (HAS_PREV ? row_b : 0u) + (HAS_X ? row_b : 0u) : 0u) +
-                                       (uint32_t)nv * val_b;
+                const int nv = (VM == 0 && va1 >= va0) ? va1 - va0 + 1 : 0;
+                const uint32_t total = (real ? box_b + dg_b : 0u) +
+                                       (fin ? (HAS_PREV ? row_b : 0u) + (HAS_X ? row_b : 0u) : 0u) + (uint32_t)nv * val_b;
                 if (z == zs) meta[b] = it;
                 const uint32_t fb = fb0 + 8u * b;
                 mbar_expect_tx(full + b, total);
                 const uint32_t st = st0 + (uint32_t)b * SL.bytes;
                 if (real) tma_4d(st + SL.box, &P.tm_in, col0, I.x0 - P.hx, I.y0 - P.hy, z, fb, pol_keep);
+                if (VM == 1 && real) tma_3d(st + SL.dg, &P.tm_val, I.x0, I.y0, z, fb, pol_once);
                 if (fin) {
                     if (HAS_PREV) tma_4d(st + SL.prev, &P.tm_prev, col0, I.x0, I.y0, z - 1, fb, pol_once);
                     if (HAS_X) tma_4d(st + SL.xa, &P.tm_xa, col0, I.x0, I.y0, z - 1, fb, pol_once);
                 }
-                for (int zz = va0; zz <= va1; ++zz) {
+                for (int zz = va0; zz < va0 + nv; ++zz) {
                     int sl = vs + (zz - z);
                     if (sl >= VS) sl -= VS;
                     tma_4d(vr0 + (uint32_t)sl * slot_bytes, &P.tm_val, 0, I.x0, I.y0, zz, fb, pol_once);
@@ -367,14 +383,15 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         const int rs = oy * P.Px + ox;  // patch row slot (prev / X rows)
         const int64_t rxy = (int64_t)(I.y0 + oy) * P.nx + (I.x0 + ox);
         const uint32_t vo = (uint32_t)rs * Kp * 8u;  // this row's DIA entries within a ring slot
-        // smem row of each in-plane position (the centre where the neighbour is outside
-        // the grid: its DIA slot is zero there)
+        // smem row of each in-plane position.  Value mode 0: the centre where the neighbour
+        // is outside the grid (its DIA slot is zero there); modes 1, 2 (constant coefficients):
+        // the neighbour's box row, which the TMA zero-filled (an exact zero term)
         int qoff[Sh::NQ];
 #pragma unroll
         for (int q = 0; q < Sh::NQ; ++q) {
             const int gx = I.x0 + ox + Sh::dx(q), gy = I.y0 + oy + Sh::dy(q);
             const bool in = gx >= 0 && gx < P.nx && gy >= 0 && gy < P.ny;
-            qoff[q] = (in ? cb + Sh::dy(q) * P.box_x + Sh::dx(q) : cb) * pwv + v;
+            qoff[q] = ((in || VM != 0) ? cb + Sh::dy(q) * P.box_x + Sh::dx(q) : cb) * pwv + v;
         }
         double *outp = P.Yout + (rxy + (int64_t)I.zc0 * nxy) * P.ld_out + (int64_t)(colv0 + v) * 2;
         const int64_t out_step = nxy * P.ld_out;
@@ -393,18 +410,37 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
             if (act) {
                 if (real) {
                     const int sp = vs == 0 ? VS - 1 : vs - 1, sn = vs + 1 == VS ? 0 : vs + 1;
-                    ARR_CHECK(vo + (size_t)Sh::K * 8 <= slot_bytes);
+                    ARR_CHECK(VM != 0 || vo + (size_t)Sh::K * 8 <= slot_bytes);
                     const double *vp = reinterpret_cast<const double *>(vring + (size_t)sp * slot_bytes + vo);
                     const double *v0 = reinterpret_cast<const double *>(vring + (size_t)vs * slot_bytes + vo);
                     const double *vm = reinterpret_cast<const double *>(vring + (size_t)sn * slot_bytes + vo);
+                    // this row's diagonal (value mode 1): plane z, staged with the box
+                    const double dgv = VM == 1 ? reinterpret_cast<const double *>(st + SL.dg)[oy * P.Pxe + ox] : 0.0;
+                    constexpr int kc = Sh::k(0, Sh::QC);  // the centre (diagonal) slot
+                    auto cf = [&](const double *v, int k) -> double {
+                        if (VM == 0) return v[k];
+                        if (VM == 1 && k == kc) return dgv;
+                        return P.coef[k];
+                    };
+                    // the staged plane's terms: row z-1 gets its dz = +1 terms (fin), row z its
+                    // dz = 0 terms (mid), row z+1 its dz = -1 terms (nxt).  Interior steps (all
+                    // three) run a branch-free copy; the first and last steps of an item the
+                    // predicated one.
+                    auto terms = [&](auto F, auto M, auto N) {
 #pragma unroll
-                    for (int q = 0; q < Sh::NQ; ++q) {
-                        ARR_CHECK(qoff[q] >= 0 && qoff[q] < P.box_x * P.box_y * pwv);
-                        const double2 y = S[qoff[q]];
-                        if (q == Sh::QC) yiB = y;
-                        if (Sh::k(1, q) >= 0 && fin) fma2(accA, vp[Sh::k(1, q)], y);    // row z-1: its dz = +1 terms
-                        if (Sh::k(0, q) >= 0 && mid) fma2(accB, v0[Sh::k(0, q)], y);    // row z:   dz = 0
-                        if (Sh::k(-1, q) >= 0 && nxt) fma2(accC, vm[Sh::k(-1, q)], y);  // row z+1: dz = -1
+                        for (int q = 0; q < Sh::NQ; ++q) {
+                            ARR_CHECK(qoff[q] >= 0 && qoff[q] < P.box_x * P.box_y * pwv);
+                            const double2 y = S[qoff[q]];
+                            if (q == Sh::QC) yiB = y;
+                            if (Sh::k(1, q) >= 0 && F()) fma2(accA, cf(vp, Sh::k(1, q)), y);
+                            if (Sh::k(0, q) >= 0 && M()) fma2(accB, cf(v0, Sh::k(0, q)), y);
+                            if (Sh::k(-1, q) >= 0 && N()) fma2(accC, cf(vm, Sh::k(-1, q)), y);
+                        }
+                    };
+                    if (fin && mid && nxt) {
+                        terms([] { return true; }, [] { return true; }, [] { return true; });
+                    } else {
+                        terms([&] { return fin; }, [&] { return mid; }, [&] { return nxt; });
                     }
                 }
                 if (fin) {
@@ -522,15 +558,55 @@ __global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_
     }
 }
 
-template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int NT>
-int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
-    constexpr int kStCons = StCta<NT>::CONS, kStThreads = NT;
-    auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X, NT>;
-    const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv);
-    const size_t ring = (size_t)(L.NS + 2) * vslot_bytes(L.Px, L.Py, L.Kpad);
+// Per DIA slot k (blockIdx.y): min and max of the slot's value over the rows whose neighbour
+// lies inside the grid (order-preserving int64 keys of the doubles, atomics: deterministic).
+__device__ __forceinline__ long long dkey(double v) {
+    const long long b = __double_as_longlong(v);
+    return b >= 0 ? b : b ^ 0x7fffffffffffffffll;
+}
+__global__ void stencil_coef_range_kernel(const double *__restrict__ dia, int Kpad, int64_t n, int64_t nx, int64_t ny,
+                                          int64_t nz, StencilSlots sl, long long *kmin, long long *kmax) {
+    const int k = blockIdx.y;
+    int bit = -1;
+    for (int b = 0; b < 27; ++b)
+        if (sl.slot[b] == k) bit = b;
+    if (bit < 0) return;
+    const int dz = bit / 9 - 1, dy = (bit / 3) % 3 - 1, dx = bit % 3 - 1;
+    long long mn = 0x7fffffffffffffffll, mx = -0x7fffffffffffffffll - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = i % nx, t = i / nx, y = t % ny, z = t / ny;
+        if (x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny || z + dz < 0 || z + dz >= nz) continue;
+        const long long key = dkey(dia[i * Kpad + k]);
+        mn = key < mn ? key : mn;
+        mx = key > mx ? key : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(kmin + k, mn);
+        atomicMax(kmax + k, mx);
+    }
+}
+__global__ void stencil_diag_extract_kernel(const double *__restrict__ dia, int Kpad, int kc, int64_t n,
+                                            double *__restrict__ diag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        diag[i] = dia[i * Kpad + kc];
+}
+double key_to_double(long long k) { return __builtin_bit_cast(double, k >= 0 ? k : k ^ 0x7fffffffffffffffll); }
+
+template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X, int VM>
+int launch_st(arr_ctx *c, StencilLaunch &L) {
+    constexpr int NT = kStThreads;
+    constexpr int kStCons = StCta<NT>::CONS;
+    auto kern = stencil_kernel<SH, HAS_PREV, SUMSQ, HAS_X, NT, VM>;
+    const StageLayout<HAS_PREV, HAS_X> SL(L.box_x * L.box_y, L.Px * L.Py, L.pwv, VM == 1 ? vdiag_bytes(L.Pxe, L.Py) : 0u);
+    const size_t ring = VM == 0 ? (size_t)(L.NS + 2) * vslot_bytes(L.Px, L.Py, L.Kpad) : 0;
     const size_t smem = 256 + std::max((size_t)L.NS * SL.bytes + ring, (size_t)kStCons * 16);
     static LaunchCache cache;
-    const int occ = cached_occupancy(cache, kern, kStThreads, smem);
+    const int occ = cached_occupancy(cache, kern, NT, smem);
     int64_t G = (int64_t)c->num_sms * occ;
     static const int pm_env = [] { const char *e = getenv("ARRABIT_ST_ORDER"); return e ? atoi(e) : 1; }();
     // L2 policies (0 evict_normal, 1 evict_last, 2 evict_first) of the Y_j boxes, the once-read
@@ -541,8 +617,8 @@ int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
     L.ypol = ypol; L.spol = spol; L.opol = opol;
     static const int verbose = getenv("ARRABIT_ST_VERBOSE") ? 1 : 0;
     if (verbose)
-        fprintf(stderr, "stencil plan: shape %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu dyn %d\n",
-                SH, L.w, L.Px, L.Py, L.npan, L.pwv, L.NS, L.Lz, L.nzc, (long long)L.nitems, (long long)G, smem,
+        fprintf(stderr, "stencil plan: shape %d vmode %d w %d Px %d Py %d npan %d pwv %d NS %d Lz %d nzc %d items %lld G %lld smem %zu dyn %d\n",
+                SH, VM, L.w, L.Px, L.Py, L.npan, L.pwv, L.NS, L.Lz, L.nzc, (long long)L.nitems, (long long)G, smem,
                 SUMSQ ? 0 : st_dyn());
     L.pm = SUMSQ ? 0 : pm_env;
     L.dyn = SUMSQ ? 0 : st_dyn();
@@ -550,34 +626,40 @@ int launch_st_nt(arr_ctx *c, StencilLaunch &L) {
     if (!L.pm) G = (G / L.npan) * L.npan;  // panel-minor: each CTA keeps one panel (static column partial sums)
     if (G > L.nitems) G = L.nitems;
     if (G < L.npan) G = L.npan;
-    kern<<<(unsigned)G, kStThreads, smem, c->stream>>>(L);
+    kern<<<(unsigned)G, NT, smem, c->stream>>>(L);
     c->launches++;
     static const char *names[4] = {"stencil_kernel (27-point, DIA, TMA-staged 2.5-D)",
                                    "stencil_kernel (7-point, DIA, TMA-staged 2.5-D)",
                                    "stencil_kernel (2-D 5-point, DIA, TMA-staged 2.5-D)",
                                    "stencil_kernel (1-D 3-point, DIA, TMA-staged 2.5-D)"};
-    c->last_kernel = names[SH];
+    static const char *names_c[4] = {"stencil_kernel (27-point, constant coefficients, TMA-staged 2.5-D)",
+                                     "stencil_kernel (7-point, constant off-diagonals, TMA-staged 2.5-D)",
+                                     "stencil_kernel (2-D 5-point, constant off-diagonals, TMA-staged 2.5-D)",
+                                     "stencil_kernel (1-D 3-point, constant off-diagonals, TMA-staged 2.5-D)"};
+    c->last_kernel = VM == 0 ? names[SH] : names_c[SH];
     return (int)G;
 }
 
-template <int SH, bool HAS_PREV, bool SUMSQ, bool HAS_X>
-int launch_st(arr_ctx *c, StencilLaunch &L) {
-    return st_threads() == 512 ? launch_st_nt<SH, HAS_PREV, SUMSQ, HAS_X, 512>(c, L)
-                               : launch_st_nt<SH, HAS_PREV, SUMSQ, HAS_X, 1024>(c, L);
-}
-
-template <int SH>
+template <int SH, int VM>
 int dispatch_st_flags(arr_ctx *c, StencilLaunch &L, bool prev, bool ss, bool xa) {
     if (!xa) {
-        if (prev && !ss) return launch_st<SH, true, false, false>(c, L);
-        if (prev && ss) return launch_st<SH, true, true, false>(c, L);
-        if (!prev && !ss) return launch_st<SH, false, false, false>(c, L);
-        return launch_st<SH, false, true, false>(c, L);
+        if (prev && !ss) return launch_st<SH, true, false, false, VM>(c, L);
+        if (prev && ss) return launch_st<SH, true, true, false, VM>(c, L);
+        if (!prev && !ss) return launch_st<SH, false, false, false, VM>(c, L);
+        return launch_st<SH, false, true, false, VM>(c, L);
     }
-    if (prev && !ss) return launch_st<SH, true, false, true>(c, L);
-    if (prev && ss) return launch_st<SH, true, true, true>(c, L);
-    if (!prev && !ss) return launch_st<SH, false, false, true>(c, L);
-    return launch_st<SH, false, true, true>(c, L);
+    if (prev && !ss) return launch_st<SH, true, false, true, VM>(c, L);
+    if (prev && ss) return launch_st<SH, true, true, true, VM>(c, L);
+    if (!prev && !ss) return launch_st<SH, false, false, true, VM>(c, L);
+    return launch_st<SH, false, true, true, VM>(c, L);
+}
+template <int SH>
+int dispatch_st_vm(arr_ctx *c, StencilLaunch &L, bool prev, bool ss, bool xa) {
+    switch (c->st.vmode) {
+        case 1: return dispatch_st_flags<SH, 1>(c, L, prev, ss, xa);
+        case 2: return dispatch_st_flags<SH, 2>(c, L, prev, ss, xa);
+        default: return dispatch_st_flags<SH, 0>(c, L, prev, ss, xa);
+    }
 }
 
 bool al16(const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
@@ -620,6 +702,21 @@ bool encode_4d(CUtensorMap *m, const double *base, int64_t cols, int64_t ld, int
            CUDA_SUCCESS;
 }
 
+// 3-D fp64 tensor map (x, y, z) over the diagonal [n] of an nx x ny x nz grid; box
+// {box_x, box_y, 1} (box_x even: 16-byte inner box rows; needs nx even for 16-byte strides,
+// and box starts at even x: a TMA box row must start 16-byte aligned)
+bool encode_diag(CUtensorMap *m, const double *base, int64_t nx, int64_t ny, int64_t nz, int box_x, int box_y) {
+    auto enc = tensor_encoder();
+    if (!enc || nx % 2 != 0) return false;
+    const cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    const cuuint64_t gstride[2] = {(cuuint64_t)nx * 8, (cuuint64_t)(nx * ny) * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), gdim, gstride, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 // Host: geometry of one launch (patch, panels, z-chunks, stages) for block width w.
@@ -630,9 +727,9 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
     const StencilState &S = c->st;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
-    const int items_max = st_threads() - 32;  // one output vector per consumer thread (IPT = 2 spills)
+    const int items_max = kStThreads - 32;  // one output vector per consumer thread (IPT = 2 spills)
     // one CTA per SM at 1024 threads; two at 512 (each up to half the SM's shared memory)
-    size_t smem_max = st_threads() == 512 ? (size_t)S.smem_optin / 2 - 2048 : (size_t)S.smem_optin - 256;
+    const size_t smem_max = (size_t)S.smem_optin - 256;
     double best = 1e300;
     bool found = false;
     const int hx = S.hx, hy = S.hy;
@@ -646,9 +743,13 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 const int nrow = Px * Py;
                 if ((int64_t)nrow * pwv > items_max) break;
                 if (Px > S.nx || Py > S.ny) break;
+                // value mode 1 stages the diagonal with x innermost: box starts x0 = k Px must
+                // be 16-byte aligned (TMA), so Px even
+                if (S.vmode == 1 && Px % 2 != 0) continue;
                 const int bx = Px + 2 * hx, by = Py + 2 * hy;
-                const size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
-                const size_t slot = vslot_bytes(Px, Py, S.Kpad);
+                size_t stage = ((size_t)bx * by + (size_t)nrow * ((has_prev ? 1 : 0) + (has_x ? 1 : 0))) * pwv * 16;
+                if (S.vmode == 1) stage += (vdiag_bytes((Px + 1) & ~1, Py) + 127) & ~(size_t)127;
+                const size_t slot = S.vmode == 0 ? vslot_bytes(Px, Py, S.Kpad) : 0;
                 int NS = 4;
                 while (NS >= 2 && (size_t)NS * stage + (size_t)(NS + 2) * slot > smem_max) --NS;
                 if (NS < 2) continue;
@@ -657,10 +758,12 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 const double rag = (double)S.nx * S.ny / ((double)npx * Px * npy * Py);
                 // z-chunks: enough work items for >= ~12 per CTA, chunks of >= 8 planes
                 const int64_t G = (int64_t)c->num_sms;
+                // ticket order: whole columns of patches (no z-chunk seams) unless that leaves
+                // fewer than ~4 items per CTA; static order: >= ~12 items per CTA
                 int nzc = 1;
                 if (dyn && st_nzc() > 0) nzc = std::min<int>(st_nzc(), (int)S.nz);
                 else
-                    while ((int64_t)npx * npy * npan * nzc < 12 * G && S.nz / (nzc + 1) >= 8) ++nzc;
+                    while ((int64_t)npx * npy * npan * nzc < (dyn ? 4 : 12) * G && S.nz / (nzc + 1) >= 8) ++nzc;
                 const int Lz = (S.nz + nzc - 1) / nzc;
                 nzc = (S.nz + Lz - 1) / Lz;
                 const int64_t items = (int64_t)npx * npy * npan * nzc;
@@ -669,8 +772,9 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 const double warm = (double)(Lz + (nzc > 1 ? 1 : 0)) / Lz;
                 const double rowbytes = 16.0 * wv;
                 const double colfill = (double)wv / ((double)npan * pwv);  // OOB columns of the last panel
+                const double abytes = S.vmode == 0 ? 8.0 * S.Kpad : (S.vmode == 1 ? 8.0 : 0.0);  // A per row
                 double cost = ((double)need / nrow * warm + 1.0 + (has_prev ? 1.0 : 0.0) + (has_x ? 1.0 : 0.0)) * rowbytes +
-                              8.0 * S.Kpad * npan;
+                              abytes * npan;
                 cost /= colfill;
                 cost *= 1.0 + 6.0 / nrow;  // fixed per-step cost (barriers, TMA issue) over the outputs of a step
                 cost /= rag * tail;
@@ -693,6 +797,9 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
     L.K = S.K;
     L.Kpad = S.Kpad;
     L.val = S.dia;
+    L.vmode = S.vmode;
+    L.Pxe = (L.Px + 1) & ~1;
+    for (int k = 0; k < 27; ++k) L.coef[k] = S.coef[k];
     L.w = w;
     return true;
 }
@@ -713,16 +820,17 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     L.partials = a.partials;
     const StencilState &S = c->st;
     if (!encode_4d(&L.tm_in, a.Yin, a.w, a.ld_in, S.nx, S.ny, S.nz, 2 * L.pwv, L.box_x, L.box_y) ||
-        !encode_4d(&L.tm_val, S.dia, S.Kpad, S.Kpad, S.nx, S.ny, S.nz, S.Kpad, L.Px, L.Py) ||
+        (S.vmode == 0 && !encode_4d(&L.tm_val, S.dia, S.Kpad, S.Kpad, S.nx, S.ny, S.nz, S.Kpad, L.Px, L.Py)) ||
+        (S.vmode == 1 && !encode_diag(&L.tm_val, S.dia, S.nx, S.ny, S.nz, L.Pxe, L.Py)) ||
         (a.Yprev && !encode_4d(&L.tm_prev, a.Yprev, a.w, a.ld_prev, S.nx, S.ny, S.nz, 2 * L.pwv, L.Px, L.Py)) ||
         (a.Xa && !encode_4d(&L.tm_xa, a.Xa, a.w, a.ld_xa, S.nx, S.ny, S.nz, 2 * L.pwv, L.Px, L.Py)))
         return -1;
     const bool prev = a.Yprev != nullptr, ss = a.partials != nullptr, xa = a.Xa != nullptr;
     switch (c->st.shape) {
-        case 0: return dispatch_st_flags<0>(c, L, prev, ss, xa);
-        case 1: return dispatch_st_flags<1>(c, L, prev, ss, xa);
-        case 2: return dispatch_st_flags<2>(c, L, prev, ss, xa);
-        case 3: return dispatch_st_flags<3>(c, L, prev, ss, xa);
+        case 0: return dispatch_st_vm<0>(c, L, prev, ss, xa);
+        case 1: return dispatch_st_vm<1>(c, L, prev, ss, xa);
+        case 2: return dispatch_st_vm<2>(c, L, prev, ss, xa);
+        case 3: return dispatch_st_vm<3>(c, L, prev, ss, xa);
     }
     return -1;
 }
@@ -773,6 +881,63 @@ arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
                                                                   sl, (double *)dia);
     c->launches++;
     if (cudaGetLastError() != cudaSuccess) return ARR_ECUDA;
+    // Constant coefficients (finite-difference operators): every slot's value the same on all
+    // rows whose neighbour is in the grid.  Then only the diagonal (vmode 1), or nothing
+    // (vmode 2), is read per row; ARRABIT_ST_VMODE caps the mode (0: always the K diagonals).
+    S.vmode = 0;
+    static const int vcap = [] { const char *e = getenv("ARRABIT_ST_VMODE"); return e ? atoi(e) : 2; }();
+    if (vcap > 0) {
+        long long *keys = nullptr;
+        if (cudaMallocAsync((void **)&keys, sizeof(long long) * 54, c->stream) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeAsync(dia, c->stream);
+            return ARR_ENOMEM;
+        }
+        std::vector<long long> init(54);
+        for (int k = 0; k < 27; ++k) { init[k] = 0x7fffffffffffffffll; init[27 + k] = -0x7fffffffffffffffll - 1; }
+        cudaMemcpyAsync(keys, init.data(), sizeof(long long) * 54, cudaMemcpyHostToDevice, c->stream);
+        stencil_coef_range_kernel<<<dim3((unsigned)blocks, K), 256, 0, c->stream>>>((const double *)dia, Kpad, c->A.n, nx,
+                                                                                    ny, nz, sl, keys, keys + 27);
+        c->launches++;
+        std::vector<long long> h(54);
+        if (cudaMemcpyAsync(h.data(), keys, sizeof(long long) * 54, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+            cudaStreamSynchronize(c->stream) != cudaSuccess) {
+            cudaFreeAsync(keys, c->stream);
+            cudaFreeAsync(dia, c->stream);
+            return ARR_ECUDA;
+        }
+        cudaFreeAsync(keys, c->stream);
+        int kc = -1;
+        for (int b = 0; b < 27; ++b)
+            if (b == 13) kc = sl.slot[b];  // (0, 0, 0): the diagonal
+        bool off_const = true, diag_const = true;
+        for (int k = 0; k < K; ++k) {
+            const bool present = h[k] <= h[27 + k];
+            const bool cst = !present || h[k] == h[27 + k];
+            S.coef[k] = present ? key_to_double(h[k]) : 0.0;
+            if (k == kc) diag_const = cst;
+            else off_const = off_const && cst;
+        }
+        if (off_const && diag_const && vcap >= 2) {
+            S.vmode = 2;
+        } else if (off_const && kc >= 0 && nx % 2 == 0) {
+            double *diag = nullptr;
+            if (cudaMallocAsync((void **)&diag, sizeof(double) * (size_t)c->A.n, c->stream) != cudaSuccess) {
+                cudaGetLastError();
+            } else {
+                stencil_diag_extract_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>((const double *)dia, Kpad, kc, c->A.n,
+                                                                                   diag);
+                c->launches++;
+                cudaFreeAsync(dia, c->stream);
+                dia = diag;
+                S.vmode = 1;
+            }
+        }
+        if (S.vmode == 2) {
+            cudaFreeAsync(dia, c->stream);
+            dia = nullptr;
+        }
+    }
     S.dia = (double *)dia;
     S.nx = nx; S.ny = ny; S.nz = nz;
     S.K = K;

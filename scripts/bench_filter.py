@@ -72,11 +72,12 @@ def main():
             ms, cnt = ctx.eig_phase_times()
             deg_ms = ms[0] / cnt[0]
             K = ctx.stencil_points
-            amod = 8 * K * A.n if K else 12 * A.nnz + 8 * (A.n + 1)
+            ab = ctx.stencil_abytes if K else None
+            amod = ab * A.n if K else 12 * A.nnz + 8 * (A.n + 1)
             byts = (amod + 16 * A.n * w + (d - 1) * (amod + 24 * A.n * w)) / d
             gbs = byts / (deg_ms / 1e3) / 1e9
             print(json.dumps({"config": spec.name, "path": path + ("+yband" if args.yband and path == "csr" else ""),
-                              "w": w, "d": d, "K": K, "ms_per_degree": round(deg_ms, 4),
+                              "w": w, "d": d, "K": K, "A_bytes_per_row": ab, "ms_per_degree": round(deg_ms, 4),
                               "bytes_per_degree": byts, "GBs": round(gbs, 1), "frac_of_measured": round(gbs / peak, 4)}),
                   flush=True)
             ctx.close()

@@ -32,14 +32,27 @@ def relF(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-# (matrix, declared grid (nx, ny, nz))
+def _varcoef(A, seed):
+    """The same pattern with every off-diagonal value scaled by its own factor in [0.5, 1.5)
+    (no constant coefficient: the K-diagonal value mode)."""
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    off = rows != A.col_idx
+    val = A.val.copy()
+    val[off] *= 0.5 + np.random.default_rng(seed).random(int(off.sum()))
+    return synth.CSR(A.n, A.row_ptr.copy(), A.col_idx.copy(), val, A.name + "_var")
+
+
+# (matrix, declared grid (nx, ny, nz), A bytes per row the stencil path reads)
 CASES = {
-    "lap1d": (lambda: synth.laplacian_1d(1000), (1000, 1, 1)),
-    "lap2d_xz": (lambda: synth.laplacian_2d(37, 41), (37, 1, 41)),   # march along y
-    "lap2d_xy": (lambda: synth.laplacian_2d(37, 41), (37, 41, 1)),   # one plane, y halo
-    "lap3dV": (lambda: synth.laplacian_3d_potential(13, 2), (13, 13, 13)),
-    "st27": (lambda: synth.stencil27_3d(11), (11, 11, 11)),
-    "st27_tall": (lambda: synth.stencil27_3d(6), (6, 6, 6)),
+    "lap1d": (lambda: synth.laplacian_1d(1000), (1000, 1, 1), 0),       # all coefficients constant
+    "lap2d_xz": (lambda: synth.laplacian_2d(37, 41), (37, 1, 41), 0),   # march along y
+    "lap2d_xy": (lambda: synth.laplacian_2d(37, 41), (37, 41, 1), 0),   # one plane, y halo
+    "lap3dV": (lambda: synth.laplacian_3d_potential(13, 2), (13, 13, 13), 56),    # nx odd: K diagonals
+    "lap3dV_even": (lambda: synth.laplacian_3d_potential(14, 2), (14, 14, 14), 8),  # the diagonal only
+    "lap3d_var": (lambda: _varcoef(synth.laplacian_3d_potential(12, 2), 3), (12, 12, 12), 56),
+    "st27": (lambda: synth.stencil27_3d(11), (11, 11, 11), 0),
+    "st27_tall": (lambda: synth.stencil27_3d(6), (6, 6, 6), 0),
+    "st27_var": (lambda: _varcoef(synth.stencil27_3d(8), 4), (8, 8, 8), 216),
 }
 
 
@@ -55,7 +68,7 @@ def _pair(arr, A, grid, w, d, ld=None):
 @pytest.mark.parametrize("kind", list(CASES))
 @pytest.mark.parametrize("w,ld", [(2, 2), (24, 26), (98, 98), (282, 282), (550, 552)])
 def test_stencil_filter_bitwise_and_oracle(arr, kind, w, ld):
-    mk, grid = CASES[kind]
+    mk, grid, abytes = CASES[kind]
     A = mk()
     if w >= A.n:
         pytest.skip("block wider than the matrix")
@@ -64,6 +77,7 @@ def test_stencil_filter_bitwise_and_oracle(arr, kind, w, ld):
     a = oracle.gershgorin_lower(A)
     b = a + 0.7 * (2 * np.abs(A.val).max() * 2 - a)
     c_csr, c_st = _pair(arr, A, grid, w, d)
+    assert c_st.stencil_abytes == abytes  # the value mode detected from the coefficients
     out = {}
     for name, ctx in (("csr", c_csr), ("st", c_st)):
         ctx.eig_set_interval(a, b)
@@ -78,9 +92,9 @@ def test_stencil_filter_bitwise_and_oracle(arr, kind, w, ld):
         assert relF(out["st"], ref) <= 1e-12
 
 
-@pytest.mark.parametrize("kind", ["lap3dV", "st27", "lap2d_xz"])
+@pytest.mark.parametrize("kind", ["lap3dV", "lap3dV_even", "lap3d_var", "st27", "lap2d_xz"])
 def test_stencil_normalised_and_interp(arr, kind):
-    mk, grid = CASES[kind]
+    mk, grid, _ = CASES[kind]
     A = mk()
     w, d = 40, 8
     X = synth.gaussian_block(A.n, w, 9)
