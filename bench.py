@@ -10,7 +10,9 @@ metric's "1/2/4/8 B200" is quoted on: BASELINE.json configs[2] = cfg3, the 3-D
 tol = 1e-10, seed 2 (--config selects another).  The 3-D grids run the stencil-aware
 filter path (eig_set_stencil; DIA + TMA-staged 2.5-D kernel), others the CSR kernels.
 value = eigenpairs/s = k * steps / (max-over-ranks device time).
-The filter's HBM GB/s (the metric's first half) is the `roofline` object; a shorter
+`roofline` is the dominant kernel of the timed steps (largest share of device time:
+at cfg3 the FP64 DMMA Gram, vs the measured DGEMM peak); `roofline.kernels` holds the
+other classes, among them the filter's HBM GB/s (the metric's first half).  A shorter
 cfg2 solve (BASELINE.json configs[1]) is reported beside it as `secondary`.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -364,13 +366,14 @@ def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps,
     clocks = sampler.stop()
     launches = ctx.launch_count - launches0
     phase_ms, phase_cnt = ctx.eig_phase_times()
+    kern_ms, kern_flops, kern_cnt = ctx.eig_kernel_times()  # the DMMA Gram / GEMM kernels alone
     # the kernel the filter degrees launch (one more filter_step, outside the timed region)
     with torch.cuda.stream(stream):
         ctx.eig_set_interval(infos[-1].a, infos[-1].b)
         ctx.filter_step(X, normalize=True)
     kernel = ctx.last_spmm_kernel
     return dict(ctx=ctx, step_ms=step_ms, infos=infos, clocks=clocks, launches=launches, phase_ms=phase_ms,
-                phase_cnt=phase_cnt, kernel=kernel, path=path, lean=ctx_lean, stencil_K=ctx.stencil_points,
+                phase_cnt=phase_cnt, kern_ms=kern_ms, kern_flops=kern_flops, kern_cnt=kern_cnt, kernel=kernel, path=path, lean=ctx_lean, stencil_K=ctx.stencil_points,
                 stencil_abytes=ctx.stencil_abytes if ctx.stencil_points else None,
                 eigenvalues=ev)
 
@@ -388,7 +391,36 @@ def Ad_of(arr, Aloc, dev, stream):
     return _AD[key]
 
 
+def load_fp64_peak():
+    """The FP64 tensor (DMMA) peak: cuBLAS DGEMM 8192^3 measured on this pool's B200
+    (profiles/peaks_fp64.json; the sustained figure for kernels timed inside a long step)."""
+    pp = os.path.join(ROOT, "profiles", "peaks_fp64.json")
+    try:
+        with open(pp) as f:
+            pk = json.load(f)
+        return float(pk["fp64_dgemm_tflops_sustained"]), "profiles/peaks_fp64.json (cuBLAS DGEMM 8192^3, back to back, measured)"
+    except Exception:
+        return None, None
+
+
+def _traffic(cid, family):
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json" if family != "gram" else f"ncu_traffic_gram_cfg{cid}.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            return tj, tj.get("dram_bytes_per_launch"), tj.get("source")
+        except Exception:
+            pass
+    return None, None, None
+
+
 def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
+    """The roofline of the DOMINANT kernel of the timed steps (largest share of the step's
+    device time, per-launch CUDA events on the context stream) plus the other two kernel
+    classes of the path: the filter degree (HBM-bound; BJ's metric), the DMMA Gram and the
+    DMMA GEMM (FP64-tensor-bound)."""
+    cid = args.config if cid is None else cid
     peak, peak_src = load_peaks()
     w = spec.w if w is None else w  # the filtered width on this rank (the column split filters w_r columns)
     deg_ms = r["phase_ms"][0] / max(1, r["phase_cnt"][0])
@@ -396,28 +428,45 @@ def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
     if args.filter == "interp":  # Clenshaw steps also read X (the a_k X term): + 8 n w per degree
         bpl += 8 * nrow * w
     achieved = bpl / (deg_ms / 1000.0) / 1e9
-    traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config if cid is None else cid}.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                tj = json.load(f)
-            if tj.get("kernel_family", "") and tj["kernel_family"] in r["kernel"]:
-                traffic = tj.get("dram_bytes_per_launch")
-                traffic_src = tj.get("source")
-        except Exception:
-            traffic = None
+    tj, traffic, traffic_src = _traffic(cid, "filter")
+    if tj is not None and not (tj.get("kernel_family", "") and tj["kernel_family"] in r["kernel"]):
+        traffic, traffic_src = None, None
     pm, st = r["phase_ms"], sum(r["step_ms"])
-    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+    filt = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "kernel": r["kernel"],
             "bytes_per_launch": bpl, "bytes_model": (
                 {None: "12 nnz + 8(n+1)", 0: "0 (all coefficients constant)", 8: "8 n (diagonal; constant off-diagonals)"}.get(
                     r["stencil_abytes"], "8 K n (K diagonals)") + " + 24 n w (16 n w on a sweep's first degree)"),
             "avg_launch_us": deg_ms * 1000.0, "launches": int(r["phase_cnt"][0]), "peak_source": peak_src,
-            "frac_of_8TBs": achieved / 8000.0, "share_of_step": pm[0] / st,
-            "phase_ms_per_step": {"filter_degrees": pm[0] / steps, "arr_project": pm[1] / steps,
-                                  "arr_basis": pm[3] / steps, "arr_H": pm[4] / steps, "arr_small_eig": pm[5] / steps,
-                                  "residuals": pm[2] / steps}}
+            "frac_of_8TBs": achieved / 8000.0, "share_of_step": pm[0] / st}
+    pk64, pk64_src = load_fp64_peak()
+    dmma = {}
+    for i, (name, kern) in enumerate((("dmma_gram", "gram_kernel_pv (FP64 DMMA m8n8k4, X^T Y split over rows)"),
+                                      ("dmma_gemm", "gemm_kernel_ca (FP64 DMMA m8n8k4, X B)"))):
+        ms, fl, cnt = float(r["kern_ms"][i]), float(r["kern_flops"][i]), int(r["kern_cnt"][i])
+        if cnt == 0 or ms <= 0:
+            continue
+        ach = fl / (ms / 1e3) / 1e12
+        o = {"bound": "tensor", "achieved": ach, "peak": pk64, "unit": "TFLOP/s",
+             "frac": ach / pk64 if pk64 else None, "traffic": None, "kernel": kern,
+             "flops_per_launch": fl / cnt, "flops_model": "2 n m1 m2 (symmetric Gram n m (m+1); upper-triangular B "
+             "2 n sum_c min(c+1, m1)), summed over the step's launches of every shape",
+             "avg_launch_us": ms * 1e3 / cnt, "launches": cnt, "peak_source": pk64_src, "share_of_step": ms / st}
+        if name == "dmma_gram":
+            tj, tr, ts = _traffic(cid, "gram")
+            if tj is not None:
+                o["traffic"], o["traffic_source"] = tr, ts
+        dmma[name] = o
+    kinds = {"filter": filt, **dmma}
+    dom = max(kinds, key=lambda k: kinds[k]["share_of_step"])
+    out = dict(kinds[dom])
+    out["dominant"] = dom
+    out["dominant_by"] = "largest share of the timed steps' device time (CUDA events per launch on the context stream)"
+    out["kernels"] = {k: v for k, v in kinds.items() if k != dom}
+    out["phase_ms_per_step"] = {"filter_degrees": pm[0] / steps, "arr_project": pm[1] / steps,
+                                "arr_basis": pm[3] / steps, "arr_H": pm[4] / steps, "arr_small_eig": pm[5] / steps,
+                                "residuals": pm[2] / steps}
+    return out
 
 
 def run_ours(args):
@@ -526,7 +575,7 @@ def run_ours(args):
                  "avg_launch_us": gms * 1e3, "flops_per_launch": fl}
     except Exception as e:  # noqa: BLE001
         dense = {"error": str(e)}
-    roofline["dense_gram"] = dense
+    roofline["gram_timed_alone"] = dense
     if spec.kind == "zipf":
         roofline["gather_model_bytes_per_launch"] = (12 * nnz_loc + 8 * (r1 - r0 + 1) + 8 * nnz_loc * spec.w
                                                      + 16 * (r1 - r0) * spec.w)

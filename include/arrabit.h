@@ -141,6 +141,9 @@ typedef struct {
                         mu_k, mu_w} - the driver's decisions and the Ritz values they are
                         taken from, for checking them against the rules                  */
     int32_t log_cap; /* rows available in log (0: no log)                                */
+    double range_digits; /* D of the dynamic-range rule (inner = 0): s = clamp(floor(D /
+                        log10 |T_d((mu_1 - c)/e)|), 1, s_max); 0 = the default D = 12
+                        (R6)                                                   */
 } arr_solve_opts;
 #define ARR_LOG_FIELDS 12
 
@@ -217,6 +220,14 @@ uint64_t eig_launch_count(const arr_ctx *c);
  * others: calls). */
 arr_status eig_set_timing(arr_ctx *c, int32_t on);
 arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts);
+/* The FP64 DMMA kernels alone (with eig_set_timing on; events around each launch,
+ * the split reduction excluded): index 0 = the Gram kernels (X^T Y, Alg. RR / ARR
+ * products P:219-224), 1 = the GEMM kernels (X B): total device ms,
+ * ALGORITHMIC flops (2 n m1 m2; a symmetric Gram n m (m+1); an upper-triangular B
+ * 2 n sum_c min(c+1, m1)) and launch counts since timing was enabled.  Synchronises
+ * the stream.  Column-split contexts report their ARR (row) context. */
+arr_status eig_kernel_times(arr_ctx *c, double *ms /* [2] */, double *flops /* [2] */,
+                            int64_t *launches /* [2] */);
 
 /* ---------------------------------------------------------------- A0: interval
  * a_out = min_i (A_ii - sum_{j!=i} |A_ij|), the Gershgorin lower bound used in

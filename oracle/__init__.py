@@ -36,6 +36,7 @@ from .core import (  # noqa: F401
     arr,
     residuals,
     sweeps_rule,
+    RANGE_DIGITS,
     solve,
     solve_deflate,
     rcond_gram,

@@ -333,11 +333,15 @@ def residuals(A, Y: np.ndarray, mu: np.ndarray) -> np.ndarray:
     return col_norms(R) / np.maximum(1.0, np.abs(mu))
 
 
-def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int, gamma=None) -> int:
+RANGE_DIGITS = 12.0  # D of the dynamic-range rule (R6)
+
+
+def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int, gamma=None,
+                digits: float = RANGE_DIGITS) -> int:
     """Sweeps between ARR steps (DESIGN.md §4 R6, the dynamic-range rule that
     replaces the paper's rcond inner stop P:1355-1388): amp = |T_d((mu_1-c)/e)|
     (|psi_d((mu_1-c)/e)| with the interpolant filter),
-    s = s_max if amp <= 1 else clamp(floor(8/log10(amp)), 1, s_max)."""
+    s = s_max if amp <= 1 else clamp(floor(D/log10(amp)), 1, s_max), D = digits."""
     c = 0.5 * (a + b)
     e = 0.5 * (b - a)
     t = (mu1 - c) / e
@@ -346,7 +350,7 @@ def sweeps_rule(mu1: float, a: float, b: float, d: int, s_max: int, gamma=None) 
         return s_max
     if not math.isfinite(amp):
         return 1
-    return int(min(max(math.floor(8.0 / math.log10(amp)), 1), s_max))
+    return int(min(max(math.floor(digits / math.log10(amp)), 1), s_max))
 
 
 @dataclass
@@ -394,7 +398,7 @@ def _degree_rule(d_max: int, a: float, b: float, mu_k: float, mu_w: float, gamma
 def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
           s_max: int = 5, w: int | None = None, max_outer: int | None = None, filter: str = "cheb",
           inner_solver: str = "mpm", arr_method: str = "qr", inner: str = "range", exits: int = 0,
-          adapt: int = 0) -> SolveResult:
+          adapt: int = 0, range_digits: float = RANGE_DIGITS) -> SolveResult:
     """ARRABIT-MPM (Alg. Arrabit2).  Defaults = the fixed-parameter solve
     (adaptive lines disabled; R3/R6/R10):
 
@@ -415,12 +419,13 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
             bit 2: d from 3, re-chosen after every ARR by Eqs. hat-d / degree
               with d as d_max;
             bit 4: continuation + deflation (solve_deflate, R19).
-      arr_method: "qr" (paper-literal) or "cgs2" (orthonormalise-then-augment, R8)."""
+      arr_method: "qr" (paper-literal) or "cgs2" (orthonormalise-then-augment, R8).
+      range_digits: D of the dynamic-range rule (R6)."""
     if adapt & 4:
         if (adapt & 3) or inner != "range" or exits or inner_solver != "mpm":
             raise ValueError("continuation + deflation runs fixed p / d MPM sweeps only")
         return solve_deflate(A, k, d, p, X0, tol=tol, maxit=maxit, s_max=s_max, w=w, filter=filter,
-                             arr_method=arr_method, max_outer=max_outer)
+                             arr_method=arr_method, max_outer=max_outer, range_digits=range_digits)
     n = A.n
     w = X0.shape[1] if w is None else w  # w - k guard vectors (P:1291-1299)
     d_max, p_max = d, p
@@ -463,7 +468,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
                     break
                 rcp = rc
         else:
-            s = sweeps_rule(mu1, a, b, d_cur, s_max, None if gamma_of is None else gamma_of(d_cur))
+            s = sweeps_rule(mu1, a, b, d_cur, s_max, None if gamma_of is None else gamma_of(d_cur), range_digits)
             for _ in range(s):
                 X = sweep(X)
         sweeps += s
@@ -508,7 +513,7 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
 
 def solve_deflate(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: int = 300,
                   s_max: int = 5, w: int | None = None, filter: str = "cheb", arr_method: str = "qr",
-                  max_outer: int | None = None) -> SolveResult:
+                  max_outer: int | None = None, range_digits: float = RANGE_DIGITS) -> SolveResult:
     """Alg. Arrabit2 with continuation (Eq. contin, P:1336-1349) and deflation (Eq. defl,
     P:1396-1416), MPM sweeps by the dynamic-range rule, fixed p and d (R19):
       tol_1 = sqrt(tol); tol_{t+1} = max(1e-2 tol_t, tol) once max res <= tol_t;
@@ -536,7 +541,7 @@ def solve_deflate(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10,
         wa = w - nc
         Qc = X[:, :nc]
         Xa = X[:, nc:]
-        s = sweeps_rule(mu1, a, b, d, s_max, gamma)
+        s = sweeps_rule(mu1, a, b, d, s_max, gamma, range_digits)
         for _ in range(s):
             Xa = mpm_sweep(A, a, b, d, Xa) if gamma is None else poly_sweep(A, a, b, gamma, Xa)
         sweeps += s

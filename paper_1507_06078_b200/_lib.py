@@ -18,7 +18,7 @@ EXPORTED = [
     "eig_init", "eig_init_w", "eig_destroy", "eig_last_error", "eig_workspace_bytes", "eig_launch_count",
     "eig_gershgorin_lower", "eig_set_interval", "eig_set_degree", "eig_set_filter", "eig_set_mode", "filter_step", "spmm", "gram", "gemm",
     "orthonormalize", "arr_project", "arr_project_p", "residuals", "eig_solve", "eig_solve_host",
-    "eig_set_timing", "eig_phase_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active", "eig_stencil_abytes", "eig_last_spmm_kernel",
+    "eig_set_timing", "eig_phase_times", "eig_kernel_times", "eig_set_schedule", "eig_set_stencil", "eig_stencil_active", "eig_stencil_abytes", "eig_last_spmm_kernel",
     "eig_init_dist", "eig_init_colsplit", "comm_get_nccl_id", "comm_init_nccl", "comm_init_local_group", "comm_rank_size", "comm_destroy",
 ]
 
@@ -40,7 +40,7 @@ class arr_solve_opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("maxit", ctypes.c_int32), ("s_max", ctypes.c_int32),
                 ("exits", ctypes.c_int32), ("inner", ctypes.c_int32), ("adapt", ctypes.c_int32),
                 ("gn", ctypes.c_int32), ("grid", ctypes.c_int64 * 3), ("log", ctypes.c_void_p),
-                ("log_cap", ctypes.c_int32)]
+                ("log_cap", ctypes.c_int32), ("range_digits", ctypes.c_double)]
 
 
 class arr_solve_info(ctypes.Structure):
@@ -96,6 +96,7 @@ def load(path: str | None = None):
         "eig_set_timing": ([vp, i32], ctypes.c_int),
         "eig_set_schedule": ([vp, vp, vp, i64], ctypes.c_int),
         "eig_phase_times": ([vp, pf64, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "eig_kernel_times": ([vp, pf64, pf64, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
         "filter_step": ([vp, vp, i64, i32, vp], ctypes.c_int),
         "spmm": ([vp, f64, f64, vp, i64, vp, i64, i32], ctypes.c_int),
         "gram": ([vp, vp, i64, i32, vp, i64, i32, vp, i64], ctypes.c_int),

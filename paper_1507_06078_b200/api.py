@@ -197,6 +197,18 @@ class EigContext:
                     "eig_phase_times")
         return ms, cnt
 
+    def eig_kernel_times(self):
+        """The FP64 DMMA kernels alone: (ms[2], flops[2], launches[2]) for the Gram (0) and
+        GEMM (1) kernels since eig_set_timing(True), flops algorithmic (include/arrabit.h)."""
+        ms = np.zeros(2)
+        fl = np.zeros(2)
+        cnt = np.zeros(2, dtype=np.int64)
+        self._check(self.lib.eig_kernel_times(self.h, ms.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                              fl.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                              cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+                    "eig_kernel_times")
+        return ms, fl, cnt
+
     # -- A0
     def eig_gershgorin_lower(self) -> float:
         a = ctypes.c_double()
@@ -319,9 +331,10 @@ class EigContext:
 
     # -- driver
     def eig_solve(self, X: torch.Tensor, tol: float = 1e-10, maxit: int = 300, s_max: int = 5, exits: int = 0,
-                  inner: str = "range", adapt: int = 0, inner_solver: str = "mpm"):
+                  inner: str = "range", adapt: int = 0, inner_solver: str = "mpm", range_digits: float = 0.0):
         """exits: the paper's extra stop rules as a bit mask: 1 = (ii), 2 = (iii).
         inner: 'range' (dynamic-range rule, R6) or 'rcond' (the paper's).
+        range_digits: D of the dynamic-range rule (0 = the library default, 12).
         adapt: the paper's adaptive p (bit 1), degree (bit 2), continuation + deflation (bit 4).
         inner_solver: 'mpm' (default) or 'gn' (Gauss-Newton, Alg. Arrabit2)."""
         px, ld, _ = _blk(X, "X")
@@ -330,6 +343,7 @@ class EigContext:
         log = np.zeros((maxit, LOG_FIELDS))
         opts.log = ctypes.c_void_p(log.ctypes.data)
         opts.log_cap = maxit
+        opts.range_digits = range_digits
         ev = np.empty(self.k)
         res = np.empty(self.k)
         info = arr_solve_info()

@@ -139,26 +139,13 @@ inline double *SHIFT_buf(arr_ctx *c) { return c->vecw + std::max(m_of(c, c->p), 
 inline double *D_buf(arr_ctx *c) { return c->vecw + 2 * (int64_t)std::max(m_of(c, c->p), ARR_MAX_W); }
 
 // ---------------------------------------------------------------- phase timing
-int t_mark(arr_ctx *c) {
-    if (!c->timing) return -1;
-    if (c->ev_next == (int)c->ev_pool.size()) {
-        cudaEvent_t e;
-        if (cudaEventCreate(&e) != cudaSuccess) return -1;
-        c->ev_pool.push_back(e);
-    }
-    const int i = c->ev_next++;
-    cudaEventRecord(c->ev_pool[i], c->stream);
-    return i;
-}
-void t_add(arr_ctx *c, int phase, int e0, int e1, int64_t count) {
-    if (e0 >= 0 && e1 >= 0) c->pending.push_back({phase, e0, e1, count});
-}
 void t_resolve(arr_ctx *c) {  // call only right after a stream sync, with no phase open
     for (const auto &p : c->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, c->ev_pool[p.e0], c->ev_pool[p.e1]) == cudaSuccess) {
             c->phase_ms[p.phase] += ms;
             c->phase_cnt[p.phase] += p.count;
+            c->phase_work[p.phase] += p.work;
         }
     }
     c->pending.clear();
@@ -209,6 +196,19 @@ double psi_eval(const std::vector<double> &a, double t) {
         b1 = b0;
     }
     return a[0] + t * b1 - b2;
+}
+
+// Sweeps between ARR steps, the dynamic-range rule (R6): s = clamp(floor(D /
+// log10 amp), 1, s_max) with amp = |T_d((mu_1 - c)/e)| the per-sweep amplification of the
+// top Ritz direction and D digits of column dynamic range between ARRs (opts->range_digits,
+// 0 = the default 12: the shifted CholeskyQR3 of the ARR is stable far beyond that, and
+// fewer ARRs per solve pay: cfg3 7 -> 4 outer iterations).
+constexpr double kRangeDigits = 12.0;
+int sweeps_rule(double amp, int s_max, double digits) {
+    const double D = digits > 0.0 ? digits : kRangeDigits;
+    if (!(amp > 1.0)) return s_max;
+    if (!isfinite(amp)) return 1;
+    return (int)std::min<double>(std::max<double>(floor(D / log10(amp)), 1.0), s_max);
 }
 
 // ---------------------------------------------------------------- distributed building blocks
@@ -859,8 +859,7 @@ arr_status solve_deflate(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opt
         if ((st = eig_set_interval(c, a, b)) != ARR_OK) { restore(); return st; }
         const double cc = 0.5 * (a + b), e = 0.5 * (b - a);
         const double amp = fabs(c->filter_kind == 1 ? psi_eval(c->coef, (mu1 - cc) / e) : chebT(c->d, (mu1 - cc) / e));
-        int s = opts->s_max;
-        if (amp > 1.0) s = !isfinite(amp) ? 1 : (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
+        const int s = sweeps_rule(amp, opts->s_max, opts->range_digits);
         CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
         for (int q = 0; q < s; ++q)
             if ((st = filter_core(c, Xa, ldx, 1, nullptr)) != ARR_OK) { restore(); return st; }
@@ -954,8 +953,7 @@ arr_status cs_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *op
         if ((st = eig_set_interval(cc, a, b)) != ARR_OK) return st;
         const double ccen = 0.5 * (a + b), e = 0.5 * (b - a);
         const double amp = fabs(cc->filter_kind == 1 ? psi_eval(cc->coef, (mu1 - ccen) / e) : chebT(cc->d, (mu1 - ccen) / e));
-        int s = opts->s_max;
-        if (amp > 1.0) s = !isfinite(amp) ? 1 : (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
+        const int s = sweeps_rule(amp, opts->s_max, opts->range_digits);
         CUDA_TRY(cudaMemsetAsync(cc->dinfo + INFO_BAD, 0, sizeof(int), cc->stream));
         for (int q = 0; q < s; ++q)
             if ((st = filter_core(cc, X, ldx, 1, nullptr)) != ARR_OK) return st;  // local: no exchange
@@ -1390,7 +1388,7 @@ arr_status eig_set_timing(arr_ctx *c, int32_t on) {
     c->pending.clear();
     c->ev_next = 0;
     c->timing = on != 0;
-    for (int i = 0; i < kPhases; ++i) { c->phase_ms[i] = 0.0; c->phase_cnt[i] = 0; }
+    for (int i = 0; i < kPhasesAll; ++i) { c->phase_ms[i] = 0.0; c->phase_cnt[i] = 0; c->phase_work[i] = 0.0; }
     return ARR_OK;
 }
 
@@ -1408,6 +1406,20 @@ arr_status eig_phase_times(arr_ctx *c, double *ms, int64_t *counts) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     t_resolve(c);
     for (int i = 0; i < kPhases; ++i) { ms[i] = c->phase_ms[i]; counts[i] = c->phase_cnt[i]; }
+    return ARR_OK;
+}
+
+arr_status eig_kernel_times(arr_ctx *c, double *ms, double *flops, int64_t *launches) {
+    GUARD(c);
+    if (!ms || !flops || !launches) return fail(c, ARR_EINVAL, "null output");
+    arr_ctx *t = c->cs ? c->cs->row : c;  // the column split's ARR runs on its row context
+    CUDA_TRY(cudaStreamSynchronize(t->stream));
+    t_resolve(t);
+    for (int i = 0; i < 2; ++i) {
+        ms[i] = t->phase_ms[6 + i];
+        flops[i] = t->phase_work[6 + i];
+        launches[i] = t->phase_cnt[6 + i];
+    }
     return ARR_OK;
 }
 
@@ -1574,11 +1586,7 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
         // sweeps between ARR steps: dynamic-range rule (R6)
         const double cc = 0.5 * (a + b), e = 0.5 * (b - a);
         const double amp = fabs(c->filter_kind == 1 ? psi_eval(c->coef, (mu1 - cc) / e) : chebT(c->d, (mu1 - cc) / e));
-        int s = opts->s_max;
-        if (amp > 1.0) {
-            if (!isfinite(amp)) s = 1;
-            else s = (int)std::min<double>(std::max<double>(floor(8.0 / log10(amp)), 1.0), opts->s_max);
-        }
+        int s = sweeps_rule(amp, opts->s_max, opts->range_digits);
         CUDA_TRY(cudaMemsetAsync(c->dinfo + INFO_BAD, 0, sizeof(int), c->stream));
         if (opts->inner == 1) {
             // the paper's inner stop: every maxit_2 = 5 sweeps, at most maxit_1 = 10

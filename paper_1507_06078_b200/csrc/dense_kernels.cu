@@ -999,6 +999,7 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     int64_t rps = (n + ns - 1) / ns;
     rps = (rps + KS - 1) / KS * KS;
     dim3 grid((m1 + TILE - 1) / TILE, (m2 + TILE - 1) / TILE, ns);
+    const int ev0 = t_mark(c);  // the DMMA kernel alone (eig_kernel_times phase 6)
 #if ARR_DMMA_CA
     if (gram_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(Y, ldy) &&
         gram_variant(gram_tile_choice(), c, X, ldx, m1, Y, ldy, m2, n, rps, ns, sym, partials)) {
@@ -1010,6 +1011,8 @@ void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const dou
     } else
 #endif
     gram_kernel<<<grid, THREADS, 0, c->stream>>>(X, ldx, m1, Y, ldy, m2, n, rps, sym, partials);
+    // algorithmic flops: 2 n m1 m2, the upper triangle n m (m + 1) for a symmetric Gram
+    t_add(c, 6, ev0, t_mark(c), 1, sym ? (double)n * m1 * (m1 + 1.0) : 2.0 * n * m1 * m2);
     gram_reduce_kernel<<<nblk((int64_t)m1 * m2, 256), 256, 0, c->stream>>>(partials, ns, m1, m2, sym, G, ldg);
     c->launches += 2;
 }
@@ -1018,6 +1021,7 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out, int64_t ldo,
                  int64_t n, int upper) {
     const unsigned grid = (unsigned)(((n + TILE - 1) / TILE) * ((m2 + TILE - 1) / TILE));
+    const int ev0 = t_mark(c);  // eig_kernel_times phase 7
 #if ARR_DMMA_CA
     if (dmma_tile_choice() > 0 && ca_ok(X, ldx) && ca_ok(B, ldb) &&
         gemm_variant(dmma_tile_choice(), c, alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper)) {
@@ -1030,6 +1034,10 @@ void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t
     } else
 #endif
     gemm_kernel<<<grid, THREADS, 0, c->stream>>>(alpha, X, ldx, m1, B, ldb, m2, beta, Cin, ldc, Out, ldo, n, upper);
+    // algorithmic flops: 2 n m1 m2; B upper triangular: 2 n sum_c min(c + 1, m1)
+    const double mults = !upper ? (double)m1 * m2
+                                : (m2 >= m1 ? 0.5 * m1 * (m1 + 1.0) + (double)(m2 - m1) * m1 : 0.5 * m2 * (m2 + 1.0));
+    t_add(c, 7, ev0, t_mark(c), 1, 2.0 * n * mults);
     c->launches++;
 }
 

@@ -33,6 +33,7 @@
 #define ARR_MAX_W 2048  // largest block width a fused SpMM launch handles
 #define ARR_MAX_P 16    // deepest ARR augmentation (the paper uses p <= 3)
 constexpr int kPhases = 6;
+constexpr int kPhasesAll = 8;  // + 6 = DMMA Gram kernels, 7 = DMMA GEMM kernels (eig_kernel_times)
 constexpr int kOmegaCols = 8;  // columns of the re-orthogonality sketch (api.cu arr_core)  // eig_phase_times: filter, arr, residuals, arr.orth, arr.H, arr.eig
 
 // Row-partition plan of one rank (comm.cu; arr_dist in include/arrabit.h).
@@ -168,10 +169,11 @@ struct arr_ctx {
     bool timing;
     std::vector<cudaEvent_t> ev_pool;
     int ev_next;
-    struct Pending { int phase, e0, e1; int64_t count; };
+    struct Pending { int phase, e0, e1; int64_t count; double work; };
     std::vector<Pending> pending;
-    double phase_ms[6];
-    int64_t phase_cnt[6];
+    double phase_ms[kPhasesAll];
+    int64_t phase_cnt[kPhasesAll];
+    double phase_work[kPhasesAll];  // algorithmic flops of the timed DMMA launches (phases 6, 7)
     // multi-GPU (eig_init_dist): communicator, partition plan, allreduce staging
     arr_comm *comm;
     int nranks;  // size of comm (1 without one)
@@ -276,6 +278,22 @@ void comm_free_plan(arr_ctx *c);
 
 // ---------------------------------------------------------------- dense (DMMA)
 int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym);
+// phase timing (eig_set_timing): an event on the context stream (-1 when timing is off) and a
+// pending (phase, start, end, count, algorithmic flops) interval resolved at the next sync
+inline int t_mark(arr_ctx *c) {
+    if (!c->timing) return -1;
+    if (c->ev_next == (int)c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        c->ev_pool.push_back(e);
+    }
+    const int i = c->ev_next++;
+    cudaEventRecord(c->ev_pool[i], c->stream);
+    return i;
+}
+inline void t_add(arr_ctx *c, int phase, int e0, int e1, int64_t count, double work = 0.0) {
+    if (e0 >= 0 && e1 >= 0) c->pending.push_back({phase, e0, e1, count, work});
+}
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
                  int32_t m2, int64_t n, double *G, int64_t ldg, double *partials);
 // upper != 0: B is upper triangular (exact zeros below the diagonal are skipped)

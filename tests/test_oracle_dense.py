@@ -128,10 +128,15 @@ def test_arr_beats_rr_on_flat_spectrum():
 
 
 def test_sweeps_rule():
-    # amp <= 1 -> s_max; amp = 1e8 -> 1; amp = 10^(8/3) -> 3
+    # amp <= 1 -> s_max; else floor(D / log10 amp) clamped to [1, s_max]: the thresholds of
+    # amp for s = 1, 2, 3 sit at 10^D, 10^(D/2), 10^(D/3) (D = 12 default, D = 8 the round-1 value)
+    assert oracle.RANGE_DIGITS == 12.0
     assert oracle.sweeps_rule(0.5, 0.0, 1.0, 10, 5) == 5
-    d = 1
-    # T_1(t) = t: choose mu1 so that (mu1 - c)/e = 1e8
-    assert oracle.sweeps_rule(1e8 * 0.5 + 0.5, 0.0, 1.0, d, 5) == 1
-    assert oracle.sweeps_rule(10 ** (8 / 3.0 + 1e-9) * 0.5 + 0.5, 0.0, 1.0, d, 5) == 2
-    assert oracle.sweeps_rule(10 ** (8 / 3.0 - 1e-6) * 0.5 + 0.5, 0.0, 1.0, d, 5) == 3
+    d = 1  # T_1(t) = t: mu1 = amp * e + c gives (mu1 - c)/e = amp with c = e = 0.5
+    for D in (8.0, 12.0):
+        kw = {} if D == 12.0 else {"digits": D}
+        assert oracle.sweeps_rule(10 ** (D + 1e-9) * 0.5 + 0.5, 0.0, 1.0, d, 5, **kw) == 1
+        assert oracle.sweeps_rule(10 ** (D / 2 - 1e-6) * 0.5 + 0.5, 0.0, 1.0, d, 5, **kw) == 2
+        assert oracle.sweeps_rule(10 ** (D / 3.0 + 1e-9) * 0.5 + 0.5, 0.0, 1.0, d, 5, **kw) == 2
+        assert oracle.sweeps_rule(10 ** (D / 3.0 - 1e-6) * 0.5 + 0.5, 0.0, 1.0, d, 5, **kw) == 3
+        assert oracle.sweeps_rule(10 ** (D / 7.0) * 0.5 + 0.5, 0.0, 1.0, d, 5, **kw) == 5  # capped at s_max
