@@ -815,7 +815,10 @@ int gram_tile_choice() {
     X(8, 64, 64, 32, 32, 16, 3, 4, true)    \
     X(9, 64, 128, 32, 64, 16, 3, 2, true)   \
     X(10, 128, 64, 64, 32, 16, 3, 2, true)  \
-    X(11, 64, 64, 32, 32, 32, 3, 2, true)
+    X(11, 64, 64, 32, 32, 32, 3, 2, true)   \
+    X(12, 128, 128, 32, 64, 16, 3, 1, true) \
+    X(13, 128, 64, 32, 32, 16, 3, 2, true)  \
+    X(14, 64, 128, 32, 32, 16, 3, 2, true)
 
 struct VarInfo {
     int BM, BN;

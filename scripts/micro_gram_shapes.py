@@ -68,7 +68,7 @@ class Diag:  # identity CSR of order n: the context only needs A.n for the dense
 
 def main():
     cub = "--no-cublas" not in sys.argv
-    tag = f"arr(tile variant {os.environ.get('ARRABIT_DMMA_TILE', '0')})"
+    tag = f"arr(gemm variant {os.environ.get('ARRABIT_DMMA_TILE', '0')}, gram variant {os.environ.get('ARRABIT_DMMA_GRAM', os.environ.get('ARRABIT_DMMA_TILE', '7'))})"
     only_cublas = "--cublas-only" in sys.argv
     syrk = cublas_syrk() if cub else None
     for n, m1, m2 in SHAPES:
