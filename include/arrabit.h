@@ -293,12 +293,18 @@ arr_status eig_set_filter(arr_ctx *c, int32_t kind);
  * X <- T_d((A - cI)/e) X by the three-term recurrence
  *   Y_0 = X, Y_1 = (A Y_0 - c Y_0)/e, Y_{j+1} = (2/e)(A Y_j - c Y_j) - Y_{j-1}
  * (Eq. cheby-poly P:377-383 on the map of Eq. rhod; Alg. Arrabit2
- * line P:1486), one fused SpMM kernel per degree.  If normalize != 0, every
+ * line P:1486), one fused SpMM kernel per degree.  If normalize == 1, every
  * column is then scaled to unit 2-norm (MPM) and, when
  * colnorm_dev != NULL, the pre-normalisation norms are written there (device
- * [w]).  X: device n x w, row-major, ldx >= w.  Uses the context scratch block.
- * Returns ARR_ENUMERIC if a norm is zero or not finite (checked only when
- * normalize != 0; this synchronises the stream). */
+ * [w]).  normalize == 2 (lazy, Survey §8a A2): the norms are computed and checked
+ * but X is left unscaled; the scale D = 1/norm is kept pending and an IMMEDIATELY
+ * following filter_step on the same X folds it into its first two degrees
+ * (p_d(A)(X D) = p_d(A) X D), saving one pass over the block; any other call on the
+ * context drops it (X then simply stays unnormalised).  d odd, the interpolant filter
+ * or colnorm_dev != NULL normalise eagerly instead.  X: device n x w, row-major,
+ * ldx >= w.  Uses the context scratch block.  Returns ARR_ENUMERIC if a norm is zero
+ * or not finite (checked only when normalize != 0; this synchronises the stream);
+ * ARR_EINVAL for normalize outside {0, 1, 2}. */
 arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev);
 
 /* ---------------------------------------------------------------- A3 (test hook)

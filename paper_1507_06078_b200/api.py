@@ -266,10 +266,13 @@ class EigContext:
         self._check(self.lib.eig_set_filter(self.h, self.FILTERS[kind]), "eig_set_filter")
 
     # -- A1/A2
-    def filter_step(self, X: torch.Tensor, normalize: bool = True, colnorm: torch.Tensor | None = None):
+    def filter_step(self, X: torch.Tensor, normalize: bool | str = True, colnorm: torch.Tensor | None = None):
+        """normalize: True (unit columns), False, or "lazy" (norms pending for the next
+        filter_step on the same X, include/arrabit.h)."""
         px, ld, _ = _blk(X, "X")
         cn = ctypes.c_void_p(colnorm.data_ptr()) if colnorm is not None else None
-        self._check(self.lib.filter_step(self.h, px, ld, 1 if normalize else 0, cn), "filter_step")
+        mode = 2 if normalize == "lazy" else (1 if normalize else 0)
+        self._check(self.lib.filter_step(self.h, px, ld, mode, cn), "filter_step")
 
     # -- A3
     def spmm(self, X: torch.Tensor, Y: torch.Tensor, alpha: float = 1.0, shift: float = 0.0):

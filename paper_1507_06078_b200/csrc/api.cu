@@ -105,10 +105,16 @@ arr_status fail(arr_ctx *c, arr_status code, const std::string &msg) {
         arr_status st_ = (expr);                                                                    \
         if (st_ != ARR_OK) return st_;                                                              \
     } while (0)
-#define GUARD(c)                                                                                    \
+#define GUARD_KEEP(c)                                                                               \
     do {                                                                                            \
         if (!(c)) return ARR_EINVAL;                                                                \
         if ((c)->poisoned != ARR_OK) return (c)->poisoned;                                          \
+    } while (0)
+// every public call but filter_step drops a pending lazy column scale (filter_step normalize = 2)
+#define GUARD(c)                                                                                    \
+    do {                                                                                            \
+        GUARD_KEEP(c);                                                                              \
+        (c)->lazy_pending = false;                                                                  \
     } while (0)
 
 inline int64_t n_glob(const arr_ctx *c) { return c->nranks > 1 ? c->plan.n_global : c->A.n; }
@@ -272,7 +278,7 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
 // new kernel arguments).  `run` issues the launches and returns the partial-row count of
 // the last launch (< 0 on an unsupported width).  ARRABIT_GRAPH=0 launches directly.
 struct GraphKey {
-    const void *X, *T, *part, *sched_row0;
+    const void *X, *T, *part, *sched_row0, *scale_in;
     int64_t ldx;
     double a, b;
     int w, d, kind, sign, normalize, stencil;
@@ -285,6 +291,7 @@ int run_degrees(arr_ctx *c, const GraphKey &key_in, Run run) {
     GraphKey key;
     memset(&key, 0, sizeof(key));  // padding bytes compared by memcmp
     key.X = key_in.X; key.T = key_in.T; key.part = key_in.part; key.sched_row0 = key_in.sched_row0;
+    key.scale_in = key_in.scale_in;
     key.ldx = key_in.ldx; key.a = key_in.a; key.b = key_in.b; key.w = key_in.w; key.d = key_in.d;
     key.kind = key_in.kind; key.sign = key_in.sign; key.normalize = key_in.normalize; key.stencil = key_in.stencil;
     if (!(c->g_exec && c->g_key_set && key == *reinterpret_cast<const GraphKey *>(c->g_key))) {
@@ -374,7 +381,17 @@ arr_status colnorm_x(arr_ctx *c, const double *partials, int nblk, int w, double
 // result a_0 X + S b_1 - b_2.  One fused SpMM per degree (the a_k X term is the kernel's
 // fourth operand); X stays intact; b_k ping-pongs between two scratch blocks with b_k
 // overwriting b_{k+2} in place.  Result (normalised) in X.
+// A pending lazy column scale of X (filter_core normalize = 2) applied explicitly (for the
+// paths that do not fold it: the interpolant filter, odd degree counts); drops a pending
+// scale of another block.
+void lazy_materialize(arr_ctx *c, double *X, int64_t ldx) {
+    if (c->lazy_pending && c->lazy_X == X) launch_scale_cols(c, X, ldx, X, ldx, c->A.n, c->w, c->lazy);
+    c->lazy_pending = false;
+}
+
 arr_status filter_interp(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
+    lazy_materialize(c, X, ldx);
+    if (normalize == 2) normalize = 1;
     const double c0 = (c->a + c->b) / (c->a - c->b), c1 = 2.0 / (c->b - c->a);
     const std::vector<double> &a = c->coef;
     const int d = (int)a.size() - 1;
@@ -408,8 +425,8 @@ arr_status filter_interp(arr_ctx *c, double *X, int64_t ldx, int normalize, doub
         }
         return g;
     };
-    GraphKey key{X, buf[0], normalize ? c->part : nullptr, c->tile_row0, ldx, c->a, c->b, w, d, 1, c->sign, normalize,
-                 c->st.on ? 1 : 0};
+    GraphKey key{X, buf[0], normalize ? c->part : nullptr, c->tile_row0, nullptr, ldx, c->a, c->b, w, d, 1, c->sign,
+                 normalize, c->st.on ? 1 : 0};
     nblk = run_degrees(c, key, run);
     if (st != ARR_OK) return st;
     if (nblk < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
@@ -427,10 +444,19 @@ arr_status filter_interp(arr_ctx *c, double *X, int64_t ldx, int normalize, doub
     return ARR_OK;
 }
 
+// normalize: 0 none, 1 the columns of the result scaled to unit norm, 2 lazily (Survey §8a
+// A2): the norms are computed but X is left unscaled and D = 1/norm becomes pending for X;
+// the next filter_core on the same X folds D into its first two degrees (p_d(A)(X D) =
+// p_d(A)X D: degree 0's output and degree 1's Y_{j-1} term are scaled by D), which saves one
+// 16 n w-byte pass per sweep.  An odd degree count (result in the scratch block) or the
+// interpolant filter normalise eagerly.
 arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double *colnorm_dev) {
     if (c->filter_kind == 1) return filter_interp(c, X, ldx, normalize, colnorm_dev);
     const double cc = 0.5 * (c->a + c->b), e = 0.5 * (c->b - c->a);
     const int w = c->w;
+    if (normalize == 2 && (c->d % 2 == 1 || colnorm_dev)) normalize = 1;
+    const double *scale_in = (c->lazy_pending && c->lazy_X == X) ? c->lazy + (ARR_MAX_W + 2) : nullptr;
+    c->lazy_pending = false;
     double *T = c->T ? c->T : c->Q;  // lean context: the basis block Q[:, 0:w] is free during sweeps
     const int64_t lt = c->T ? ldT(c) : ldQ(c);
     double *cur = X;
@@ -452,6 +478,7 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
             } else {
                 s.Yprev = ot; s.ld_prev = ldo; s.alpha = 2.0 / e; s.beta = -1.0;
             }
+            if (scale_in && j <= 1) { s.colscale = scale_in; s.scale_mode = j == 0 ? 1 : 2; }
             s.shift = cc;
             s.Yout = ot; s.ld_out = ldo;
             s.partials = (normalize && j == c->d - 1) ? c->part : nullptr;
@@ -462,15 +489,21 @@ arr_status filter_core(arr_ctx *c, double *X, int64_t ldx, int normalize, double
         }
         return g;
     };
-    GraphKey key{X, T, normalize ? c->part : nullptr, c->tile_row0, ldx, c->a, c->b, w, c->d, 0, c->sign, normalize,
-                 c->st.on ? 1 : 0};
+    GraphKey key{X, T, normalize ? c->part : nullptr, c->tile_row0, scale_in, ldx, c->a, c->b, w, c->d, 0, c->sign,
+                 normalize != 0, c->st.on ? 1 : 0};
     nblk = run_degrees(c, key, run);
     if (st != ARR_OK) return st;
     if (nblk < 0) return fail(c, ARR_EINVAL, "filter_step: unsupported block width");
     if (c->d % 2 == 1) { cur = T; ldcur = lt; }  // Y_d is in the scratch block after an odd degree count
     t_add(c, 0, ev0, t_mark(c), c->d);
     CHECK_LAUNCH();
-    if (normalize) {
+    if (normalize == 2) {  // lazy: norms and D = 1/norm pending for X (d even: the result is in X)
+        ST_TRY(colnorm_x(c, c->part, nblk, w, c->lazy, nullptr));
+        launch_check_norms(c, c->lazy, w, c->dinfo + INFO_BAD);
+        launch_recip(c, c->lazy, w, c->lazy + (ARR_MAX_W + 2));
+        c->lazy_pending = true;
+        c->lazy_X = X;
+    } else if (normalize) {
         double *nrm = colnorm_dev ? colnorm_dev : NORM_buf(c);
         ST_TRY(colnorm_x(c, c->part, nblk, w, nrm, nullptr));
         launch_check_norms(c, nrm, w, c->dinfo + INFO_BAD);
@@ -1120,6 +1153,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         {(void **)&c->dinfo, sizeof(int) * 64},
         {(void **)&c->sched, sizeof(unsigned long long) * 2},
         {(void **)&c->omega, sizeof(double) * (size_t)w * kOmegaCols},
+        {(void **)&c->lazy, sizeof(double) * 2 * (ARR_MAX_W + 2)},
     };
     size_t total = 0;
     for (auto &x : al) {
@@ -1247,7 +1281,7 @@ arr_status eig_destroy(arr_ctx *c) {
     if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
     stencil_release(c);
     void *ptrs[] = {c->T, c->Q, c->part, c->small, c->evals, c->vecw, c->dinfo, c->sched, c->solver_work,
-                    c->trtri_dwork, c->omega};
+                    c->trtri_dwork, c->omega, c->lazy};
     for (void *p : ptrs)
         dev_free(p, c->stream);
     cudaStreamSynchronize(c->stream);
@@ -1364,7 +1398,8 @@ arr_status eig_set_filter(arr_ctx *c, int32_t kind) {
 }
 
 arr_status filter_step(arr_ctx *c, double *X, int64_t ldx, int32_t normalize, double *colnorm_dev) {
-    GUARD(c);
+    GUARD_KEEP(c);
+    if (normalize < 0 || normalize > 2) return fail(c, ARR_EINVAL, "filter_step: normalize must be 0, 1 or 2");
     Nvtx nvtx_("arrabit::filter_step");
     if (c->cs) return filter_step(c->cs->col, X, ldx, normalize, colnorm_dev);  // this rank's columns: no exchange
     if (!c->have_interval) return fail(c, ARR_EINVAL, "eig_set_interval not called");
@@ -1606,9 +1641,12 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
                 rcp = rc;
             }
         } else {
+            // MPM sweeps with the column normalisation folded lazily into the next
+            // sweep (Survey §8a A2); the sweep before the ARR normalises explicitly
+            static const bool lazy = [] { const char *e = getenv("ARRABIT_LAZY_NORM"); return !(e && atoi(e) == 0); }();
             for (int q = 0; q < s; ++q) {
                 if (opts->gn) st = gn_step(c, X, ldx);             // GN inner solver
-                else st = filter_core(c, X, ldx, 1, nullptr);      // MPM sweep
+                else st = filter_core(c, X, ldx, (lazy && q + 1 < s) ? 2 : 1, nullptr);
                 if (st != ARR_OK) return st;
             }
         }

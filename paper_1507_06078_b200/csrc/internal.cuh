@@ -93,6 +93,8 @@ struct StencilLaunch {
     double *Yout;
     int64_t ld_in, ld_prev, ld_out, ld_xa;
     double alpha, shift, beta, gxa;
+    const double *colscale;  // lazy MPM column scale (SpmmArgs::colscale) or nullptr
+    int scale_mode;          // 1: scale the output, 2: scale the Y_{j-1} term
     double *partials;
     const double *val;
     double coef[27];  // constant coefficients by DIA slot (vmode 1: off-diagonal slots; vmode 2: all)
@@ -137,6 +139,11 @@ struct arr_ctx {
     double *small;    // dense m x m buffers (H, V, B ...)
     double *evals;    // [m]
     double *vecw;     // [2*ARR_MAX_W] column norms / shifts / scales
+    // lazy MPM normalisation (filter_core normalize = 2): lazy[0, mw) = the pending column
+    // norms of lazy_X, lazy[mw, 2 mw) = their reciprocals D (mw = ARR_MAX_W + 2)
+    double *lazy;
+    const double *lazy_X;
+    bool lazy_pending;
     int *dinfo;       // cuSOLVER info + rank counters
     unsigned long long *sched;  // [2] SpMM tile ticket (zeroed at init, self-resetting)
     double *omega;              // [w x kOmegaCols] seeded Gaussian sketch of the ARR re-orthogonality check
@@ -210,6 +217,11 @@ struct SpmmArgs {
     const double *Xa;        // optional fourth operand: Yout += gxa * Xa (interpolant filter), or nullptr
     int64_t ld_xa;
     double gxa;
+    // lazy MPM normalisation (Survey §8a A2, p_d(A)(X D) = p_d(A) X D): per-column scale D,
+    // scale_mode 1 = the output is D * (...) (the first degree), 2 = the Y_{j-1} term is
+    // beta D y_prev (the second degree); 0 / nullptr = none
+    const double *colscale;
+    int scale_mode;
     double *partials;        // [gridDim.x * w] column sums of squares of the output, or nullptr
     unsigned long long *sched;  // [2] dynamic tile ticket + finished-CTA count (self-resetting)
     const int64_t *tile_row0;   // optional processing order: tile t = rows [tile_row0[t], +tile_len[t])
@@ -255,6 +267,7 @@ void launch_colnorm_root(arr_ctx *c, double *x, int32_t w, const double *mu_div)
 // X[i, col] *= 1/norm[col] (in place) or Out = In / norm
 void launch_scale_cols(arr_ctx *c, const double *In, int64_t ld_in, double *Out, int64_t ld_out,
                        int64_t n, int32_t w, const double *norms);
+void launch_recip(arr_ctx *c, const double *x, int32_t w, double *out);  // out = 1 / x
 void launch_gershgorin(arr_ctx *c, double *partial, int *nblk_out);
 void launch_rowlen_max(arr_ctx *c, int *dev_out);
 // exact-cover check of a schedule: bad = 1 unless every row is covered once

@@ -217,8 +217,9 @@ __device__ __forceinline__ void row_epilogue(const SpmmArgs &a, int64_t i, int T
         for (int e = 0; e < VEC; ++e) {
             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
             double o = epi(a.alpha, V::get(acc[v], e), sh, V::get(yi, e));
-            if (HAS_PREV) o = fma(a.beta, V::get(yp[v], e), o);
+            if (HAS_PREV) o = fma(a.scale_mode == 2 ? a.beta * __ldg(a.colscale + vv * VEC + e) : a.beta, V::get(yp[v], e), o);
             if (HAS_X) o = fma(a.gxa, V::get(xa, e), o);
+            if (a.scale_mode == 1) o *= __ldg(a.colscale + vv * VEC + e);
             V::set(out, e, o);
             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
         }
@@ -442,8 +443,11 @@ __global__ void __launch_bounds__(kMaxThreads, ARR_SPMM_MINB) spmm_tile_kernel(S
                         for (int e = 0; e < VEC; ++e) {
                             const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
                             double o = epi(a.alpha, V::get(acc, e), sh, V::get(yi, e));
-                            if (HAS_PREV) o = fma(a.beta, V::get(yp, e), o);
+                            if (HAS_PREV)
+                                o = fma(a.scale_mode == 2 ? a.beta * __ldg(a.colscale + vv * VEC + e) : a.beta,
+                                        V::get(yp, e), o);
                             if (HAS_X) o = fma(a.gxa, a.Xa[i * a.ld_xa + vv * VEC + e], o);
+                            if (a.scale_mode == 1) o *= __ldg(a.colscale + vv * VEC + e);
                             V::set(out, e, o);
                             if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                         }
@@ -676,8 +680,11 @@ __global__ void __launch_bounds__(kMaxThreads + 32, ARR_SPMM_WS_MINB) spmm_ws_ke
                     for (int e = 0; e < VEC; ++e) {
                         const double sh = COLSHIFT ? __ldg(a.colshift + vv * VEC + e) : a.shift;
                         double o = epi(a.alpha, Vv::get(acc, e), sh, Vv::get(yi, e));
-                        if (HAS_PREV) o = fma(a.beta, Vv::get(yp, e), o);
+                        if (HAS_PREV)
+                            o = fma(a.scale_mode == 2 ? a.beta * __ldg(a.colscale + vv * VEC + e) : a.beta,
+                                    Vv::get(yp, e), o);
                         if (HAS_X) o = fma(a.gxa, a.Xa[i * a.ld_xa + vv * VEC + e], o);
+                        if (a.scale_mode == 1) o *= __ldg(a.colscale + vv * VEC + e);
                         Vv::set(out, e, o);
                         if (SUMSQ) ss[v][e] = fma(o, o, ss[v][e]);
                     }
@@ -961,6 +968,18 @@ void launch_colsum(arr_ctx *c, const double *partials, int nblk, int32_t w, doub
 
 void launch_colnorm_root(arr_ctx *c, double *x, int32_t w, const double *mu_div) {
     colnorm_root_kernel<<<(w + 127) / 128, 128, 0, c->stream>>>(x, w, mu_div);
+    c->launches++;
+}
+
+namespace {
+__global__ void recip_kernel(const double *__restrict__ x, int w, double *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < w) out[i] = 1.0 / x[i];
+}
+}  // namespace
+
+void launch_recip(arr_ctx *c, const double *x, int32_t w, double *out) {
+    recip_kernel<<<(w + 255) / 256, 256, 0, c->stream>>>(x, w, out);
     c->launches++;
 }
 

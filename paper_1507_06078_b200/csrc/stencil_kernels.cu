@@ -394,6 +394,10 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
             qoff[q] = ((in || VM != 0) ? cb + Sh::dy(q) * P.box_x + Sh::dx(q) : cb) * pwv + v;
         }
         double *outp = P.Yout + (rxy + (int64_t)I.zc0 * nxy) * P.ld_out + (int64_t)(colv0 + v) * 2;
+        // lazy MPM scale of this thread's two columns (SpmmArgs::colscale)
+        double2 csc = make_double2(1.0, 1.0);
+        if (P.scale_mode != 0 && act) csc = __ldg(reinterpret_cast<const double2 *>(P.colscale) + colv0 + v);
+        const double2 bsc = P.scale_mode == 2 ? make_double2(P.beta * csc.x, P.beta * csc.y) : make_double2(P.beta, P.beta);
         const int64_t out_step = nxy * P.ld_out;
         double2 accA = make_double2(0.0, 0.0), accB = make_double2(0.0, 0.0), yiA = make_double2(0.0, 0.0);
         const int zs = max(I.zc0 - 1, 0);
@@ -458,12 +462,16 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                 out.x = epi(P.alpha, accA.x, P.shift, yiA.x);
                 out.y = epi(P.alpha, accA.y, P.shift, yiA.y);
                 if (HAS_PREV) {
-                    out.x = fma(P.beta, yp.x, out.x);
-                    out.y = fma(P.beta, yp.y, out.y);
+                    out.x = fma(bsc.x, yp.x, out.x);
+                    out.y = fma(bsc.y, yp.y, out.y);
                 }
                 if (HAS_X) {
                     out.x = fma(P.gxa, xa.x, out.x);
                     out.y = fma(P.gxa, xa.y, out.y);
+                }
+                if (P.scale_mode == 1) {
+                    out.x *= csc.x;
+                    out.y *= csc.y;
                 }
                 if (SUMSQ) {
                     ss0 = fma(out.x, out.x, ss0);
@@ -817,6 +825,7 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     L.Yout = a.Yout; L.ld_out = a.ld_out;
     L.Xa = a.Xa; L.ld_xa = a.ld_xa;
     L.alpha = a.alpha; L.shift = a.shift; L.beta = a.beta; L.gxa = a.gxa;
+    L.colscale = a.colscale; L.scale_mode = a.colscale ? a.scale_mode : 0;
     L.partials = a.partials;
     const StencilState &S = c->st;
     if (!encode_4d(&L.tm_in, a.Yin, a.w, a.ld_in, S.nx, S.ny, S.nz, 2 * L.pwv, L.box_x, L.box_y) ||

@@ -163,3 +163,55 @@ def test_stencil_solve_and_arr(arr, kind):
     assert np.max(np.abs(outs[True][0] - outs[False][0]) / np.abs(outs[False][0])) <= 1e-13
     lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
     assert np.max(np.abs(outs[True][0] - lam) / np.abs(lam)) <= 1e-10
+
+
+# ---------------------------------------------------------------- lazy MPM normalisation
+@pytest.mark.parametrize("kind", ["lap2d_xz", "lap3dV", "lap3dV_even", "st27", "st27_var"])
+@pytest.mark.parametrize("w", [24, 98])
+@pytest.mark.parametrize("d", [1, 2, 6])
+def test_lazy_normalisation(arr, kind, w, d):
+    """filter_step(normalize="lazy") leaves X = p_d(A) X unscaled with its norms pending; the
+    next filter_step on the same X folds D = 1/norm into its first two degrees, so its output
+    is p_d(A) applied to the NORMALISED block (Survey §8a A2: p_d(A)(X D) = p_d(A) X D).
+    Checked against the oracle on both kernel families; any other call in between drops the
+    pending scale; d odd normalises eagerly."""
+    mk, grid, _ = CASES[kind]
+    A = mk()
+    X0 = synth.gaussian_block(A.n, w, 7)
+    c_csr, c_st = _pair(arr, A, grid, w, d)
+    a = c_csr.eig_gershgorin_lower()
+    b = a + 0.7 * (float(np.abs(A.val).max()) * 8 - a)
+    outs = []
+    for ctx in (c_csr, c_st):
+        ctx.eig_set_interval(a, b)
+        X = dev_block(X0, w + 2)
+        ctx.filter_step(X, normalize="lazy")
+        Y1 = X.cpu().numpy().copy()
+        ctx.filter_step(X, normalize=False)
+        outs.append((Y1, X.cpu().numpy().copy()))
+    y1 = oracle.cheb_filter(A, a, b, d, X0)
+    if d % 2 == 1:  # an odd degree count normalises eagerly (the result sits in the scratch block)
+        y1 = oracle.mpm_sweep(A, a, b, d, X0)
+    y2 = oracle.cheb_filter(A, a, b, d, oracle.mpm_sweep(A, a, b, d, X0))
+    for Y1, Y2 in outs:
+        assert relF(Y1, y1) <= 1e-12, "lazy sweep output is the unscaled p_d(A) X"
+        assert relF(Y2, y2) <= 1e-12, "the pending scale is folded into the next sweep"
+    # the two families reduce the column norms in different orders (different CTA partials),
+    # so D, and with it the folded sweep, agree to rounding only
+    assert relF(outs[0][1], outs[1][1]) <= 1e-14
+    # dropped by any other call: the next sweep filters the unscaled block
+    ctx = c_csr
+    X = dev_block(X0, w + 2)
+    ctx.filter_step(X, normalize="lazy")
+    ctx.eig_phase_times()
+    ctx.filter_step(X, normalize=False)
+    assert relF(X.cpu().numpy(), oracle.cheb_filter(A, a, b, d, y1)) <= 1e-12
+    # a lazy sweep followed by an eager one equals two MPM sweeps
+    X = dev_block(X0, w + 2)
+    ctx.filter_step(X, normalize="lazy")
+    ctx.filter_step(X, normalize=True)
+    ref = oracle.mpm_sweep(A, a, b, d, oracle.mpm_sweep(A, a, b, d, X0))
+    assert relF(X.cpu().numpy(), ref) <= 1e-12
+    assert np.max(np.abs(np.linalg.norm(X.cpu().numpy(), axis=0) - 1.0)) <= 1e-14
+    for cx in (c_csr, c_st):
+        cx.close()
