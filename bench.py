@@ -496,7 +496,10 @@ def run_ours(args):
     elif partitioned:
         ps = _partition_spec(spec)
         bounds = pt.bounds_planes(ps[1], ps[2], world) if ps[0] == "planes" else pt.bounds_balanced(A.row_ptr, world)
-        plan = pt.local_plan(A, bounds, rank)
+        # 3-D grids: each rank's interior tiles in y-band order (the row order the CSR kernels
+        # run on one GPU without the stencil path; results unchanged)
+        yband = (spec.size, spec.size, {"lap3dV": 10, "st27": 8}[spec.kind]) if spec.kind in ("lap3dV", "st27") else None
+        plan = pt.local_plan(A, bounds, rank, yband=yband)
         Aloc = plan
         r0, r1 = plan.row_begin, plan.row_begin + plan.n_own
         nrows = plan.n_rows_block
@@ -677,7 +680,7 @@ def run_ours(args):
         par = ("1 GPU" if world == 1 else
                (f"column split over {world} GPUs (A replicated, column-local filter, ARR on a balanced row "
                 f"partition; NCCL all-to-all transposes + halo/all-gather + allreduce)" if colsplit else
-                f"row partition over {world} GPUs ({_partition_spec(spec)[0]}), NCCL halo/all-gather + allreduce"
+                f"row partition over {world} GPUs ({_partition_spec(spec)[0]}" + (", interior tiles in y-band order" if spec.kind in ("lap3dV", "st27") else "") + "), NCCL halo/all-gather + allreduce"
                 if partitioned else f"{world} independent replicas (no collective)"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

@@ -97,9 +97,36 @@ class LocalPlan:
         return self.n_own
 
 
-def local_plan(A, bounds: np.ndarray, rank: int) -> LocalPlan:
+def _yband_tiles(mask: np.ndarray, row_begin: int, nx: int, ny: int, band: int):
+    """The rows of `mask` (local ids of owned rows, global id = row_begin + local) in y-band
+    order on an nx x ny x nz grid (x fastest): for each band of `band` y-lines, for each
+    z-plane, the band's contiguous rows of that plane, cut into tiles of <= TILE rows.  The
+    same rows as _runs_to_tiles(mask), in the order that keeps a band's gathered neighbour
+    rows (y +- 1 lines, z +- 1 planes) L2-resident (schedule.yband_3d)."""
+    n = mask.shape[0]
+    plane = nx * ny
+    z0, z1 = row_begin // plane, (row_begin + n - 1) // plane + 1
+    r0s, lens = [], []
+    for yb in range(0, ny, band):
+        h = min(band, ny - yb)
+        for z in range(z0, z1):
+            g0 = z * plane + yb * nx
+            a, b = max(g0, row_begin), min(g0 + h * nx, row_begin + n)
+            if a >= b:
+                continue
+            t0, tl = _runs_to_tiles(mask[a - row_begin:b - row_begin])
+            r0s.append(t0 + (a - row_begin))
+            lens.append(tl)
+    if not r0s:
+        return np.zeros(0, np.int64), np.zeros(0, np.int32)
+    return np.concatenate(r0s).astype(np.int64), np.concatenate(lens).astype(np.int32)
+
+
+def local_plan(A, bounds: np.ndarray, rank: int, yband: tuple | None = None) -> LocalPlan:
     """The local CSR and exchange plan of `rank` for the row blocks `bounds`
-    (bounds[r] .. bounds[r+1]-1 are rank r's rows)."""
+    (bounds[r] .. bounds[r+1]-1 are rank r's rows).  yband = (nx, ny, band): the interior
+    tiles in y-band order of an nx x ny x nz grid (results unchanged: only the order in
+    which rows are computed moves)."""
     size = len(bounds) - 1
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     n_own = r1 - r0
@@ -128,14 +155,14 @@ def local_plan(A, bounds: np.ndarray, rank: int) -> LocalPlan:
     send_rows = (np.concatenate(send_lists) if send_lists else np.zeros(0)).astype(np.int32)
     boundary = np.zeros(n_own, dtype=bool)
     boundary[e_rows] = True
-    int_row0, int_len = _runs_to_tiles(~boundary)
+    int_row0, int_len = _runs_to_tiles(~boundary) if yband is None else _yband_tiles(~boundary, r0, *yband)
     bnd_row0, bnd_len = _runs_to_tiles(boundary)
     return LocalPlan(rank, size, int(A.n), r0, n_own, n_ghost, rp, loc.astype(np.int32), vals, ghost_global,
                      peers, send_off, send_rows, recv_off, int_row0, int_len, bnd_row0, bnd_len)
 
 
-def plans(A, bounds: np.ndarray) -> list[LocalPlan]:
-    return [local_plan(A, bounds, r) for r in range(len(bounds) - 1)]
+def plans(A, bounds: np.ndarray, yband: tuple | None = None) -> list[LocalPlan]:
+    return [local_plan(A, bounds, r, yband) for r in range(len(bounds) - 1)]
 
 
 def check_plans(ps: list[LocalPlan]) -> None:

@@ -62,10 +62,10 @@ def run_ranks(G, fn):
     return out
 
 
-def make_rank(arr, A, G, spec, k, p, d, w=None):
+def make_rank(arr, A, G, spec, k, p, d, w=None, yband=None):
     """Plans, communicators and a per-rank factory of (ctx, plan, stream)."""
     pt = arr.partition
-    ps = pt.plans(A, _bounds(pt, A, spec, G))
+    ps = pt.plans(A, _bounds(pt, A, spec, G), yband=yband)
     comms = arr.Comm.local_group(G)
 
     def ctx_of(r):
@@ -84,9 +84,12 @@ def to_rank_block(X, plan, ld=None):
     return blk[:, :X.shape[1]]
 
 
-@pytest.mark.parametrize("kind,G", [("lap3dV", 2), ("lap3dV", 3), ("zipf", 2), ("zipf", 3), ("st27", 4),
-                                    ("lap2d", 2)])
-def test_dist_filter_bitwise_and_normalised(arr, kind, G):
+@pytest.mark.parametrize("kind,G,yb", [("lap3dV", 2, None), ("lap3dV", 3, None), ("zipf", 2, None), ("zipf", 3, None),
+                                       ("st27", 4, None), ("lap2d", 2, None), ("lap3dV", 2, (13, 13, 4)),
+                                       ("st27", 3, (11, 11, 3))])
+def test_dist_filter_bitwise_and_normalised(arr, kind, G, yb):
+    """yb: the interior tiles in y-band order (partition.local_plan(yband=...), bench.py's
+    N > 1 default on the 3-D grids): the row order moves, the sums do not."""
     mk, sp = CASES[kind]
     A = mk()
     k, d = 24, 9
@@ -102,7 +105,7 @@ def test_dist_filter_bitwise_and_normalised(arr, kind, G):
     X1 = torch.from_numpy(X0).cuda()
     c1.filter_step(X1, normalize=True)
     ref_nrm = X1.cpu().numpy()
-    ps, comms, ctx_of = make_rank(arr, A, G, sp(G), k, 1, d)
+    ps, comms, ctx_of = make_rank(arr, A, G, sp(G), k, 1, d, yband=yb)
 
     def work(r):
         ctx, s = ctx_of(r)

@@ -173,3 +173,26 @@ def test_gloo_world2_distributed_sweep_matches_oracle(kind):
     err, gerr = q.get(timeout=5)
     assert err <= 1e-12, err
     assert gerr <= 1e-12, gerr
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+@pytest.mark.parametrize("band", [1, 3, 9])
+def test_yband_interior_order_same_rows(G, band):
+    """z-slab plans with the interior tiles in y-band order (bench.py's N > 1 default on the
+    3-D grids): the same interior rows, each exactly once, tiles <= TILE rows, and the order
+    is band-major (all planes of a band before the next band)."""
+    N = 9
+    A = synth.laplacian_3d_potential(N, 2)
+    bounds = pt.bounds_planes(N, N * N, G)
+    nat = pt.plans(A, bounds)
+    yb = pt.plans(A, bounds, yband=(N, N, band))
+    pt.check_plans(yb)
+    for p, q in zip(nat, yb):
+        assert np.array_equal(p.bnd_row0, q.bnd_row0) and np.array_equal(p.bnd_len, q.bnd_len)
+        rows_p = np.concatenate([np.arange(r, r + ln) for r, ln in zip(p.int_row0, p.int_len)] or [np.zeros(0, int)])
+        rows_q = np.concatenate([np.arange(r, r + ln) for r, ln in zip(q.int_row0, q.int_len)] or [np.zeros(0, int)])
+        assert len(rows_q) == len(set(rows_q.tolist())) and np.array_equal(np.sort(rows_p), np.sort(rows_q))
+        assert (q.int_len <= pt.TILE).all()
+        if len(rows_q):
+            yline = ((rows_q + q.row_begin) // N) % N
+            assert (np.diff(yline // band) >= 0).all(), "band-major order"
