@@ -521,13 +521,22 @@ def run_ours(args):
     # host memory before each step, outside the timed region
     blk = 8 * nrows * (c1 - c0)
     x0_on_host = blk * (spec.p + 4) > 0.9 * torch.cuda.get_device_properties(dev).total_memory
+    # the solve's block X with 128-byte rows (leading dimension rounded up to 16 doubles, the
+    # layout eig_solve_host and the library's own blocks use: TMA boxes and 16-byte vectors
+    # start on sector boundaries)
+    ldp = (X0h.shape[1] + 15) // 16 * 16
+
+    def padded(rows, cols):
+        return torch.empty((rows, ldp), dtype=torch.float64, device=dev)[:, :cols]
+
     with torch.cuda.stream(stream):
         if x0_on_host:
             X0 = torch.from_numpy(X0h).pin_memory()
-            X = torch.empty(X0.shape, dtype=torch.float64, device=dev)
+            X = padded(*X0.shape)
         else:
-            X0 = torch.from_numpy(X0h).to(dev)
-            X = torch.empty_like(X0)
+            X0 = padded(*X0h.shape)
+            X0.copy_(torch.from_numpy(X0h).to(dev))
+            X = padded(*X0.shape)
         flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)  # > 126 MB L2
     stream.synchronize()
     if partitioned:
@@ -594,8 +603,12 @@ def run_ours(args):
         try:
             A2, spec2 = configs.build_config(2)
             with torch.cuda.stream(stream):
-                X02 = torch.from_numpy(configs.starting_block(spec2)).to(dev)
-                X2 = torch.empty_like(X02)
+                x02 = torch.from_numpy(configs.starting_block(spec2)).to(dev)
+                ld2 = (x02.shape[1] + 15) // 16 * 16  # 128-byte rows, as for the main workload
+                X02 = torch.empty((x02.shape[0], ld2), dtype=torch.float64, device=dev)[:, :x02.shape[1]]
+                X02.copy_(x02)
+                X2 = torch.empty((x02.shape[0], ld2), dtype=torch.float64, device=dev)[:, :x02.shape[1]]
+                del x02
             args2 = argparse.Namespace(**vars(args))
             args2.config = 2
             r2 = solve_run(arr, torch, spec2, A2, A2, X02, X2, flush, stream, dev, args2, 3, 2)
