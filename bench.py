@@ -404,7 +404,8 @@ def load_fp64_peak():
 
 
 def _traffic(cid, family):
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json" if family != "gram" else f"ncu_traffic_gram_cfg{cid}.json")
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{family}_cfg{cid}.json" if family in ("gram", "gemm")
+                      else f"ncu_traffic_cfg{cid}.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:
@@ -452,10 +453,10 @@ def roofline_of(r, spec, nrow, nnz, args, steps, cid=None, w=None):
              "flops_per_launch": fl / cnt, "flops_model": "2 n m1 m2 (symmetric Gram n m (m+1); upper-triangular B "
              "2 n sum_c min(c+1, m1)), summed over the step's launches of every shape",
              "avg_launch_us": ms * 1e3 / cnt, "launches": cnt, "peak_source": pk64_src, "share_of_step": ms / st}
-        if name == "dmma_gram":
-            tj, tr, ts = _traffic(cid, "gram")
-            if tj is not None:
-                o["traffic"], o["traffic_source"] = tr, ts
+        tj, tr, ts = _traffic(cid, name[5:])  # profiles/ncu_traffic_{gram,gemm}_cfg<N>.json
+        if tj is not None:
+            o["traffic"], o["traffic_source"] = tr, ts
+            o["traffic_note"] = "mean DRAM bytes per launch over the launches of one ARR (ncu --set full)"
         dmma[name] = o
     kinds = {"filter": filt, **dmma}
     dom = max(kinds, key=lambda k: kinds[k]["share_of_step"])

@@ -56,19 +56,29 @@ void solver_release(cusolverDnHandle_t h) {
 }
 
 // Device memory of contexts and of the host-buffer entry: stream-ordered
-// allocations from the device's default pool, which keeps up to 4 GiB between
-// calls (repeated eig_solve_host calls reuse it instead of cudaMalloc/cudaFree).
+// allocations from the device's default pool.  The pool keeps, between calls, up to
+// the largest footprint a context has needed so far (at least 4 GiB, at most a quarter
+// of the device; ARRABIT_POOL_KEEP=0: 4 GiB), so repeated eig_solve_host calls reuse
+// their memory instead of mapping it again (cudaMemPoolTrimTo releases it).
+std::mutex g_pool_keep_mu;
+uint64_t g_pool_keep = 0;
+void pool_keep_at_least(uint64_t bytes) {
+    static const bool on = [] { const char *e = getenv("ARRABIT_POOL_KEEP"); return !(e && atoi(e) == 0); }();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t thr = std::max<uint64_t>((uint64_t)4 << 30, on ? std::min<uint64_t>(bytes, total_b / 4) : 0);
+    std::lock_guard<std::mutex> lk(g_pool_keep_mu);
+    if (thr <= g_pool_keep) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess)
+        g_pool_keep = thr;
+}
 cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t s) {
     static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = (uint64_t)4 << 30;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    });
+    std::call_once(once, [] { pool_keep_at_least(0); });
     return cudaMallocAsync(p, bytes, s);
 }
 void dev_free(void *p, cudaStream_t s) {
@@ -1754,6 +1764,9 @@ arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const 
     }
     arr_csr A{n, nnz, d_rp, d_ci, d_val};
     st = eig_init_w(&c, &A, k, w, p, d, stream);
+    if (st == ARR_OK)  // keep this call's footprint in the pool for the next call (dev_alloc)
+        pool_keep_at_least((uint64_t)c->ws_bytes + sizeof(double) * (uint64_t)n * ldx +
+                           (sizeof(int64_t) * (n + 1) + (sizeof(int32_t) + sizeof(double)) * (uint64_t)nnz));
     if (st == ARR_OK && (opts->grid[0] || opts->grid[1] || opts->grid[2]))
         st = eig_set_stencil(c, opts->grid[0], opts->grid[1], opts->grid[2]);
     if (st == ARR_OK) st = eig_solve(c, d_X, ldx, opts, eigval, res, info);

@@ -30,7 +30,8 @@ def main(rep, cid, family, source=None):
     per = sum(o["dram_read"] + o["dram_write"] for o in out) / len(out)
     doc = {"kernel_family": family, "dram_bytes_per_launch": per, "launches_profiled": out,
            "source": source or rep, "how": "ncu --set full --clock-control none: dram__bytes_read.sum + dram__bytes_write.sum"}
-    name = f"profiles/ncu_traffic_gram_cfg{cid}.json" if family == "gram" else f"profiles/ncu_traffic_cfg{cid}.json"
+    name = (f"profiles/ncu_traffic_{family}_cfg{cid}.json" if family in ("gram", "gemm")
+            else f"profiles/ncu_traffic_cfg{cid}.json")
     with open(name, "w") as f:
         json.dump(doc, f, indent=1)
     print(json.dumps({"cfg": cid, "dram_bytes_per_launch": per}))
