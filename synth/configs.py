@@ -50,7 +50,10 @@ CONFIGS = {
     2: ConfigSpec("cfg2_lap2d_300x300", "lap2d", 300, k=200, d=20, p=1, seed=1),
     3: ConfigSpec("cfg3_lap3d_100^3_plusV", "lap3dV", 100, k=500, d=20, p=2, seed=2, gpus="1/2/4/8"),
     4: ConfigSpec("cfg4_zipf_n4e6", "zipf", 4_000_000, k=1000, d=15, p=1, seed=3, gpus="1/2/4/8"),
-    5: ConfigSpec("cfg5_st27_256^3", "st27", 256, k=256, d=30, p=2, seed=4, gpus="1/2/4/8"),
+    # cfg5: the sweeps cap s_max = 10 (R6): |T_30| amplifies the top Ritz direction only
+    # ~2.4x per sweep, so the dynamic-range rule would allow ~30 sweeps and the cap binds; measured
+    # on B200 (profiles/r02/cfg5_smax.log): s_max 5 -> 14 outer / 97.5 s, 10 -> 7 outer / 68.9 s
+    5: ConfigSpec("cfg5_st27_256^3", "st27", 256, k=256, d=30, p=2, seed=4, gpus="1/2/4/8", s_max=10),
 }
 
 # Small analogues of every config generator (oracle-solvable in seconds).
