@@ -239,10 +239,17 @@ def oracle_step_estimate(A, spec, cid):
                f"({ta:.2f} s) on the full block, extrapolated to the oracle's own full solve ({S} sweeps, {O} ARR)")
         return S * ts + O * ta, smp
     gold = oracle_golden(cid)
-    S = gold["sweeps"] if gold else 24
+    import oracle
+    # the golden solve's sweep count when it ran under the current sweeps rule (R6);
+    # else the count of the GPU solve under the same rule (profiles/r02: cfg3 18, cfg5 56)
+    same_rule = bool(gold) and float(gold.get("range_digits", 8.0)) == float(oracle.RANGE_DIGITS)
+    gpu_counts = {3: 18, 5: 56}
+    S = gold["sweeps"] if same_rule else gpu_counts.get(cid, 24)
+    src = ("the oracle golden solve" if same_rule else
+           "the GPU solve's count under the same sweeps rule" if cid in gpu_counts else "assumed")
     ts = oracle_filter_sample(A, spec) * spec.w / 16
     smp = (f"{spec.name}: one MPM sweep of 16 of the {spec.w} columns ({ts * 16 / spec.w:.2f} s) x w/16, "
-           f"extrapolated to {S} sweeps ({'the oracle golden solve' if gold else 'assumed'}); ARR not sampled")
+           f"extrapolated to {S} sweeps ({src}); ARR not sampled")
     return S * ts, smp
 
 

@@ -43,7 +43,7 @@ def main():
     out = {
         "source": "scripts/oracle_golden.py (oracle/ only)",
         "config": spec.name, "n": int(A.n), "nnz": int(A.nnz), "k": spec.k, "w": spec.w, "d": spec.d, "p": spec.p,
-        "seed": spec.seed, "tol": spec.tol, "arr_method": args.arr,
+        "seed": spec.seed, "tol": spec.tol, "arr_method": args.arr, "range_digits": float(oracle.RANGE_DIGITS),
         "converged": bool(r.converged), "outer": r.outer, "sweeps": r.sweeps,
         "max_residual": float(r.res.max()), "eigenvalues": [float(x) for x in r.mu],
         "residuals": [float(x) for x in r.res], "seconds": time.time() - t0,
