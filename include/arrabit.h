@@ -377,7 +377,10 @@ arr_status eig_solve(arr_ctx *c, double *X, int64_t ldx, const arr_solve_opts *o
  * (n x w, row-major, ld = w; w >= k, w - k guard columns) from host memory to
  * the device, runs eig_solve on a fresh context, copies the k eigenvalues,
  * residuals and eigenvectors (n x k, row-major, ld = k; evec may be NULL) back.
- * All host pointers; device memory is allocated and freed inside. */
+ * All host pointers; device memory is allocated and freed inside, from the device's
+ * default stream-ordered pool, which keeps up to min(this call's footprint, a quarter
+ * of the device) cached for the next call (ARRABIT_POOL_KEEP=0: 4 GiB;
+ * cudaMemPoolTrimTo on the default pool releases it). */
 arr_status eig_solve_host(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
                           const double *val, int32_t k, int32_t w, int32_t p, int32_t d, const double *X0,
                           const arr_solve_opts *opts, double *eigval, double *res, double *evec,
