@@ -561,3 +561,33 @@ def test_solve_with_gn_inner_solver(arr, kind):
     assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) < 1e-10
     cert = oracle.residuals(A, host(Xd)[:, :spec.k], ev)
     assert np.all(cert <= 1.01 * spec.tol)
+
+
+def test_phase_and_kernel_times(arr):
+    """eig_set_timing / eig_phase_times / eig_kernel_times: the d filter launches of a sweep
+    are counted; the DMMA Gram and GEMM launches report their ALGORITHMIC flops (2 n m1 m2,
+    a symmetric Gram n m (m + 1), an upper-triangular B 2 n sum_c min(c + 1, m1)) and
+    positive device times; a Gram of known shape adds exactly its flops."""
+    A = synth.laplacian_2d(60)
+    k, p, d = 24, 1, 7
+    ctx = arr.eig_init(arr.to_device_csr(A), k, p, d)
+    X = torch.from_numpy(synth.gaussian_block(A.n, k, 3)).cuda()
+    ctx.eig_set_interval(ctx.eig_gershgorin_lower(), 6.0)
+    ctx.eig_set_timing(True)
+    ctx.filter_step(X, normalize=True)
+    Y = torch.empty_like(X)
+    ctx.arr_project(X, Y)
+    ms, cnt = ctx.eig_phase_times()
+    assert cnt[0] == d and ms[0] > 0 and cnt[1] == 1 and ms[1] > 0
+    kms, kfl, kcnt = ctx.eig_kernel_times()
+    assert kcnt[0] > 0 and kcnt[1] > 0 and (kms > 0).all()
+    G = torch.empty((k, 8), dtype=torch.float64, device="cuda")
+    ctx.eig_set_timing(True)  # zeroes the totals
+    ctx.gram(X, X[:, :8], G)
+    ms2, fl2, c2 = ctx.eig_kernel_times()
+    assert c2[0] == 1 and c2[1] == 0 and fl2[0] == 2.0 * A.n * k * 8
+    Gs = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    ctx.gram(X, X, Gs)  # symmetric: the upper triangle's n k (k + 1)
+    ms3, fl3, c3 = ctx.eig_kernel_times()
+    assert c3[0] == 2 and fl3[0] - fl2[0] == float(A.n) * k * (k + 1)
+    ctx.close()
