@@ -705,15 +705,33 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
                 ST_TRY(gram_x(c, Q, lq, jw, Qj, lq, w, G_buf(c), w));
                 launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, Qj, lq, Qj, lq, c->A.n);
             }
+            // CholeskyQR2 of the re-projected block; a block of pure rounding noise (an exactly
+            // invariant Krylov block, e.g. a diagonal A) can make a Gram numerically indefinite:
+            // then the pass is redone by SVQB, which completes dependent directions (R7)
             int *inf = c->dinfo + INFO_CHOL;
+            auto chol_ok = [&](int pass_idx) -> int {  // 1 ok, 0 failed, -1 CUDA error
+                if (cudaMemcpyAsync(c->h_istage + 48, inf + 2 * pass_idx, sizeof(int) * 2, cudaMemcpyDeviceToHost,
+                                    c->stream) != cudaSuccess ||
+                    cudaStreamSynchronize(c->stream) != cudaSuccess)
+                    return -1;
+                return c->h_istage[48] == 0 && c->h_istage[49] == 0;
+            };
             CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(int) * 4, c->stream));
             if ((st = cholqr_pass(c, Qj, lq, T, lt, w, false, inf, nullptr)) != ARR_OK) return st;
+            int okp = chol_ok(0);
+            if (okp < 0) return fail(c, ARR_ECUDA, "arr_project: CUDA error");
+            if (!okp) {  // Qj still holds the re-projected block
+                if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
+            }
             if ((st = cholqr_pass(c, T, lt, Qj, lq, w, false, inf + 2, nullptr)) != ARR_OK) return st;
-            CUDA_TRY(cudaMemcpyAsync(c->h_istage + 48, inf, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream));
-            CUDA_TRY(cudaStreamSynchronize(c->stream));
-            for (int q = 0; q < 4; ++q)
-                if (c->h_istage[48 + q] != 0)
-                    return fail(c, ARR_ENUMERIC, "arr_project: re-orthonormalisation of an augmentation block failed");
+            okp = chol_ok(1);
+            if (okp < 0) return fail(c, ARR_ECUDA, "arr_project: CUDA error");
+            if (!okp) {  // T still holds the first pass's (nearly orthonormal) output
+                if ((st = svqb_pass(c, T, lt, Qj, lq, w, nullptr)) != ARR_OK) return st;
+                if ((st = svqb_pass(c, Qj, lq, T, lt, w, nullptr)) != ARR_OK) return st;
+                launch_copy_rows(c, T, lt, Qj, lq, c->A.n, w);
+                CHECK_LAUNCH();
+            }
         }
     }
     { const int e = t_mark(c); t_add(c, 3, evs, e, 1); evs = e; }

@@ -222,7 +222,10 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(double alpha, const doubl
 #define ARR_DMMA_STAGES 2  // measured on B200: 2 stages at 5 CTAs/SM beat 4 stages at 3 (cfg3 ARR basis 623 -> 576 ms)
 #endif
 #ifndef ARR_DMMA_MINB
-#define ARR_DMMA_MINB 5
+// 4 CTAs/SM (128 registers): the A fragments of a k-step get their own registers (at 5 CTAs,
+// 96 registers, one register pair was reloaded before every 4 DMMAs); +1-2% on every ARR
+// GEMM shape (profiles/r02/dmma_gemm_minb.log)
+#define ARR_DMMA_MINB 4
 #endif
 constexpr int S_CA = ARR_DMMA_STAGES;
 
