@@ -660,7 +660,8 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
                     launch_gemm(c, -1.0, c->defl_Q, c->defl_ld, c->defl_n, G_buf(c), w, w, 1.0, T, lt, T, lt, c->A.n);
                 }
             }
-            for (int pass = 0; pass < 2; ++pass) {
+            static const int cgs_passes = [] { const char *e = getenv("ARRABIT_CGS_PASSES"); return e ? std::max(1, atoi(e)) : 2; }();
+            for (int pass = 0; pass < cgs_passes; ++pass) {
                 ST_TRY(gram_x(c, Q, lq, jw, T, lt, w, G_buf(c), w));
                 // The first pass's coefficients Q[:, :jw]^T (A U_{j-1}) ARE rows [0, jw) of
                 // block column j-1 of H = Q^T A Q (same SpMM output, same Gram kernel on the

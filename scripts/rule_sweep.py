@@ -54,7 +54,7 @@ def main():
         ev, res, info = ctx.eig_solve(X, tol=spec.tol, maxit=spec.maxit, s_max=args.smax, inner=args.inner)
         torch.cuda.synchronize()
         out.append(time.perf_counter() - t0)
-    r = {"config": spec.name, "digits": os.environ.get("ARRABIT_RANGE_DIGITS", "8"), "smax": args.smax,
+    r = {"config": spec.name, "env": {k: v for k, v in os.environ.items() if k.startswith("ARRABIT_")}, "smax": args.smax,
          "inner": args.inner, "converged": bool(info.converged), "outer": int(info.outer), "sweeps": int(info.sweeps),
          "maxres": float(res.max()), "solve_s": min(out), "s_per_outer": [int(l["s"]) for l in ctx.last_log]}
     if args.save:
