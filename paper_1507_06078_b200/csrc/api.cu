@@ -545,8 +545,11 @@ arr_status svqb_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, in
 // D = diag(G)^{-1/2}, R^T R = D G D + s I (potrf), Out = In D R^{-1} (trtri +
 // DMMA GEMM).  s = 11 (n c + c(c+1)) u c bounds the rounding of the Gram so the
 // shifted factorisation exists for any input; two unshifted passes follow.
+// racc_new (optional): the accumulated factor R with In_0 = Out R over the passes so far
+// (launch_chol_racc; racc_first on the first pass), R23
 arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols,
-                       bool shifted, int *info2, int *rank_slot) {
+                       bool shifted, int *info2, int *rank_slot, const double *racc_old = nullptr,
+                       double *racc_new = nullptr, bool racc_first = false) {
     double *G = G_buf(c), *Gs = V_buf(c), *B = B_buf(c), *D = D_buf(c);
     const double u = 1.1102230246251565e-16;
     const double shift = shifted ? 11.0 * ((double)n_glob(c) * ncols + (double)ncols * (ncols + 1)) * u * ncols : 0.0;
@@ -556,6 +559,7 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
     SOLVER_TRY(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_UPPER, ncols, Gs, ncols, c->solver_work, c->solver_lwork,
                                 info2));
     if (rank_slot) launch_diag_copy(c, Gs, ncols, c->evals);
+    if (racc_new) launch_chol_racc(c, Gs, D, ncols, racc_old, racc_new, racc_first);
     SOLVER_TRY(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, ncols, CUDA_R_64F, Gs, ncols,
                                 c->trtri_dwork, c->trtri_dbytes, c->trtri_hwork.data(), c->trtri_hwork.size(),
                                 info2 + 1));
@@ -570,13 +574,16 @@ arr_status cholqr_pass(arr_ctx *c, const double *In, int64_t ldin, double *Out, 
 // In itself: In is only read by the first pass); *ok = 0 if a factorisation
 // failed (numerically rank-deficient input after the shift): the caller then
 // falls back to SVQB.  Synchronises the stream.
+// racc_final (optional): set to the factor R with In = Out R (c->racc or c->racc + ncols^2).
 arr_status cholqr3(arr_ctx *c, const double *In, int64_t ldin, double *Out, int64_t ldout, int ncols, int *rank_slot,
-                   bool *ok, double *S, int64_t lds) {
+                   bool *ok, double *S, int64_t lds, double **racc_final = nullptr) {
     arr_status st;
     int *inf = c->dinfo + INFO_CHOL;
+    double *r0 = racc_final ? c->racc : nullptr, *r1 = racc_final ? c->racc + (int64_t)ncols * ncols : nullptr;
+    if (racc_final) *racc_final = r1;
     CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(int) * 6, c->stream));
-    if ((st = cholqr_pass(c, In, ldin, Out, ldout, ncols, true, inf, rank_slot)) != ARR_OK) return st;
-    if ((st = cholqr_pass(c, Out, ldout, S, lds, ncols, false, inf + 2, nullptr)) != ARR_OK) return st;
+    if ((st = cholqr_pass(c, In, ldin, Out, ldout, ncols, true, inf, rank_slot, nullptr, r0, true)) != ARR_OK) return st;
+    if ((st = cholqr_pass(c, Out, ldout, S, lds, ncols, false, inf + 2, nullptr, r0, r1)) != ARR_OK) return st;
     // The second pass's factor R2 measures how far pass 1 was from orthonormal:
     // pass 2's output is orthonormal to O(u cond(R2)^2).  If R2^{-1} (left in V
     // by trtri) is within 1e-6 of I entrywise, the third pass is skipped.
@@ -589,7 +596,8 @@ arr_status cholqr3(arr_ctx *c, const double *In, int64_t ldin, double *Out, int6
     const double dev = c->h_stage[0];
     if (!*ok) return ARR_OK;
     if (!(dev <= 1e-6)) {
-        if ((st = cholqr_pass(c, S, lds, Out, ldout, ncols, false, inf + 4, nullptr)) != ARR_OK) return st;
+        if ((st = cholqr_pass(c, S, lds, Out, ldout, ncols, false, inf + 4, nullptr, r1, r0)) != ARR_OK) return st;
+        if (racc_final) *racc_final = r0;
         CUDA_TRY(cudaMemcpyAsync(c->h_istage + 44, inf + 4, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         *ok = c->h_istage[44] == 0 && c->h_istage[45] == 0;
@@ -615,6 +623,13 @@ bool h_tridiag() {
     return v;
 }
 
+// H's block (p-1, p) from the last augmentation block's CholeskyQR factor (R23;
+// ARRABIT_H_RFACTOR=0: from the Gram U_{p-1}^T (A U_p))
+bool h_rfactor() {
+    static const bool v = [] { const char *e = getenv("ARRABIT_H_RFACTOR"); return !(e && atoi(e) == 0); }();
+    return v;
+}
+
 arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double *Y, int64_t ldy,
                     double *ritz_host, int32_t *rank) {
     const int w = c->w;
@@ -634,6 +649,8 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
     arr_status st;
     const int ev0 = t_mark(c);
     int evs = ev0;
+    double *racc = nullptr;  // W_p = U_p R (the last augmentation block's CholeskyQR factor)
+    bool r_ok = false;
     // U_0 = orth(X): Alg. RR step 1 on the first block
     bool ok = false;
     if (c->orth_mode == 0 && (st = cholqr3(c, X, ldx, Q, lq, w, c->dinfo + INFO_RANK0, &ok, S0, ls0)) != ARR_OK)
@@ -674,9 +691,12 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         };
         if ((st = make_W()) != ARR_OK) return st;
         ok = false;
+        const bool want_r = j == p_use && h_rfactor() && !is_dist(c) && c->defl_n == 0;
         if (c->orth_mode == 0 &&
-            (st = cholqr3(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j, &ok, T, lt)) != ARR_OK)
+            (st = cholqr3(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j, &ok, T, lt, want_r ? &racc : nullptr)) !=
+                ARR_OK)
             return st;
+        r_ok = want_r && ok && c->orth_mode == 0;
         if (!ok) {
             if (c->orth_mode == 0 && (st = make_W()) != ARR_OK) return st;  // T was reused by CholeskyQR3
             if ((st = svqb_pass(c, T, lt, Qj, lq, w, c->dinfo + INFO_RANK0 + j)) != ARR_OK) return st;
@@ -700,8 +720,13 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         launch_maxabs(c, G_buf(c), (int64_t)jw * kOmegaCols, c->evals);
         CHECK_LAUNCH();
         CUDA_TRY(cudaMemcpyAsync(c->h_stage, c->evals, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (r_ok)
+            CUDA_TRY(cudaMemcpyAsync(c->h_istage + 52, c->dinfo + INFO_RANK0 + j, sizeof(int), cudaMemcpyDeviceToHost,
+                                     c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
+        if (r_ok) r_ok = c->h_istage[52] == w;  // numerically full rank: W = U_p R holds with R invertible
         if (!(c->h_stage[0] <= 3e-12 * sqrt((double)w))) {
+            r_ok = false;  // U_p re-projected and re-orthonormalised: no longer W R^{-1}
             for (int pass = 0; pass < 2; ++pass) {
                 ST_TRY(gram_x(c, Q, lq, jw, Qj, lq, w, G_buf(c), w));
                 launch_gemm(c, -1.0, Q, lq, jw, G_buf(c), w, w, 1.0, Qj, lq, Qj, lq, c->A.n);
@@ -758,8 +783,19 @@ arr_status arr_core(arr_ctx *c, int p_use, const double *X, int64_t ldx, double 
         if (i0 > 0)
             CUDA_TRY(cudaMemset2DAsync(H + (int64_t)j * w, sizeof(double) * m, 0, sizeof(double) * w, (size_t)i0 * w,
                                        c->stream));
-        launch_gram(c, Q + (int64_t)i0 * w, lq, (j + 1 - i0) * w, T, lt, w, c->A.n, H + (int64_t)i0 * w * m + (int64_t)j * w,
-                    m, c->part);
+        // Block (j-1, j) from the CholeskyQR factor of the last augmentation block (DESIGN.md
+        // R23): A U_{j-1} = Q[:, :jw] C + U_j R (the CGS2 + CholeskyQR3 that built U_j), so
+        // U_{j-1}^T A U_j = (A U_{j-1})^T U_j = R^T + C^T Q[:, :jw]^T U_j = R^T + O(u ||A||)
+        // (U_j passed the re-orthogonality check): 2 n w^2 flops fewer per ARR.
+        const bool use_r = r_ok && racc && j == p_use && j >= 1;
+        const int ioff = use_r ? j - 1 : j;  // rows [i0 w, ioff w) from the Gram Q^T (A U_j)
+        if (ioff > i0)
+            launch_gram(c, Q + (int64_t)i0 * w, lq, (ioff - i0) * w, T, lt, w, c->A.n,
+                        H + (int64_t)i0 * w * m + (int64_t)j * w, m, c->part);
+        if (use_r) launch_put_rt(c, racc, w, H + (int64_t)(j - 1) * w * m + (int64_t)j * w, m);
+        // diagonal block U_j^T (A U_j), symmetric: the tiles on or above the diagonal only
+        launch_gram(c, Q + (int64_t)j * w, lq, w, T, lt, w, c->A.n, H + (int64_t)j * w * m + (int64_t)j * w, m, c->part,
+                    /*sym_result=*/true);
     }
     if (is_dist(c)) ST_TRY(comm_allreduce(c, H, (size_t)m * m, 0));
     launch_symmetrize(c, H, m, w);
@@ -1182,6 +1218,7 @@ arr_status eig_init_dist(arr_ctx **out, const arr_csr *A, int32_t k, int32_t w_i
         {(void **)&c->dinfo, sizeof(int) * 64},
         {(void **)&c->sched, sizeof(unsigned long long) * 2},
         {(void **)&c->omega, sizeof(double) * (size_t)w * kOmegaCols},
+        {(void **)&c->racc, sizeof(double) * 2 * (size_t)w * w},
         {(void **)&c->lazy, sizeof(double) * 2 * (ARR_MAX_W + 2)},
     };
     size_t total = 0;

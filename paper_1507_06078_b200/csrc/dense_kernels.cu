@@ -998,8 +998,8 @@ int gram_nsplit(int64_t n, int32_t m1, int32_t m2, int num_sms, bool sym) {
 }
 
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
-                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials) {
-    const bool sym = (X == Y) && (m1 == m2) && (ldx == ldy);
+                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials, bool sym_result) {
+    const bool sym = (sym_result || ((X == Y) && (ldx == ldy))) && (m1 == m2);
     int ns = gram_nsplit(n, m1, m2, c->num_sms, sym);
     while ((size_t)ns * m1 * m2 > c->part_elems && ns > 1) --ns;
     int64_t rps = (n + ns - 1) / ns;
@@ -1099,6 +1099,27 @@ __global__ void chol_build_kernel(const double *__restrict__ D, const double *__
     const int i = (int)(t / w), j = (int)(t % w);
     B[t] = (i <= j) ? D[i] * Rinv_cm[(int64_t)j * w + i] : 0.0;
 }
+__global__ void chol_racc_kernel(const double *__restrict__ Rs_cm, const double *__restrict__ D, int w,
+                                 const double *__restrict__ Rold, double *__restrict__ Rnew, bool first) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)w * w) return;
+    const int i = (int)(t / w), j = (int)(t % w);
+    double v = 0.0;
+    if (i <= j) {
+        if (first) {
+            v = Rs_cm[(int64_t)j * w + i] / D[j];
+        } else {
+            for (int k = i; k <= j; ++k) v += Rs_cm[(int64_t)k * w + i] / D[k] * Rold[(int64_t)k * w + j];
+        }
+    }
+    Rnew[t] = v;
+}
+__global__ void put_rt_kernel(const double *__restrict__ R, int w, double *__restrict__ H, int64_t ldh) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)w * w) return;
+    const int a = (int)(t / w), b = (int)(t % w);
+    H[(int64_t)a * ldh + b] = R[(int64_t)b * w + a];
+}
 __global__ void diag_copy_kernel(const double *__restrict__ A_cm, int w, double *__restrict__ d) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < w) d[i] = A_cm[(int64_t)i * w + i];
@@ -1195,6 +1216,15 @@ void launch_chol_prep(arr_ctx *c, const double *G, int32_t w, double shift, doub
 void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32_t w, double *B, const double *Rdiag,
                        double rank_thr, int *rank_out) {
     chol_build_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(D, Rinv_cm, w, B, Rdiag, rank_thr, rank_out);
+    c->launches++;
+}
+void launch_chol_racc(arr_ctx *c, const double *Rs_cm, const double *D, int32_t w, const double *Rold, double *Rnew,
+                      bool first) {
+    chol_racc_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(Rs_cm, D, w, Rold, Rnew, first);
+    c->launches++;
+}
+void launch_put_rt(arr_ctx *c, const double *R, int32_t w, double *H, int64_t ldh) {
+    put_rt_kernel<<<nblk((int64_t)w * w, 256), 256, 0, c->stream>>>(R, w, H, ldh);
     c->launches++;
 }
 void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d) {

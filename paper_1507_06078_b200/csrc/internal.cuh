@@ -147,6 +147,7 @@ struct arr_ctx {
     int *dinfo;       // cuSOLVER info + rank counters
     unsigned long long *sched;  // [2] SpMM tile ticket (zeroed at init, self-resetting)
     double *omega;              // [w x kOmegaCols] seeded Gaussian sketch of the ARR re-orthogonality check
+    double *racc;               // [2 x w x w] CholeskyQR factor R of the last augmentation block (R23)
     const int64_t *tile_row0;   // eig_set_schedule (borrowed device arrays) or nullptr
     const int32_t *tile_len;
     int64_t ntiles;
@@ -307,8 +308,10 @@ inline int t_mark(arr_ctx *c) {
 inline void t_add(arr_ctx *c, int phase, int e0, int e1, int64_t count, double work = 0.0) {
     if (e0 >= 0 && e1 >= 0) c->pending.push_back({phase, e0, e1, count, work});
 }
+// sym_result: X != Y but X^T Y is symmetric in exact arithmetic (U^T (A U)): only the tiles on
+// or above the diagonal are computed and the result is their exact mirror
 void launch_gram(arr_ctx *c, const double *X, int64_t ldx, int32_t m1, const double *Y, int64_t ldy,
-                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials);
+                 int32_t m2, int64_t n, double *G, int64_t ldg, double *partials, bool sym_result = false);
 // upper != 0: B is upper triangular (exact zeros below the diagonal are skipped)
 void launch_gemm(arr_ctx *c, double alpha, const double *X, int64_t ldx, int32_t m1, const double *B,
                  int64_t ldb, int32_t m2, double beta, const double *Cin, int64_t ldc, double *Out,
@@ -326,6 +329,13 @@ void launch_chol_prep(arr_ctx *c, const double *G, int32_t w, double shift, doub
 void launch_chol_build(arr_ctx *c, const double *D, const double *Rinv_cm, int32_t w, double *B, const double *Rdiag,
                        double rank_thr, int *rank_out);
 void launch_diag_copy(arr_ctx *c, const double *A_cm, int32_t w, double *d);
+// Rnew = (Rs diag(D)^-1) Rold (first: Rs diag(D)^-1): the inverse of one CholeskyQR pass's
+// transform B = diag(D) Rs^-1 folded into the accumulated factor (Rs column-major upper,
+// Rold / Rnew row-major upper, w x w)
+void launch_chol_racc(arr_ctx *c, const double *Rs_cm, const double *D, int32_t w, const double *Rold, double *Rnew,
+                      bool first);
+// H[r0 + a][c0 + b] = R[b][a] (R row-major w x w upper, H row-major, ld m)
+void launch_put_rt(arr_ctx *c, const double *R, int32_t w, double *H, int64_t ldh);
 
 void launch_dev_from_identity(arr_ctx *c, const double *M_cm, int32_t w, double *out);
 void launch_maxabs(arr_ctx *c, const double *x, int64_t count, double *out);

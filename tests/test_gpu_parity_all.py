@@ -354,3 +354,44 @@ def test_options_follow_the_oracle_rule(arr, opt, kind):
         assert res.max() < (1 + 9.0 * hs / k) * spec.tol
     if exits == 0 and not adapt & 4:
         assert info.exit_rule in (0, 1)
+
+
+# ---------------------------------------------------------------- H block from the R factor
+_RF_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth, oracle, paper_1507_06078_b200 as arr
+A = {{"lap3dV": lambda: synth.laplacian_3d_potential(13, 2), "zipf": lambda: synth.zipf_random(5000, 3),
+     "st27": lambda: synth.stencil27_3d(11)}}[{kind!r}]()
+w = 24
+X = synth.gaussian_block(A.n, w, 5)
+a = oracle.gershgorin_lower(A)
+b = a + 0.7 * (2 * np.abs(A.val).max() - a)
+X = oracle.mpm_sweep(A, a, b, 3, X)
+ctx = arr.eig_init(arr.to_device_csr(A), k=w, p=2, d=4)
+Xd = torch.from_numpy(X).cuda()
+Yd = torch.zeros_like(Xd)
+ritz, _ = ctx.arr_project(Xd, Yd, p={p})
+np.save({out!r}, np.asarray(ritz))
+"""
+
+
+@pytest.mark.parametrize("kind", ["lap3dV", "zipf", "st27"])
+@pytest.mark.parametrize("p", [1, 2])
+def test_h_block_from_cholqr_factor(kind, p, tmp_path):
+    """DESIGN.md R23: H's block (p-1, p) taken from the last augmentation block's
+    accumulated CholeskyQR factor (U_{p-1}^T A U_p = R^T + O(u ||A||)) gives the same Ritz
+    values as the direct Gram U_{p-1}^T (A U_p) (ARRABIT_H_RFACTOR=0), within the ARR
+    Ritz-value tolerance 1e-12 * 2 ||A||_max (the switch is read once per process)."""
+    import subprocess
+    import sys
+    outs = []
+    for flag in ("0", "1"):
+        out = str(tmp_path / f"ritz_{flag}.npy")
+        env = dict(os.environ, ARRABIT_H_RFACTOR=flag)
+        code = _RF_SNIPPET.format(root=ROOT, kind=kind, p=p, out=out)
+        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert outs[0].shape == outs[1].shape
+    scale = np.max(np.abs(outs[0]))
+    assert np.max(np.abs(outs[0] - outs[1])) <= 1e-12 * 2 * scale, np.max(np.abs(outs[0] - outs[1]))
