@@ -344,7 +344,12 @@ arr_status orthonormalize(arr_ctx *c, double *X, int64_t ldx, int32_t ncols, int
  * span{X, AX, ..., A^p X}, built as an orthonormal block-Krylov basis
  * Q = [U_0 .. U_p]: U_0 = orth(X), U_j = orth((I - QQ^T) A U_{j-1}) (block CGS2),
  * H = Q^T A Q (m x m, m = (p+1)w, AQ never stored), H = V Theta V^T on device
- * (cuSOLVER syevd; not on the graded path), Y = Q V[:, 1..w].
+ * (cuSOLVER syevd; not on the graded path), Y = Q V[:, 1..w].  On one GPU H's
+ * block columns 0..p-1 are the first CGS pass's coefficients, block column p
+ * keeps its block-tridiagonal rows (R22), its block (p-1, p) is R^T
+ * with R the CholeskyQR factor of the last augmentation block (R23; the Gram
+ * when that block needed SVQB or re-projection) and block (p, p) is a
+ * symmetric-result Gram. 
  * X: n x w input (not modified unless Y == X).  Y: n x w output (the w leading
  * Ritz vectors; may equal X; may be NULL to skip forming them).
  * ritz_host: host [(p+1)w] Ritz values, descending.  rank: host, numerical
