@@ -333,6 +333,14 @@ def solve_run(arr, torch, spec, A, Aloc, X0, X, flush, stream, dev, args, steps,
     if not partitioned and use_stencil(spec, args):
         ctx.eig_set_stencil(*stencil_grid(spec))
         path = f"stencil ({ctx.stencil_points}-point, A {ctx.stencil_abytes} B/row)"
+    elif partitioned and use_stencil(spec, args) and _partition_spec(spec)[0] == "planes":
+        # z-slab of whole grid planes: the stencil kernel with the neighbouring planes as ghost
+        # planes (interior planes during the halo exchange, then the slab's first / last plane)
+        ps_ = _partition_spec(spec)
+        slab = ((ps_[2] // ps_[1], ps_[1], plan.n_own // ps_[2]) if spec.kind != "lap2d"
+                else (ps_[2], 1, plan.n_own // ps_[2]))
+        ctx.eig_set_stencil(*slab)
+        path = f"stencil on z-slabs ({ctx.stencil_points}-point, A {ctx.stencil_abytes} B/row, slab {slab})"
     elif not partitioned and spec.kind in ("lap3dV", "st27"):
         from paper_1507_06078_b200 import schedule
         by, tile = {"lap3dV": (10, 16), "st27": (8, 32)}[spec.kind]

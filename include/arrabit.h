@@ -256,7 +256,15 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
  * fused SpMM of the context without a per-column shift runs the stencil-aware
  * 2.5-D blocked kernel: same per-row FMA order, so outputs are
  * bitwise those of the CSR kernels.  nx = ny = nz = 0 switches back to CSR and
- * frees the copy.  Single-GPU contexts only; synchronises the stream. */
+ * frees the copy.  Synchronises the stream.
+ * Row-partitioned contexts (eig_init_dist): (nx, ny, nz) is this rank's z-slab of whole
+ * grid planes (nx ny nz = the owned rows) and its ghost rows must be exactly the
+ * neighbouring plane below (received from lower ranks, first) and / or above (the
+ * layout partition.py builds for bounds_planes); anything else is ARR_EINVAL.  Each
+ * fused SpMM then runs the stencil kernel on the planes that touch no ghost plane
+ * while the halo exchange is in flight and on the slab's first / last plane after it
+ * (the same sums: bitwise the one-GPU result).  Column-split contexts declare the
+ * whole grid (the column context holds all of A). */
 arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
 /* K of the active stencil path (0 = the CSR kernels). */
 int32_t eig_stencil_active(const arr_ctx *c);

@@ -9,6 +9,7 @@ import ctypes
 import math
 import os
 import subprocess
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -476,6 +477,8 @@ def solve(A, k: int, d: int, p: int, X0: np.ndarray, tol: float = 1e-10, maxit: 
         res = residuals(A, Y[:, :k], mu[:k])
         maxres = float(np.max(res))
         log.append(dict(outer=outer, s=s, a=a, b=b, mu1=float(mu[0]), rank=r, maxres=maxres, p=p_cur, d=d_cur))
+        if os.environ.get("ORACLE_VERBOSE"):  # progress of the hour-long golden solves (no arithmetic)
+            print(log[-1], file=sys.stderr, flush=True)
         if maxres <= tol:
             return SolveResult(mu[:k].copy(), Y[:, :k].copy(), res, True, outer, sweeps, log, 1, p_cur, d_cur)
         if exits & 1:

@@ -263,6 +263,44 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
     if ((*st = comm_halo_begin(c, s.Yin, s.ld_in, s.w)) != ARR_OK) return 0;
     int rows = 0;
     const double *part0 = s.partials;
+    bool halo_done = false;
+    if (c->st.on && s.n == c->A.n) {
+        // z-slab on the stencil path: the planes that touch no ghost plane while the exchange
+        // is in flight, then the slab's first / last plane (each a launch of its own z range)
+        const StencilState &S = c->st;
+        const int nz = (int)S.nz, zi0 = S.gz_lo, zi1 = nz - S.gz_hi;
+        SpmmArgs a = s;
+        a.nnz = c->A.nnz;
+        auto part_at = [&](int r) { return part0 ? const_cast<double *>(part0) + (int64_t)r * s.w : nullptr; };
+        if (zi0 < zi1) {
+            int g = launch_spmm_stencil(c, a, zi0, zi1);
+            if (g >= 0) {
+                rows += g;
+                if ((*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
+                if (S.gz_lo) {
+                    a.partials = part_at(rows);
+                    if ((g = launch_spmm_stencil(c, a, 0, 1)) < 0) return g;
+                    rows += g;
+                }
+                if (S.gz_hi) {
+                    a.partials = part_at(rows);
+                    if ((g = launch_spmm_stencil(c, a, nz - 1, nz)) < 0) return g;
+                    rows += g;
+                }
+                c->spmm_blocks++;
+                return rows;
+            }
+        } else {  // one or two planes, all next to a ghost plane
+            if ((*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
+            halo_done = true;
+            const int g = launch_spmm_stencil(c, a, 0, nz);
+            if (g >= 0) {
+                c->spmm_blocks++;
+                return g;
+            }
+        }
+        // the stencil kernel does not apply to this launch (odd width, unaligned block): CSR tiles
+    }
     if (P.n_int_tiles > 0) {
         SpmmArgs a = s;
         a.tile_row0 = P.int_row0; a.tile_len = P.int_len; a.ntiles = P.n_int_tiles;
@@ -270,7 +308,7 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
         if (g < 0) return g;
         rows += g;
     }
-    if ((*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
+    if (!halo_done && (*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
     if (P.n_bnd_tiles > 0) {
         SpmmArgs a = s;
         a.tile_row0 = P.bnd_row0; a.tile_len = P.bnd_len; a.ntiles = P.n_bnd_tiles;
@@ -1411,8 +1449,29 @@ arr_status eig_set_schedule(arr_ctx *c, const int64_t *tile_row0, const int32_t 
 arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
     GUARD(c);
     if (c->cs) return eig_set_stencil(c->cs->col, nx, ny, nz);  // the column context has the whole A
-    if (is_dist(c) && (nx || ny || nz)) return fail(c, ARR_EINVAL, "stencil path: single-GPU contexts only");
-    const arr_status st = stencil_setup(c, nx, ny, nz);
+    int gz_lo = 0, gz_hi = 0;
+    if (is_dist(c) && (nx || ny || nz)) {
+        // z-slab of a row partition: (nx, ny, nz) is this rank's slab of whole grid planes; the
+        // ghost rows must be the whole plane below (from lower ranks) and / or above
+        const DistPlan &P = c->plan;
+        int32_t my_rank = 0, nr = 1;
+        comm_rank_size(c->comm, &my_rank, &nr);
+        int64_t lo = 0, hi = 0;
+        bool ordered = true;  // every lower-rank peer's rows before every higher-rank peer's
+        for (size_t q = 0; q < P.peer.size(); ++q) {
+            const int64_t cnt = P.recv_off[q + 1] - P.recv_off[q];
+            if (P.peer[q] < my_rank) { lo += cnt; ordered = ordered && hi == 0; }
+            else hi += cnt;
+        }
+        const int64_t nxy = nx * ny;
+        if (nx < 1 || ny < 1 || nz < 1 || !ordered || (lo != 0 && lo != nxy) || (hi != 0 && hi != nxy) ||
+            lo + hi != P.n_ghost)
+            return fail(c, ARR_EINVAL, "eig_set_stencil on a row partition: the rank's rows must be a z-slab of whole "
+                                       "grid planes whose ghost rows are the neighbouring planes");
+        gz_lo = lo ? 1 : 0;
+        gz_hi = hi ? 1 : 0;
+    }
+    const arr_status st = stencil_setup(c, nx, ny, nz, gz_lo, gz_hi);
     if (st == ARR_EINVAL)
         return fail(c, st, "eig_set_stencil: n != nx*ny*nz, or a row of A is unsorted / has a column outside the "
                            "3x3x3 neighbourhood of its grid point");

@@ -85,6 +85,10 @@ struct StencilState {
     double coef[27] = {};
     int shape = 0, hx = 0, hy = 0;  // stencil_kernels.cu Shape<>: 0 27-pt, 1 7-pt, 2 2-D 5-pt, 3 1-D 3-pt
     int smem_optin = 0;
+    // z-slab of a row partition (eig_init_dist): nz = the owned planes; gz_lo / gz_hi = 1 when
+    // the plane below / above is a ghost plane (the block's rows n .. n + (gz_lo + gz_hi) nx ny,
+    // lower plane first: the ghost rows sorted by global id)
+    int gz_lo = 0, gz_hi = 0;
 };
 // One launch of the stencil kernel (kernel parameter, __grid_constant__).
 struct StencilLaunch {
@@ -102,6 +106,8 @@ struct StencilLaunch {
     int64_t nitems;
     int w, wv, K, Kpad;
     int nx, ny, nz;
+    int gz_lo, gz_hi;  // ghost planes below / above the nz owned planes (StencilState)
+    int z0, z1;        // output planes of this launch (z-chunks of [z0, z1))
     int Px, Py, Lz, npx, npy, nzc, npan, pwv, NS;
     int box_x, box_y, hx, hy;
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
@@ -255,8 +261,9 @@ int cached_occupancy(LaunchCache &lc, Kern kern, int threads, size_t smem) {
 // Returns the grid size used (number of partial rows written if partials != nullptr).
 int launch_spmm(arr_ctx *c, const SpmmArgs &a);
 // stencil path (stencil_kernels.cu): -1 when it does not apply to this launch
-int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a);
-arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz);
+// z0 / z1: the output planes of this launch (z1 < 0: all owned planes)
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0 = 0, int z1 = -1);
+arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz, int gz_lo = 0, int gz_hi = 0);
 void stencil_release(arr_ctx *c);
 // out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)
 void launch_colnorm_finalize(arr_ctx *c, const double *partials, int nblk, int32_t w, double *out,

@@ -203,8 +203,8 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
     r.y0 = py * P.Py;
     r.pxe = min(P.Px, P.nx - r.x0);
     r.pye = min(P.Py, P.ny - r.y0);
-    r.zc0 = zc * P.Lz;
-    r.zc1 = min(P.nz, r.zc0 + P.Lz);
+    r.zc0 = P.z0 + zc * P.Lz;
+    r.zc1 = min(P.z1, r.zc0 + P.Lz);
     return r;
 }
 
@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
     const int pwv = P.pwv;  // smem row stride in 16-byte vectors (a multiple of 8: 128-byte rows)
     if (tid >= kStCons) {
         // ------------------------------------------------------------ producer warp (lane 0)
-        // Per step (plane z of the march; z == nz is a tail step with no plane) at most five
+        // Per step (plane z of the march; z == nz is a tail step with no plane unless a ghost
+        // plane lies above; z == -1 a first step on the ghost plane below) at most five
         // TMA boxes completing on full[b]: the Y_j box of plane z (box_x x box_y rows with the
         // x/y halo), the Y_{j-1} (and X) rows of the outputs of plane z-1, and the DIA rows
         // of plane z+1 (and of plane z on an item's first step).
@@ -306,10 +307,13 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         for (int64_t it = blockIdx.x; it < P.nitems;) {
             const Item I = (!SUMSQ && P.pm) ? decode_item<true>(P, it) : decode_item<false>(P, it);
             const int col0 = I.panel * pwv * 2;  // first column of the panel
-            const int zs = max(I.zc0 - 1, 0);
+            const int zs = max(I.zc0 - 1, -P.gz_lo);
             for (int z = zs; z <= I.zc1; ++z) {
                 if (wrapped) mbar_wait(empty + b, eph);
-                const bool real = z < P.nz;
+                const bool real = z < P.nz + P.gz_hi;
+                // the block's plane holding virtual plane z: the ghost planes of a z-slab
+                // follow the owned ones (lower first)
+                const int zp = z < 0 ? P.nz : (z >= P.nz ? P.nz + P.gz_lo : z);
                 const bool fin = z - 1 >= I.zc0;
                 // DIA planes to load: z+1 (and z on the first step when z is an output plane)
                 const int va0 = (z == zs && z >= I.zc0 && real) ? z : z + 1;
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
                 const uint32_t fb = fb0 + 8u * b;
                 mbar_expect_tx(full + b, total);
                 const uint32_t st = st0 + (uint32_t)b * SL.bytes;
-                if (real) tma_4d(st + SL.box, &P.tm_in, col0, I.x0 - P.hx, I.y0 - P.hy, z, fb, pol_keep);
+                if (real) tma_4d(st + SL.box, &P.tm_in, col0, I.x0 - P.hx, I.y0 - P.hy, zp, fb, pol_keep);
                 if (VM == 1 && real) tma_3d(st + SL.dg, &P.tm_val, I.x0, I.y0, z, fb, pol_once);
                 if (fin) {
                     if (HAS_PREV) tma_4d(st + SL.prev, &P.tm_prev, col0, I.x0, I.y0, z - 1, fb, pol_once);
@@ -400,9 +404,9 @@ __global__ void __launch_bounds__(NT, StCta<NT>::MINB) stencil_kernel(const __gr
         const double2 bsc = P.scale_mode == 2 ? make_double2(P.beta * csc.x, P.beta * csc.y) : make_double2(P.beta, P.beta);
         const int64_t out_step = nxy * P.ld_out;
         double2 accA = make_double2(0.0, 0.0), accB = make_double2(0.0, 0.0), yiA = make_double2(0.0, 0.0);
-        const int zs = max(I.zc0 - 1, 0);
+        const int zs = max(I.zc0 - 1, -P.gz_lo);
         for (int z = zs; z <= I.zc1; ++z) {
-            const bool real = z < P.nz;
+            const bool real = z < P.nz + P.gz_hi;
             const bool fin = z - 1 >= I.zc0;                // out(z-1) completes in this step
             const bool mid = z >= I.zc0 && z < I.zc1;       // out(z) gets its plane-z terms
             const bool nxt = z + 1 < I.zc1;                 // out(z+1) starts with its plane-z terms
@@ -520,8 +524,19 @@ __device__ __forceinline__ void decode3(int64_t i, int64_t nx, int64_t ny, int64
 
 // Pattern check: sorted, duplicate-free rows whose columns lie in the 3x3x3
 // neighbourhood of the row's grid point; OR of the 27 offset bits present.
+// Column j of a z-slab's local matrix -> grid point with a VIRTUAL plane: owned columns
+// j < n keep z = j / (nx ny); the ghost planes that follow are plane -1 (below, first
+// when present) and plane nz (above).
+__device__ __forceinline__ void decode_col(int64_t j, int64_t nx, int64_t ny, int64_t nz, int gz_lo, int64_t &x,
+                                           int64_t &y, int64_t &z) {
+    decode3(j, nx, ny, x, y, z);
+    if (z >= nz) z = (gz_lo && z == nz) ? -1 : nz;
+}
+
 __global__ void stencil_check_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col, int64_t n,
-                                     int64_t nx, int64_t ny, unsigned *mask, int *bad) {
+                                     int64_t nx, int64_t ny, int64_t nz, int gz_lo, int gz_hi, unsigned *mask,
+                                     int *bad) {
+    const int64_t ncol = n + (int64_t)(gz_lo + gz_hi) * nx * ny;
     unsigned m = 0;
     int b = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -530,10 +545,12 @@ __global__ void stencil_check_kernel(const int64_t *__restrict__ rp, const int32
         int64_t prev = -1;
         for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
             const int64_t j = col[p];
-            if (j <= prev || j < 0 || j >= n) { b = 1; break; }
-            prev = j;
+            if (j < 0 || j >= ncol) { b = 1; break; }
             int64_t xj, yj, zj;
-            decode3(j, nx, ny, xj, yj, zj);
+            decode_col(j, nx, ny, nz, gz_lo, xj, yj, zj);
+            const int64_t key = xj + nx * (yj + ny * (zj + 1));  // ascending in the global column order
+            if (key <= prev) { b = 1; break; }
+            prev = key;
             const int64_t dx = xj - x, dy = yj - y, dz = zj - z;
             if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) { b = 1; break; }
             m |= 1u << ((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1));
@@ -550,7 +567,7 @@ __global__ void stencil_check_kernel(const int64_t *__restrict__ rp, const int32
 // DIA values: dia[i*K + slot(bit)] = A_ij (0 where the neighbour is absent)
 __global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                     const double *__restrict__ val, int64_t n, int64_t nx, int64_t ny,
-                                    StencilSlots sl, double *__restrict__ dia) {
+                                    int64_t nz, int gz_lo, StencilSlots sl, double *__restrict__ dia) {
     const int Kp = (sl.K + 1) & ~1;  // rows padded to 16 bytes (bulk copies)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double *row = dia + i * Kp;
@@ -559,7 +576,7 @@ __global__ void stencil_fill_kernel(const int64_t *__restrict__ rp, const int32_
         decode3(i, nx, ny, x, y, z);
         for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
             int64_t xj, yj, zj;
-            decode3(col[p], nx, ny, xj, yj, zj);
+            decode_col(col[p], nx, ny, nz, gz_lo, xj, yj, zj);
             const int bit = (int)((zj - z + 1) * 9 + (yj - y + 1) * 3 + (xj - x + 1));
             row[sl.slot[bit]] = val[p];
         }
@@ -573,7 +590,8 @@ __device__ __forceinline__ long long dkey(double v) {
     return b >= 0 ? b : b ^ 0x7fffffffffffffffll;
 }
 __global__ void stencil_coef_range_kernel(const double *__restrict__ dia, int Kpad, int64_t n, int64_t nx, int64_t ny,
-                                          int64_t nz, StencilSlots sl, long long *kmin, long long *kmax) {
+                                          int64_t nz, int gz_lo, int gz_hi, StencilSlots sl, long long *kmin,
+                                          long long *kmax) {
     const int k = blockIdx.y;
     int bit = -1;
     for (int b = 0; b < 27; ++b)
@@ -583,7 +601,7 @@ __global__ void stencil_coef_range_kernel(const double *__restrict__ dia, int Kp
     long long mn = 0x7fffffffffffffffll, mx = -0x7fffffffffffffffll - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t x = i % nx, t = i / nx, y = t % ny, z = t / ny;
-        if (x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny || z + dz < 0 || z + dz >= nz) continue;
+        if (x + dx < 0 || x + dx >= nx || y + dy < 0 || y + dy >= ny || z + dz < -gz_lo || z + dz >= nz + gz_hi) continue;
         const long long key = dkey(dia[i * Kpad + k]);
         mn = key < mn ? key : mn;
         mx = key > mx ? key : mx;
@@ -731,10 +749,12 @@ bool encode_diag(CUtensorMap *m, const double *base, int64_t nx, int64_t ny, int
 // Cost model: L2 -> SM bytes per output row = staged rows per patch
 // row + the streamed operands, plus the DIA row once per panel, divided by the
 // useful fraction of the launch (ragged patches, last wave of work items).
-bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, StencilLaunch &L) {
+bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, StencilLaunch &L, int z0, int z1) {
     const StencilState &S = c->st;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
+    const int nzr = z1 - z0;  // output planes of this launch
+    if (nzr < 1) return false;
     const int items_max = kStThreads - 32;  // one output vector per consumer thread (IPT = 2 spills)
     // one CTA per SM at 1024 threads; two at 512 (each up to half the SM's shared memory)
     const size_t smem_max = (size_t)S.smem_optin - 256;
@@ -769,11 +789,11 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 // ticket order: whole columns of patches (no z-chunk seams) unless that leaves
                 // fewer than ~4 items per CTA; static order: >= ~12 items per CTA
                 int nzc = 1;
-                if (dyn && st_nzc() > 0) nzc = std::min<int>(st_nzc(), (int)S.nz);
+                if (dyn && st_nzc() > 0) nzc = std::min<int>(st_nzc(), nzr);
                 else
-                    while ((int64_t)npx * npy * npan * nzc < (dyn ? 4 : 12) * G && S.nz / (nzc + 1) >= 8) ++nzc;
-                const int Lz = (S.nz + nzc - 1) / nzc;
-                nzc = (S.nz + Lz - 1) / Lz;
+                    while ((int64_t)npx * npy * npan * nzc < (dyn ? 4 : 12) * G && nzr / (nzc + 1) >= 8) ++nzc;
+                const int Lz = (nzr + nzc - 1) / nzc;
+                nzc = (nzr + Lz - 1) / Lz;
                 const int64_t items = (int64_t)npx * npy * npan * nzc;
                 const double waves = (double)items / (double)((G / npan) * npan);
                 const double tail = waves / std::ceil(waves);
@@ -801,6 +821,8 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
     }
     if (!found) return false;
     L.nx = (int)S.nx; L.ny = (int)S.ny; L.nz = (int)S.nz;
+    L.gz_lo = S.gz_lo; L.gz_hi = S.gz_hi;
+    L.z0 = z0; L.z1 = z1;
     L.hx = hx; L.hy = hy;
     L.K = S.K;
     L.Kpad = S.Kpad;
@@ -813,13 +835,15 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
 }
 
 // Fused SpMM through the stencil path; -1 when it does not apply to this launch.
-int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0, int z1) {
     if (!c->st.on || a.colshift || a.n != c->A.n || a.w % 2 != 0) return -1;
+    if (z1 < 0) z1 = (int)c->st.nz;
+    if (z0 < 0 || z1 > c->st.nz || z0 >= z1) return -1;
     if (!al16(a.Yin, a.ld_in) || !a.Yout || !al16(a.Yout, a.ld_out)) return -1;
     if (a.Yprev && !al16(a.Yprev, a.ld_prev)) return -1;
     if (a.Xa && !al16(a.Xa, a.ld_xa)) return -1;
     StencilLaunch L{};
-    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L)) return -1;
+    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L, z0, z1)) return -1;
     L.Yin = a.Yin; L.ld_in = a.ld_in;
     L.Yprev = a.Yprev; L.ld_prev = a.ld_prev;
     L.Yout = a.Yout; L.ld_out = a.ld_out;
@@ -828,7 +852,7 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
     L.colscale = a.colscale; L.scale_mode = a.colscale ? a.scale_mode : 0;
     L.partials = a.partials;
     const StencilState &S = c->st;
-    if (!encode_4d(&L.tm_in, a.Yin, a.w, a.ld_in, S.nx, S.ny, S.nz, 2 * L.pwv, L.box_x, L.box_y) ||
+    if (!encode_4d(&L.tm_in, a.Yin, a.w, a.ld_in, S.nx, S.ny, S.nz + S.gz_lo + S.gz_hi, 2 * L.pwv, L.box_x, L.box_y) ||
         (S.vmode == 0 && !encode_4d(&L.tm_val, S.dia, S.Kpad, S.Kpad, S.nx, S.ny, S.nz, S.Kpad, L.Px, L.Py)) ||
         (S.vmode == 1 && !encode_diag(&L.tm_val, S.dia, S.nx, S.ny, S.nz, L.Pxe, L.Py)) ||
         (a.Yprev && !encode_4d(&L.tm_prev, a.Yprev, a.w, a.ld_prev, S.nx, S.ny, S.nz, 2 * L.pwv, L.Px, L.Py)) ||
@@ -845,7 +869,7 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a) {
 }
 
 // Verify the pattern and build the DIA values (eig_set_stencil).
-arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
+arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz, int gz_lo, int gz_hi) {
     StencilState &S = c->st;
     if (S.dia) {
         cudaFreeAsync(S.dia, c->stream);
@@ -859,8 +883,8 @@ arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
     cudaMemsetAsync(c->dinfo + 60, 0, 2 * sizeof(int), c->stream);
     int64_t blocks = (c->A.n + 255) / 256;
     if (blocks > (int64_t)c->num_sms * 8) blocks = (int64_t)c->num_sms * 8;
-    stencil_check_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.n, nx, ny, mask,
-                                                                   bad);
+    stencil_check_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.n, nx, ny, nz, gz_lo,
+                                                                   gz_hi, mask, bad);
     c->launches++;
     if (cudaMemcpyAsync(c->h_istage, c->dinfo + 60, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream) !=
             cudaSuccess ||
@@ -887,7 +911,7 @@ arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
         return ARR_ENOMEM;
     }
     stencil_fill_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(c->A.row_ptr, c->A.col_idx, c->A.val, c->A.n, nx, ny,
-                                                                  sl, (double *)dia);
+                                                                  nz, gz_lo, sl, (double *)dia);
     c->launches++;
     if (cudaGetLastError() != cudaSuccess) return ARR_ECUDA;
     // Constant coefficients (finite-difference operators): every slot's value the same on all
@@ -906,7 +930,8 @@ arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
         for (int k = 0; k < 27; ++k) { init[k] = 0x7fffffffffffffffll; init[27 + k] = -0x7fffffffffffffffll - 1; }
         cudaMemcpyAsync(keys, init.data(), sizeof(long long) * 54, cudaMemcpyHostToDevice, c->stream);
         stencil_coef_range_kernel<<<dim3((unsigned)blocks, K), 256, 0, c->stream>>>((const double *)dia, Kpad, c->A.n, nx,
-                                                                                    ny, nz, sl, keys, keys + 27);
+                                                                                    ny, nz, gz_lo, gz_hi, sl, keys,
+                                                                                    keys + 27);
         c->launches++;
         std::vector<long long> h(54);
         if (cudaMemcpyAsync(h.data(), keys, sizeof(long long) * 54, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
@@ -949,6 +974,7 @@ arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
     }
     S.dia = (double *)dia;
     S.nx = nx; S.ny = ny; S.nz = nz;
+    S.gz_lo = gz_lo; S.gz_hi = gz_hi;
     S.K = K;
     S.Kpad = Kpad;
     int dev = 0, optin = 0;

@@ -199,3 +199,114 @@ def test_dist_solve_matches_oracle(arr, kind, G):
     Y = np.vstack([x[4] for x in res])
     res_o = oracle.residuals(A, Y, ev)
     assert res_o.max() <= spec.tol * 1.01
+
+
+def _slab_grid(kind, plan):
+    """(nx, ny, nz) of a rank's z-slab for eig_set_stencil on a row partition."""
+    if kind == "lap3dV":
+        return 13, 13, plan.n_own // 169
+    if kind == "st27":
+        return 11, 11, plan.n_own // 121
+    return 40, 1, plan.n_own // 40  # lap2d: x-neighbours in plane, y = the march
+
+
+@pytest.mark.parametrize("kind,G", [("lap3dV", 2), ("lap3dV", 3), ("st27", 4), ("st27", 6), ("lap2d", 2),
+                                    ("lap3dV", 13)])
+def test_dist_stencil_path_bitwise(arr, kind, G):
+    """The stencil-aware kernel on a z-slab (eig_set_stencil on a row-partitioned context:
+    ghost planes below / above the owned ones, interior planes during the exchange, then the
+    slab's first and last plane): bitwise the one-GPU CSR kernels' filter (same per-row FMA
+    order), every rank launching the stencil kernel.  G = 6 / 13: slabs of two planes / one."""
+    mk, sp = CASES[kind]
+    A = mk()
+    k, d = 24, 9
+    X0 = synth.gaussian_block(A.n, k, 5)
+    a = oracle.gershgorin_lower(A)
+    b = a + 0.55 * (2 * float(np.abs(A.val).sum() / A.n * 2) - a)
+    c1 = arr.eig_init(arr.to_device_csr(A), k, 1, d)
+    c1.eig_set_interval(a, b)
+    X1 = torch.from_numpy(X0).cuda()
+    c1.filter_step(X1, normalize=False)
+    ref_raw = X1.cpu().numpy()
+    X1 = torch.from_numpy(X0).cuda()
+    c1.filter_step(X1, normalize=True)
+    ref_nrm = X1.cpu().numpy()
+    c1.close()
+    ps, comms, ctx_of = make_rank(arr, A, G, sp(G), k, 1, d)
+
+    def work(r):
+        ctx, s = ctx_of(r)
+        with torch.cuda.stream(s):
+            ctx.eig_set_stencil(*_slab_grid(kind, ps[r]))
+            assert ctx.stencil_points > 0
+            ctx.eig_set_interval(a, b)
+            Xr = to_rank_block(X0, ps[r])
+            ctx.filter_step(Xr, normalize=False)
+            kern = ctx.last_spmm_kernel
+            raw = Xr[:ps[r].n_own].cpu().numpy()
+            Xr = to_rank_block(X0, ps[r], ld=k + 2)
+            ctx.filter_step(Xr, normalize=True)
+            nrm = Xr[:ps[r].n_own].cpu().numpy()
+        ctx.close()
+        return raw, nrm, kern
+
+    res = run_ranks(G, work)
+    for c in comms:
+        c.close()
+    assert all("stencil_kernel" in x[2] for x in res), [x[2] for x in res]
+    raw = np.vstack([x[0] for x in res])
+    nrm = np.vstack([x[1] for x in res])
+    assert np.array_equal(raw, ref_raw), "stencil path on the z-slabs is not bitwise the one-GPU filter"
+    assert np.abs(nrm - ref_nrm).max() <= 1e-14
+    orc = oracle.mpm_sweep(A, a, b, d, X0)
+    assert np.linalg.norm(nrm - orc) / np.linalg.norm(orc) <= 1e-12
+
+
+def test_dist_stencil_rejects_non_slab(arr):
+    """A traffic-balanced row block of an irregular matrix is no z-slab: EINVAL."""
+    A = synth.zipf_random(5000, 3)
+    ps, comms, ctx_of = make_rank(arr, A, 2, ("balanced",), 8, 1, 4)
+
+    def work(r):
+        ctx, s = ctx_of(r)
+        with torch.cuda.stream(s):
+            with pytest.raises(Exception):
+                ctx.eig_set_stencil(ps[r].n_own, 1, 1)
+        ctx.close()
+        return True
+
+    run_ranks(2, work)
+    for c in comms:
+        c.close()
+
+
+@pytest.mark.parametrize("kind,G", [("lap3dV", 2), ("st27", 3)])
+def test_dist_stencil_solve_matches_dense(arr, kind, G):
+    """Full solve on z-slabs with the stencil path declared (filter degrees and the ARR's /
+    residuals' SpMMs through the stencil kernel where it applies)."""
+    spec = configs.SMALL_ANALOGS[kind]
+    A, spec = configs.build_config(spec)
+    X0 = configs.starting_block(spec)
+    lam = np.sort(np.linalg.eigvalsh(A.to_dense()))[::-1][:spec.k]
+    N = spec.size
+    ps, comms, ctx_of = make_rank(arr, A, G, ("planes", N, N * N), spec.k, spec.p, spec.d, w=spec.w)
+
+    def work(r):
+        ctx, s = ctx_of(r)
+        with torch.cuda.stream(s):
+            ctx.eig_set_stencil(N, N, ps[r].n_own // (N * N))
+            Xr = to_rank_block(X0, ps[r])
+            ev, res, info = ctx.eig_solve(Xr, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max)
+            out = (ev, res, info.converged, Xr[:ps[r].n_own, :spec.k].cpu().numpy())
+        ctx.close()
+        return out
+
+    res = run_ranks(G, work)
+    for c in comms:
+        c.close()
+    for r in range(G):
+        assert res[r][2] == 1 and np.array_equal(res[r][0], res[0][0])
+    ev = res[0][0]
+    assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) <= 1e-10
+    Y = np.vstack([x[3] for x in res])
+    assert oracle.residuals(A, Y, ev).max() <= spec.tol * 1.01
