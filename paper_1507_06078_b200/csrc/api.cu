@@ -230,6 +230,18 @@ int sweeps_rule(double amp, int s_max, double digits) {
 // ---------------------------------------------------------------- distributed building blocks
 inline bool is_dist(const arr_ctx *c) { return c->nranks > 1; }
 
+// Rows of a z-slab's end planes (next to a ghost plane) on the stencil path: 1 = the CSR
+// kernels over the plan's boundary tiles, 0 = one-plane launches of the stencil kernel.
+// Default: CSR for the <= 7-point shapes, the stencil kernel for the 27-point one (whose
+// gather is L1-bound); ARRABIT_SLAB_BND=csr|stencil overrides.
+inline bool slab_bnd_csr(int shape) {
+    static const int v = [] {
+        const char *e = getenv("ARRABIT_SLAB_BND");
+        return !e ? -1 : (strcmp(e, "csr") == 0 ? 1 : 0);
+    }();
+    return v < 0 ? shape != 0 : v == 1;
+}
+
 // Fused SpMM over the owned rows.  Distributed: start the ghost-row exchange
 // of Yin, compute the interior rows while it is in flight, then the boundary
 // rows.  Column sums of squares (if requested) of the two launches are written
@@ -277,14 +289,24 @@ int spmm_x(arr_ctx *c, SpmmArgs s, arr_status *st, bool op = true) {
             if (g >= 0) {
                 rows += g;
                 if ((*st = comm_halo_end(c, const_cast<double *>(s.Yin))) != ARR_OK) return 0;
-                if (S.gz_lo) {
-                    a.partials = part_at(rows);
-                    if ((g = launch_spmm_stencil(c, a, 0, 1)) < 0) return g;
+                if (S.bnd_is_ends && slab_bnd_csr(S.shape)) {
+                    // the end planes' rows on the CSR kernels (the plan's boundary tiles): a
+                    // one-plane march stages three planes per output plane, the gather does not
+                    SpmmArgs bt = s;
+                    bt.tile_row0 = P.bnd_row0; bt.tile_len = P.bnd_len; bt.ntiles = P.n_bnd_tiles;
+                    bt.partials = part_at(rows);
+                    const char *kern = c->last_kernel;  // the fused SpMM's kernel: the interior's
+                    if ((g = launch_spmm(c, bt)) < 0) return g;
+                    c->last_kernel = kern;
                     rows += g;
-                }
-                if (S.gz_hi) {
+                } else if (S.gz_lo && S.gz_hi) {  // both end planes in one launch
                     a.partials = part_at(rows);
-                    if ((g = launch_spmm_stencil(c, a, nz - 1, nz)) < 0) return g;
+                    if ((g = launch_spmm_stencil(c, a, 0, nz, true)) < 0) return g;
+                    rows += g;
+                } else if (S.gz_lo || S.gz_hi) {
+                    a.partials = part_at(rows);
+                    const int zb = S.gz_lo ? 0 : nz - 1;
+                    if ((g = launch_spmm_stencil(c, a, zb, zb + 1)) < 0) return g;
                     rows += g;
                 }
                 c->spmm_blocks++;
@@ -1472,6 +1494,27 @@ arr_status eig_set_stencil(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz) {
         gz_hi = hi ? 1 : 0;
     }
     const arr_status st = stencil_setup(c, nx, ny, nz, gz_lo, gz_hi);
+    if (st == ARR_OK && is_dist(c) && c->st.on) {
+        // are the plan's boundary tiles exactly the slab's end planes?
+        const DistPlan &P = c->plan;
+        const int64_t nxy = nx * ny, nown = c->A.n;
+        std::vector<int64_t> r0((size_t)P.n_bnd_tiles);
+        std::vector<int32_t> ln((size_t)P.n_bnd_tiles);
+        if (P.n_bnd_tiles > 0) {
+            CUDA_TRY(cudaMemcpyAsync(r0.data(), P.bnd_row0, sizeof(int64_t) * r0.size(), cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaMemcpyAsync(ln.data(), P.bnd_len, sizeof(int32_t) * ln.size(), cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+        }
+        int64_t total = 0;
+        bool inside = true;
+        for (size_t t = 0; t < r0.size(); ++t) {
+            const int64_t a0 = r0[t], a1 = r0[t] + ln[t];
+            const bool in_lo = gz_lo && a1 <= nxy, in_hi = gz_hi && a0 >= nown - nxy;
+            inside = inside && (in_lo || in_hi);
+            total += ln[t];
+        }
+        c->st.bnd_is_ends = inside && nz >= 2 && total == (int64_t)(gz_lo + gz_hi) * nxy;
+    }
     if (st == ARR_EINVAL)
         return fail(c, st, "eig_set_stencil: n != nx*ny*nz, or a row of A is unsorted / has a column outside the "
                            "3x3x3 neighbourhood of its grid point");

@@ -89,6 +89,9 @@ struct StencilState {
     // the plane below / above is a ghost plane (the block's rows n .. n + (gz_lo + gz_hi) nx ny,
     // lower plane first: the ghost rows sorted by global id)
     int gz_lo = 0, gz_hi = 0;
+    // the plan's boundary tiles (rows with a ghost column) are exactly the slab's first / last
+    // plane: those rows may run on the CSR kernels after the exchange (api.cu spmm_x)
+    bool bnd_is_ends = false;
 };
 // One launch of the stencil kernel (kernel parameter, __grid_constant__).
 struct StencilLaunch {
@@ -108,6 +111,7 @@ struct StencilLaunch {
     int nx, ny, nz;
     int gz_lo, gz_hi;  // ghost planes below / above the nz owned planes (StencilState)
     int z0, z1;        // output planes of this launch (z-chunks of [z0, z1))
+    int zstep;         // distance of consecutive z-chunks' first planes (Lz; z1 - 1 - z0 for the two end planes)
     int Px, Py, Lz, npx, npy, nzc, npan, pwv, NS;
     int box_x, box_y, hx, hy;
     int pm;  // 1: panel-major work-item order (stencil_kernels.cu decode_item)
@@ -261,8 +265,9 @@ int cached_occupancy(LaunchCache &lc, Kern kern, int threads, size_t smem) {
 // Returns the grid size used (number of partial rows written if partials != nullptr).
 int launch_spmm(arr_ctx *c, const SpmmArgs &a);
 // stencil path (stencil_kernels.cu): -1 when it does not apply to this launch
-// z0 / z1: the output planes of this launch (z1 < 0: all owned planes)
-int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0 = 0, int z1 = -1);
+// z0 / z1: the output planes of this launch (z1 < 0: all owned planes); ends_only: just the
+// planes z0 and z1 - 1 (a z-slab's two planes next to the ghost planes, one launch)
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0 = 0, int z1 = -1, bool ends_only = false);
 arr_status stencil_setup(arr_ctx *c, int64_t nx, int64_t ny, int64_t nz, int gz_lo = 0, int gz_hi = 0);
 void stencil_release(arr_ctx *c);
 // out[col] = sqrt(sum_b partials[b*w + col]) ; if rel != nullptr: out /= max(1,|rel|)

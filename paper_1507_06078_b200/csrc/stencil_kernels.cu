@@ -203,7 +203,7 @@ __device__ __forceinline__ Item decode_item(const StencilLaunch &P, int64_t it) 
     r.y0 = py * P.Py;
     r.pxe = min(P.Px, P.nx - r.x0);
     r.pye = min(P.Py, P.ny - r.y0);
-    r.zc0 = P.z0 + zc * P.Lz;
+    r.zc0 = P.z0 + zc * P.zstep;
     r.zc1 = min(P.z1, r.zc0 + P.Lz);
     return r;
 }
@@ -749,12 +749,13 @@ bool encode_diag(CUtensorMap *m, const double *base, int64_t nx, int64_t ny, int
 // Cost model: L2 -> SM bytes per output row = staged rows per patch
 // row + the streamed operands, plus the DIA row once per panel, divided by the
 // useful fraction of the launch (ragged patches, last wave of work items).
-bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, StencilLaunch &L, int z0, int z1) {
+bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, StencilLaunch &L, int z0, int z1,
+                  bool ends_only) {
     const StencilState &S = c->st;
     if (!S.on || w % 2 != 0) return false;
     const int wv = w / 2;
-    const int nzr = z1 - z0;  // output planes of this launch
-    if (nzr < 1) return false;
+    const int nzr = ends_only ? 2 : z1 - z0;  // output planes of this launch
+    if (nzr < 1 || (ends_only && z1 - z0 < 2)) return false;
     const int items_max = kStThreads - 32;  // one output vector per consumer thread (IPT = 2 spills)
     // one CTA per SM at 1024 threads; two at 512 (each up to half the SM's shared memory)
     const size_t smem_max = (size_t)S.smem_optin - 256;
@@ -792,12 +793,16 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
                 if (dyn && st_nzc() > 0) nzc = std::min<int>(st_nzc(), nzr);
                 else
                     while ((int64_t)npx * npy * npan * nzc < (dyn ? 4 : 12) * G && nzr / (nzc + 1) >= 8) ++nzc;
+                if (ends_only) nzc = 2;  // two single-plane chunks: z0 and z1 - 1
                 const int Lz = (nzr + nzc - 1) / nzc;
                 nzc = (nzr + Lz - 1) / Lz;
                 const int64_t items = (int64_t)npx * npy * npan * nzc;
                 const double waves = (double)items / (double)((G / npan) * npan);
                 const double tail = waves / std::ceil(waves);
-                const double warm = (double)(Lz + (nzc > 1 ? 1 : 0)) / Lz;
+                // planes staged per chunk beyond its Lz outputs (a sub-range of a slab, or a slab
+                // with ghost planes, stages the plane below and above as well)
+                const int extra = (ends_only || z1 - z0 < S.nz) ? 2 : (nzc > 1 ? 1 : 0) + S.gz_lo + S.gz_hi;
+                const double warm = (double)(Lz + extra) / Lz;
                 const double rowbytes = 16.0 * wv;
                 const double colfill = (double)wv / ((double)npan * pwv);  // OOB columns of the last panel
                 const double abytes = S.vmode == 0 ? 8.0 * S.Kpad : (S.vmode == 1 ? 8.0 : 0.0);  // A per row
@@ -823,6 +828,7 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
     L.nx = (int)S.nx; L.ny = (int)S.ny; L.nz = (int)S.nz;
     L.gz_lo = S.gz_lo; L.gz_hi = S.gz_hi;
     L.z0 = z0; L.z1 = z1;
+    L.zstep = ends_only ? z1 - 1 - z0 : L.Lz;
     L.hx = hx; L.hy = hy;
     L.K = S.K;
     L.Kpad = S.Kpad;
@@ -835,7 +841,7 @@ bool stencil_plan(const arr_ctx *c, int w, bool has_prev, bool has_x, bool dyn, 
 }
 
 // Fused SpMM through the stencil path; -1 when it does not apply to this launch.
-int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0, int z1) {
+int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0, int z1, bool ends_only) {
     if (!c->st.on || a.colshift || a.n != c->A.n || a.w % 2 != 0) return -1;
     if (z1 < 0) z1 = (int)c->st.nz;
     if (z0 < 0 || z1 > c->st.nz || z0 >= z1) return -1;
@@ -843,7 +849,7 @@ int launch_spmm_stencil(arr_ctx *c, const SpmmArgs &a, int z0, int z1) {
     if (a.Yprev && !al16(a.Yprev, a.ld_prev)) return -1;
     if (a.Xa && !al16(a.Xa, a.ld_xa)) return -1;
     StencilLaunch L{};
-    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L, z0, z1)) return -1;
+    if (!stencil_plan(c, a.w, a.Yprev != nullptr, a.Xa != nullptr, !a.partials && st_dyn(), L, z0, z1, ends_only)) return -1;
     L.Yin = a.Yin; L.ld_in = a.ld_in;
     L.Yprev = a.Yprev; L.ld_prev = a.ld_prev;
     L.Yout = a.Yout; L.ld_out = a.ld_out;

@@ -3,7 +3,11 @@
 mkdir -p gpurun_out/r02l
 timeout 1500 python -m pytest tests/test_gpu_dist.py tests/test_gpu_stencil.py -x -q -m gpu -rs > gpurun_out/r02l/pytest_dist_stencil.log 2>&1
 echo "pytest exit $?" >> gpurun_out/r02l/pytest_dist_stencil.log
-tail -15 gpurun_out/r02l/pytest_dist_stencil.log
-# cfg3 on 2 and 4 in-process ranks? (not a bench: correctness + per-rank kernel timing of a slab)
-ARRABIT_ST_VERBOSE=1 timeout 600 python scripts/slab_filter_bench.py > gpurun_out/r02l/slab_filter_bench.log 2>&1
-tail -20 gpurun_out/r02l/slab_filter_bench.log
+ARRABIT_SLAB_BND=stencil timeout 1500 python -m pytest tests/test_gpu_dist.py -x -q -m gpu -k stencil > gpurun_out/r02l/pytest_dist_stencil_ends.log 2>&1
+echo "pytest exit $?" >> gpurun_out/r02l/pytest_dist_stencil_ends.log
+tail -5 gpurun_out/r02l/pytest_dist_stencil.log gpurun_out/r02l/pytest_dist_stencil_ends.log
+# cfg3 slabs of G in-process ranks at full size: bitwise check + wall time of all ranks together
+for m in csr stencil; do
+  ARRABIT_SLAB_BND=$m timeout 600 python scripts/slab_filter_bench.py 3 > gpurun_out/r02l/slab_filter_bench_cfg3_$m.log 2>&1
+  tail -4 gpurun_out/r02l/slab_filter_bench_cfg3_$m.log
+done
