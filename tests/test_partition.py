@@ -196,3 +196,42 @@ def test_yband_interior_order_same_rows(G, band):
         if len(rows_q):
             yline = ((rows_q + q.row_begin) // N) % N
             assert (np.diff(yline // band) >= 0).all(), "band-major order"
+
+
+@pytest.mark.parametrize("kind,yband", [("lap2d", None), ("lap3dV", None), ("st27", None), ("lap3dV", (9, 9, 3))])
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_zslab_plans_have_whole_ghost_planes_lower_first(kind, yband, G):
+    """What eig_set_stencil on a row-partitioned context relies on (include/arrabit.h): on
+    a bounds_planes partition of a stencil operator every rank owns whole planes, its ghost
+    rows are exactly the plane below (from lower ranks, first in the block) and / or the
+    plane above, and the plan's boundary tiles are exactly the slab's first / last plane
+    (the rows the stencil path hands to the CSR kernels after the exchange)."""
+    mk, planes = SMALL[kind]
+    A = mk()
+    nplanes, nxy = planes
+    ps = pt.plans(A, pt.bounds_planes(nplanes, nxy, G), yband=yband)
+    for p in ps:
+        assert p.n_own % nxy == 0 and p.n_own >= nxy
+        lo = p.rank > 0
+        hi = p.rank < G - 1
+        want = []
+        if lo:
+            want.append(np.arange(p.row_begin - nxy, p.row_begin))
+        if hi:
+            want.append(np.arange(p.row_begin + p.n_own, p.row_begin + p.n_own + nxy))
+        np.testing.assert_array_equal(p.ghost_global, np.concatenate(want) if want else np.empty(0, dtype=np.int64))
+        # peers in rank order: the lower neighbour's rows are received first
+        cnt = np.diff(p.recv_off)
+        assert [int(q) for q in p.peer] == sorted(int(q) for q in p.peer)
+        assert int(cnt[p.peer < p.rank].sum()) == (nxy if lo else 0)
+        assert int(cnt[p.peer > p.rank].sum()) == (nxy if hi else 0)
+        bnd = np.zeros(p.n_own, dtype=bool)
+        for r0, ln in zip(p.bnd_row0, p.bnd_len):
+            assert not bnd[r0:r0 + ln].any()
+            bnd[r0:r0 + ln] = True
+        ends = np.zeros(p.n_own, dtype=bool)
+        if lo:
+            ends[:nxy] = True
+        if hi:
+            ends[p.n_own - nxy:] = True
+        np.testing.assert_array_equal(bnd, ends)
