@@ -234,6 +234,14 @@ def orthonormalize(Z: np.ndarray):
     return Q[:, :r], r
 
 
+# Eigen-decomposition of the small projected matrix H (Alg. RR step 3): the
+# oracle's own cyclic Jacobi (dense.jacobi_eigh) everywhere, except where a caller sets
+# EIGH = "lapack" (numpy.linalg.eigh as a library step): only scripts/oracle_golden.py does,
+# for the m = 1650 problems of the full cfg3 solve, where the numpy Jacobi takes ~25 minutes
+# per ARR.  The two are cross-checked in tests/test_oracle_own_dense.py.
+EIGH = "jacobi"
+
+
 def _ritz(A, U: np.ndarray, H: np.ndarray | None = None):
     """Alg. RR steps 2-4 on an orthonormal U: H = U^T A U (symmetrised),
     H = V Sigma V^T by cyclic Jacobi (dense.jacobi_eigh), Ritz values descending,
@@ -241,7 +249,7 @@ def _ritz(A, U: np.ndarray, H: np.ndarray | None = None):
     if H is None:
         H = U.T @ spmm(A, U) if U.shape[1] > 0 else np.zeros((0, 0))
     H = 0.5 * (H + H.T)
-    mu, V = dense.jacobi_eigh(H)
+    mu, V = dense.jacobi_eigh(H) if EIGH == "jacobi" else np.linalg.eigh(H)
     order = np.argsort(-mu, kind="stable")
     return mu[order], V[:, order]
 

@@ -3,7 +3,7 @@ synth/; no CUDA path).  SURVEY §8c-6: cfg3 by the oracle's orthonormalise-then-
 ARR (the paper-literal pivoted QR of the n x 1650 Krylov block takes hours); cfg4 on
 the same generator at n = 4e5, k = 100 (the full n = 4e6 solve needs ~100 GB).
 
-    python scripts/oracle_golden.py --config 3 --arr cgs2
+    python scripts/oracle_golden.py --config 3 --arr cgs2 --eigh lapack
     python scripts/oracle_golden.py --config 4 --n 400000 --k 100 --arr qr
 """
 import argparse
@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="generator size override (zipf: n; grids: edge)")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--arr", default="qr", choices=["qr", "cgs2"])
+    ap.add_argument("--eigh", default="jacobi", choices=["jacobi", "lapack"],
+                    help="the projected eigenproblem: the oracle's cyclic Jacobi, or LAPACK as a library step "
+                         "(cfg3: m = 1650, Jacobi in numpy takes ~25 min per ARR)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     spec = configs.CONFIGS[args.config]
@@ -37,13 +40,15 @@ def main():
         tag += f"_n{spec.n}_k{spec.k}"
     A, spec = configs.build_config(spec)
     X0 = configs.starting_block(spec)
+    import oracle.core as oc
+    oc.EIGH = args.eigh
     t0 = time.time()
     r = oracle.solve(A, spec.k, spec.d, spec.p, X0, tol=spec.tol, maxit=spec.maxit, s_max=spec.s_max,
                      w=spec.w, arr_method=args.arr)
     out = {
         "source": "scripts/oracle_golden.py (oracle/ only)",
         "config": spec.name, "n": int(A.n), "nnz": int(A.nnz), "k": spec.k, "w": spec.w, "d": spec.d, "p": spec.p,
-        "seed": spec.seed, "tol": spec.tol, "arr_method": args.arr, "range_digits": float(oracle.RANGE_DIGITS),
+        "seed": spec.seed, "tol": spec.tol, "arr_method": args.arr, "eigh": args.eigh, "range_digits": float(oracle.RANGE_DIGITS),
         "converged": bool(r.converged), "outer": r.outer, "sweeps": r.sweeps,
         "max_residual": float(r.res.max()), "eigenvalues": [float(x) for x in r.mu],
         "residuals": [float(x) for x in r.res], "seconds": time.time() - t0,

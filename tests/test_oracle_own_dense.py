@@ -220,3 +220,26 @@ def test_rcond_inner_rule_and_exits():
     assert r.exit_rule in (1, 2, 3)
     if r.exit_rule == 3:  # (iii): max res < (1 + 9h/k) tol
         assert r.res.max() < 10 * 1e-10
+
+
+def test_ritz_lapack_switch_equals_jacobi():
+    """oracle.core.EIGH = "lapack" (the cfg3 golden's m = 1650 projected problems,
+    scripts/oracle_golden.py --eigh lapack) gives the Ritz values and the Ritz subspaces of
+    the default cyclic Jacobi (Alg. RR step 3)."""
+    import oracle.core as oc
+    import synth
+    A = synth.laplacian_3d_potential(7, 2)
+    X = synth.gaussian_block(A.n, 12, 3)
+    assert oc.EIGH == "jacobi"
+    mu_j, Y_j, r_j = oc.arr(A, X, 2, method="cgs2")
+    try:
+        oc.EIGH = "lapack"
+        mu_l, Y_l, r_l = oc.arr(A, X, 2, method="cgs2")
+    finally:
+        oc.EIGH = "jacobi"
+    assert r_j == r_l
+    assert np.max(np.abs(mu_j - mu_l)) <= 1e-13 * np.max(np.abs(mu_j))
+    # same residuals of the kept pairs (vectors agree up to sign / rotations inside clusters)
+    rj = oc.residuals(A, Y_j, mu_j[:12])
+    rl = oc.residuals(A, Y_l, mu_l[:12])
+    assert np.max(np.abs(rj - rl)) <= 1e-12
