@@ -310,3 +310,38 @@ def test_dist_stencil_solve_matches_dense(arr, kind, G):
     assert np.max(np.abs(ev - lam) / np.maximum(1, np.abs(lam))) <= 1e-10
     Y = np.vstack([x[3] for x in res])
     assert oracle.residuals(A, Y, ev).max() <= spec.tol * 1.01
+
+
+def test_dist_stencil_odd_width_falls_back_to_csr(arr):
+    """An odd block width is outside the stencil kernel's reach (16-byte column vectors): a
+    z-slab context with the stencil declared runs the CSR tiles for that launch (exchange
+    started once, ended once) and stays bitwise the one-GPU result."""
+    A = synth.laplacian_3d_potential(13, 2)
+    k, d, G = 23, 5, 3
+    X0 = synth.gaussian_block(A.n, k, 5)
+    a = oracle.gershgorin_lower(A)
+    b = a + 6.0
+    c1 = arr.eig_init(arr.to_device_csr(A), k, 1, d)
+    c1.eig_set_interval(a, b)
+    X1 = torch.from_numpy(X0).cuda()
+    c1.filter_step(X1, normalize=False)
+    ref = X1.cpu().numpy()
+    c1.close()
+    ps, comms, ctx_of = make_rank(arr, A, G, ("planes", 13, 169), k, 1, d)
+
+    def work(r):
+        ctx, s = ctx_of(r)
+        with torch.cuda.stream(s):
+            ctx.eig_set_stencil(13, 13, ps[r].n_own // 169)
+            ctx.eig_set_interval(a, b)
+            Xr = to_rank_block(X0, ps[r])
+            ctx.filter_step(Xr, normalize=False)
+            out = Xr[:ps[r].n_own].cpu().numpy(), ctx.last_spmm_kernel
+        ctx.close()
+        return out
+
+    res = run_ranks(G, work)
+    for c in comms:
+        c.close()
+    assert all("CSR" in x[1] for x in res), [x[1] for x in res]
+    assert np.array_equal(np.vstack([x[0] for x in res]), ref)
