@@ -18,7 +18,9 @@ cfg2 solve (BASELINE.json configs[1]) is reported beside it as `secondary`.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 N>1 (torchrun): the config is row-partitioned over the ranks (z-slabs / balanced
 blocks; halo or all-gather exchange before every SpMM and Gram allreduce over NCCL
-inside libarrabit; strong scaling); --replicas runs independent copies instead.
+inside libarrabit; strong scaling; on the grids every rank declares its z-slab and runs
+the stencil kernel with the neighbouring planes as ghost planes); --replicas runs
+independent copies instead.
 """
 from __future__ import annotations
 
@@ -709,7 +711,7 @@ def run_ours(args):
         par = ("1 GPU" if world == 1 else
                (f"column split over {world} GPUs (A replicated, column-local filter, ARR on a balanced row "
                 f"partition; NCCL all-to-all transposes + halo/all-gather + allreduce)" if colsplit else
-                f"row partition over {world} GPUs ({_partition_spec(spec)[0]}" + (", interior tiles in y-band order" if spec.kind in ("lap3dV", "st27") else "") + "), NCCL halo/all-gather + allreduce"
+                f"row partition over {world} GPUs ({_partition_spec(spec)[0]}; SpMM path: {r['path']}" + ("; CSR interior tiles in y-band order" if spec.kind in ("lap3dV", "st27") else "") + "), NCCL halo/all-gather + allreduce"
                 if partitioned else f"{world} independent replicas (no collective)"))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
